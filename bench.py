@@ -1,0 +1,393 @@
+"""Benchmark of the exit-measure hot path (BASELINE.json metric: walks/s and
+walk-steps/s for A, % of the FP32 issue roofline).
+
+One "step" = one pass of the hot path over the whole workload: every walk of
+every pole run to the eps-shell and binned into the (n_poles, n0 + n1) int64
+count rows (the reference's run_accumulate, S/backend.py:147-199, S/ =
+/root/reference/pkg/src/exitmeasure/), plus -- at N > 1 GPUs -- the NCCL
+all-gather of the count rows to every rank.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+                    [--precision fp32|ref64] [--chain max|woe]
+    python bench.py --impl reference ...   # the reference's own CPU path
+
+Workload at N=1: BASELINE configs[1] (cfg2, the unit square with
+K=[[2,.8],[.8,1]], 256 poles x 1e5 walks, eps 1e-5, 512 edge bins).
+Multi-GPU: poles are sharded cyclically over ranks (pole i -> rank i mod N,
+RNG keyed by the global pole id), so per-GPU work shrinks as N grows
+("scaling": "strong", total work fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# Algorithmic FP32 lane-ops per walk step of the IMPLEMENTED chain, counted
+# with SURVEY.md §8(d)'s convention (add/sub/mul/fma/min/max/compare = 1;
+# sqrt/rsqrt/div/sin/cos are XU ops, counted separately; RNG separately).
+# Derivation per term is in DESIGN.md ("F_step of the implemented kernels").
+F_STEP = {
+    # (cfg, chain): (fp32 ops, xu ops)
+    (1, "woe"): (15, 3), (1, "max"): (15, 3),
+    (2, "woe"): (19, 2), (2, "max"): (23, 2),
+    (3, "woe"): (27, 4), (3, "max"): (49, 8),
+    (4, "woe"): (32, 4), (4, "max"): (50, 6),
+    (5, "woe"): (35, 4), (5, "max"): (45, 4),
+}
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled on a thread during the timed
+    region (the recipe's clocks line)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            idx = device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[device])
+                except ValueError:
+                    idx = device
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self._nv = None
+            self.error = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((mhz, reasons))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mhz = sorted(s[0] for s in self.samples)
+        active = set()
+        for _, r in self.samples:
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    active.add(name)
+        return {"sm_mhz": float(mhz[len(mhz) // 2]), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(active), "samples": len(self.samples)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
+    """The reference's own CPU path (oracle/_ref, the unmodified exitmeasure
+    package with its compiled Cython kernel) on a bounded sample of the
+    workload: all poles x n_sample walks.  Falls back to the C restatement
+    (oracle/em_oracle.c) if oracle/_ref is absent."""
+    ref = ROOT / "oracle" / "_ref"
+    sub = cfg.subset(None, n_sample)
+    if (ref / "exitmeasure").exists():
+        sys.path.insert(0, str(ref))
+        from exitmeasure import backend as rb
+        from exitmeasure.geometry import Ball, Box, BoundaryPointSet, make_domain
+
+        from paper_2409_03686_b200 import backend as B
+
+        geom = B.pack_geometry(sub.dom)
+        if sub.index in (1, 2, 4):
+            outer = (Ball(np.zeros(sub.d), 1.0) if sub.index in (1, 4)
+                     else Box(np.array([0.5, 0.5]), 0.5))
+            dom = make_domain(outer, gamma0=())
+            pts = np.ascontiguousarray(sub.fam1.points)
+            s1 = rb.pack_side(BoundaryPointSet(pts, np.zeros(len(pts), int),
+                                               np.arange(len(pts), dtype=float), ()),
+                              sub.d, sub.eps)
+            s0 = rb.pack_side(None, sub.d, sub.eps)
+        elif sub.index == 3:
+            from exitmeasure.geometry import catalog, side_points
+
+            dom = catalog("annulus")
+            s0 = rb.pack_side(side_points(dom, "gamma0", [512]), 2, sub.eps)
+            s1 = rb.pack_side(side_points(dom, "gamma1", [512]), 2, sub.eps)
+        else:
+            dom = None
+        if dom is not None:
+            t0 = time.perf_counter()
+            r = rb.run_accumulate(dom, sub.kt.k_sqrt, sub.poles, sub.seed, sub.eps, 10**6,
+                                  n_sample, s0, s1, threads=threads)
+            dt = time.perf_counter() - t0
+            walks = sub.n_poles * n_sample
+            return (walks / dt, float(r.steps_sum.sum()) / dt, "reference", dt,
+                    float(r.steps_sum.sum()) / walks)
+        del geom
+    from oracle import oracle as O
+
+    from paper_2409_03686_b200 import backend as B
+
+    geom = B.pack_geometry(sub.dom)
+    s0 = B.pack_side(sub.fam0, sub.d, sub.eps)
+    s1 = B.pack_side(sub.fam1, sub.d, sub.eps)
+    t0 = time.perf_counter()
+    raw0, raw1, ss, *_ = O.run_accumulate_packed(
+        geom.gi, geom.gf, geom.comp_side, sub.kt.k_sqrt, sub.poles, sub.seed, sub.eps, 10**6,
+        n_sample, (s0.anchors, s0.blk, s0.blkf), (s1.anchors, s1.blk, s1.blkf), threads=threads)
+    dt = time.perf_counter() - t0
+    walks = sub.n_poles * n_sample
+    return walks / dt, float(ss.sum()) / dt, "port", dt, float(ss.sum()) / walks
+
+
+REF_SAMPLE = {1: 10_000, 2: 4096, 3: 256, 4: 64, 5: 16}
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(args.config)
+    threads = os.cpu_count() or 1
+    n_sample = args.ref_sample or REF_SAMPLE[cfg.index]
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v = cpu_reference_walks_per_s(cfg, n_sample, threads)
+        if i >= args.warmup:
+            vals.append(v)
+        info = v
+    wps = float(np.median([v[0] for v in vals]))
+    sps = float(np.median([v[1] for v in vals]))
+    ms = float(np.median([v[3] for v in vals])) * 1e3
+    sample = (f"{cfg.name}: all {cfg.n_poles} poles x {n_sample} walks/pole "
+              f"({cfg.n_poles * n_sample:.3g} walks) per step, threads={threads}")
+    line = {
+        "impl": "reference", "metric": "walks/s", "value": wps, "unit": "walks/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "steps_per_s": sps, "mean_steps_per_walk": info[4],
+        "config": {"workload": cfg.name, "poles": cfg.n_poles, "walks_per_pole": n_sample,
+                   "eps": cfg.eps},
+        "cpu_baseline": {"value": wps, "unit": "walks/s", "cores": threads, "kind": info[2],
+                         "sample": sample},
+        "e2e": {"value": wps, "unit": "walks/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = _dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local if world > 1 else 0
+    torch.cuda.set_device(device)
+    from paper_2409_03686_b200 import _native, backend, configs
+
+    cfg = configs.get(args.config)
+    if args.n_rep:
+        cfg = cfg.subset(None, args.n_rep)
+    ids = np.arange(rank, cfg.n_poles, world)  # cyclic row shard
+    geom = backend.pack_geometry(cfg.dom)
+    s0 = backend.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = backend.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    plan = backend.Plan(geom, cfg.kt.k_sqrt, cfg.poles[ids], cfg.eps, 10**6, s0, s1,
+                        precision=args.precision, chain=args.chain, device=device,
+                        pole_ids=ids)
+    row = plan.n0 + plan.n1
+    m_local = len(ids)
+    m_pad = -(-cfg.n_poles // world)
+    counts = torch.zeros((m_pad, row), dtype=torch.int64, device="cuda")
+    stats = torch.zeros((3, m_pad), dtype=torch.int64, device="cuda")
+    gathered = torch.zeros((world * m_pad, row), dtype=torch.int64, device="cuda") if world > 1 else None
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def one_step():
+        plan.run_device(cfg.seed, cfg.n_rep, counts.data_ptr(), stats.data_ptr(),
+                        stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, counts)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        one_step()
+    torch.cuda.synchronize()
+    steps_per_run = int(stats[0, :m_local].sum().item())
+    ffma_peak, _ = _native.fp32_peak(device)
+    info = _native.device_info(device)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    with ClockSampler(device) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            one_step()
+            ev[i][1].record(stream)
+            launches += plan.last_launches()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        st = torch.tensor([steps_per_run], device="cuda", dtype=torch.int64)
+        dist.all_reduce(st)
+        steps_total_run = int(st.item())
+    else:
+        steps_total_run = steps_per_run
+    walks = cfg.total_walks * args.steps
+    value = walks / (tot_ms * 1e-3)
+    steps_per_s = steps_total_run * args.steps / (tot_ms * 1e-3)
+    clocks = clk.summary()
+
+    # roofline: FP32 issue bound of this kernel on this GPU
+    fp32, xu = F_STEP[(cfg.index, plan.chain if plan.precision == "fp32" else "woe")]
+    per_gpu_steps_s = steps_per_s / world
+    achieved = fp32 * per_gpu_steps_s / 1e12
+    clk_mhz = clocks["sm_mhz"] or (info["clock_khz"] / 1e3)
+    peak_nominal = info["sm_count"] * 128 * clk_mhz * 1e6 / 1e12
+    peak_ffma = ffma_peak / 1e12
+
+    # e2e through the public API: host numpy in, host numpy out, one call
+    e2e_val = None
+    h2d = d2h = 0
+    if rank == 0:
+        sub_ids = ids
+        e2e_times = []
+        for i in range(max(2, min(args.steps, 5))):
+            t0 = time.perf_counter()
+            r = backend.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles[sub_ids], cfg.seed,
+                                       cfg.eps, 10**6, cfg.n_rep, s0, s1,
+                                       precision=plan.precision, chain=plan.chain,
+                                       device=device, pole_ids=sub_ids)
+            e2e_times.append(time.perf_counter() - t0)
+        e2e_val = len(sub_ids) * cfg.n_rep * world / float(np.median(e2e_times[1:]))
+        h2d = (cfg.poles[sub_ids].nbytes + s0.anchors.nbytes + s1.anchors.nbytes
+               + geom.gi.nbytes + geom.gf.nbytes + cfg.kt.k_sqrt.nbytes)
+        d2h = r.counts.nbytes + 3 * 8 * len(sub_ids)
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            n_sample = REF_SAMPLE[cfg.index]
+            c = cpu_reference_walks_per_s(cfg, n_sample, os.cpu_count() or 1)
+            cpu = {"value": c[0], "unit": "walks/s", "cores": os.cpu_count() or 1,
+                   "kind": c[2],
+                   "sample": f"{cfg.name}: all {cfg.n_poles} poles x {n_sample} walks/pole "
+                             f"({c[3]:.1f} s), steps/s {c[1]:.3g}"}
+        line = {
+            "metric": "walks/s", "value": value, "unit": "walks/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if plan.precision == "fp32" else "f64", "data": "synthetic",
+            "steps_per_s": steps_per_s,
+            "mean_steps_per_walk": steps_total_run / cfg.total_walks,
+            "config": {"workload": f"{cfg.name}: {cfg.n_poles} poles x {cfg.n_rep:.0e} walks, "
+                                   f"eps {cfg.eps:g}, {plan.n0 + plan.n1} bins",
+                       "precision": plan.precision, "chain": plan.chain,
+                       "parallelism": f"rows cyclic over {world} GPU(s)",
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "counts": "int64 (n_poles, n0+n1) rows + step stats"},
+            "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
+                         "unit": "Top/s", "frac": achieved / peak_nominal,
+                         "traffic": None,
+                         "f_step": {"fp32": fp32, "xu": xu},
+                         "peak_note": f"{info['sm_count']} SMs x 128 FP32 lanes x median SM "
+                                      f"clock under load {clk_mhz:.0f} MHz (MEASURED_PEAKS.json "
+                                      "has no FP32 figure)",
+                         "peak_measured_ffma": peak_ffma,
+                         "frac_of_measured_ffma": achieved / peak_ffma,
+                         "frac_at_max_clock": achieved / (info["sm_count"] * 128 *
+                                                          (clocks["sm_max_mhz"] or 1965) * 1e-6)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "walks/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": "paper_2409_03686_b200.backend.run_accumulate (host numpy in/out)"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--chain", default=None)
+    ap.add_argument("--n-rep", type=int, default=None, help="override walks per pole")
+    ap.add_argument("--ref-sample", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,199 @@
+/*
+ * exitmeasure_b200.h -- C ABI of the B200-native exit-measure library
+ * (libexitmeasure_b200.so).  Plain pointers and sizes only; host buffers are
+ * owned by the caller, device buffers by the library.
+ *
+ * Reference interface each entry point replaces (S/ = /root/reference/pkg/
+ * src/exitmeasure/; the reference binds its kernel through Cython, the
+ * ctypes binding that replaces it is paper_2409_03686_b200/_native.py and is
+ * shown in INTEGRATION.md):
+ *
+ *   em_walk_exits_chunk   <- _kernel.walk_exits_chunk   S/_kernel.pyx:376-411
+ *   em_accumulate_chunk   <- _kernel.accumulate_chunk   S/_kernel.pyx:414-464
+ *   em_plan_* / em_run_accumulate
+ *                         <- backend.run_accumulate     S/backend.py:147-199
+ *                            (one launch for all (pole, replicate) walks
+ *                            instead of a thread pool over 8192-walk chunks)
+ *   em_run_exits          <- backend.run_exits          S/backend.py:202-227
+ *
+ * Two arithmetic paths sit behind the same entry points:
+ *   EM_PREC_REF64 -- bit-exact FP64 mirror of the reference kernel: the same
+ *                    Philox4x64-10 streams (key (seed,0), counter
+ *                    (draw,0,replicate,pole)), Marsaglia directions, operand
+ *                    order and lexicographic binning, so counts equal the
+ *                    reference's exactly.
+ *   EM_PREC_FP32  -- the production kernel: Philox4x32-10 streams keyed by
+ *                    (seed, pole, replicate), angle-based directions, FP32
+ *                    walk state, persistent lane refill and closed-form /
+ *                    grid-accelerated binning.  Statistically equivalent to
+ *                    the reference (same exit law), not bit-identical.
+ *
+ * Return codes: EM_OK, EM_BUDGET (some walk exceeded max_steps; the
+ * lexicographically first (pole, replicate) is reported, outputs are then
+ * meaningless -- the reference's WalkBudgetError contract, S/backend.py:
+ * 189-192), or a negative error with a message from em_last_error().
+ * All entry points are reentrant: each calling host thread gets its own
+ * stream and workspace (the reference's thread-pool contract,
+ * S/backend.py:159-178).
+ */
+#ifndef EXITMEASURE_B200_H
+#define EXITMEASURE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EM_ABI_VERSION 1
+
+#define EM_OK 0
+#define EM_BUDGET 1
+#define EM_ERR_INVALID (-1)
+#define EM_ERR_CUDA (-2)
+#define EM_ERR_UNSUPPORTED (-3)
+#define EM_ERR_NOMEM (-4)
+
+#define EM_PREC_REF64 0
+#define EM_PREC_FP32 1
+
+/* EM_CHAIN_WOE: the reference chain x <- x + sd(x) K^{1/2} u
+ *   (S/_kernel.pyx:185-196).
+ * EM_CHAIN_MAX: x <- x + r(x) K^{1/2} u with r(x) >= sd(x) a certified lower
+ *   bound of the largest K^{1/2}-ellipsoid inscribed in the domain (exact for
+ *   faces, closed-form bounds for balls/holes); same stopping rule sd <= eps,
+ *   same exit law, fewer steps.  FP32 only. */
+#define EM_CHAIN_WOE 0
+#define EM_CHAIN_MAX 1
+
+#define EM_MAX_HOLES 16
+
+/* Packed geometry: the reference's GeomPack (S/backend.py:50-54,71-83).
+ *   gi = [d, outer_kind (0 ball, 1 box), n_holes (, n_notch)]
+ *   gf = [outer_center(d), R|h, (hole_center(d), r)*, (nx, ny) if n_notch]
+ * The optional 4th gi word is this library's extension for cfg5's L-box: a
+ * quadrant prism {x >= nx, y >= ny} removed from a 3D box, boundary
+ * component 1 + n_holes. */
+typedef struct {
+  const int64_t* gi;
+  int64_t gi_len;
+  const double* gf;
+  int64_t gf_len;
+  const int8_t* comp_side; /* side (0 gamma0 / 1 gamma1) per component */
+  int64_t n_comp;
+  const double* ksqrt; /* d x d row-major, normalised (lambda_max = 1) */
+} em_geometry;
+
+/* One side's weight family: the reference's SidePack (S/backend.py:57-68).
+ * blk rows (kind, start, count): kind 0 generic (brute force / grid),
+ * 1 uniform circle, 2 uniform square.  blkf rows (cx, cy, cz, radius|h).
+ * blk_phase (NULL = all 0, the reference layout) shifts uniform anchors to
+ * spacing * (k + phase) along the curve. */
+typedef struct {
+  const double* anchors; /* (n_anchors, d) */
+  int64_t n_anchors;
+  const int64_t* blk;
+  const double* blkf;
+  int64_t n_blk;
+  int32_t wkind; /* 0 voronoi (1 idw: EM_ERR_UNSUPPORTED in this ABI version) */
+  int32_t idw_power;
+  const double* idw_radii;
+  const double* blk_phase;
+} em_side;
+
+typedef struct {
+  int32_t precision; /* EM_PREC_* */
+  int32_t chain;     /* EM_CHAIN_* (EM_PREC_REF64 requires EM_CHAIN_WOE) */
+  int32_t device;    /* CUDA ordinal */
+  int32_t block;     /* threads per block, 0 = library default */
+  int32_t grid;      /* persistent blocks, 0 = library default (SMs x occupancy) */
+  int32_t reserved;
+} em_options;
+
+/* Per-run outputs.  Host pointers for em_plan_run / em_run_accumulate,
+ * device pointers for em_plan_run_device.  counts is (n_poles, n0 + n1)
+ * int64, side-0 columns first. */
+typedef struct {
+  int64_t* counts;
+  int64_t* steps_sum; /* (n_poles,) */
+  int64_t* steps_sq;
+  int64_t* steps_max;
+  int64_t err_pole; /* set when EM_BUDGET (pole position in the plan) */
+  int64_t err_rep;
+} em_outputs;
+
+typedef struct em_plan em_plan;
+
+int em_abi_version(void);
+const char* em_last_error(void);
+int em_device_count(void);
+/* sm_count, max SM clock (kHz), compute capability major/minor */
+int em_device_info(int device, int* sm_count, int* clock_khz, int* cc_major, int* cc_minor);
+
+/* Drop-in for _kernel.walk_exits_chunk (S/_kernel.pyx:376-411), REF64.
+ * x_out (n, d), steps_out (n,), comp_out (n,); *err_rep = first failing
+ * replicate or -1. */
+int em_walk_exits_chunk(const em_geometry* g, const double* pole_xy, int64_t pole_index,
+                        int64_t rep_start, int64_t rep_end, uint64_t seed, double eps,
+                        int64_t max_steps, int device, double* x_out, int64_t* steps_out,
+                        int64_t* comp_out, int64_t* err_rep);
+
+/* Drop-in for _kernel.accumulate_chunk (S/_kernel.pyx:414-464), REF64.
+ * out0/out1 are accumulated in place (+=); stats = (steps_sum, steps_sq,
+ * steps_max, idw_fallbacks); *err_rep = first failing replicate or -1. */
+int em_accumulate_chunk(const em_geometry* g, const double* pole_xy, int64_t pole_index,
+                        int64_t rep_start, int64_t rep_end, uint64_t seed, double eps,
+                        int64_t max_steps, const em_side* s0, const em_side* s1, int device,
+                        double* out0, double* out1, int64_t* stats, int64_t* err_rep);
+
+/* Batched path (S/backend.py:147-199).  A plan uploads geometry, poles,
+ * anchors and the binning accelerators once; runs then keep everything
+ * resident in HBM.  pole_ids (NULL = 0..n_poles-1) are the pole indices
+ * that key the RNG streams, so a row-sharded multi-GPU run reproduces the
+ * single-GPU counts exactly. */
+int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
+                   const double* poles, const int64_t* pole_ids, int64_t n_poles,
+                   double eps, int64_t max_steps, const em_options* opt, em_plan** out);
+int em_plan_destroy(em_plan* p);
+/* walks rep in [rep_start, rep_start + n_rep) for every pole; host outputs */
+int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_outputs* out);
+/* same, outputs left in device memory (caller-owned, zeroed by the library)
+ * and work ordered on `stream` (cudaStream_t, NULL = the plan's stream) */
+int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                       em_outputs* dev_out, void* stream);
+/* device time (ms) of the walk kernel of the last run, CUDA events on the
+ * launching stream; walks and steps of that run */
+int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int64_t* steps);
+/* number of library kernels launched by the last run (the walk kernel plus
+ * any zeroing/packing kernels) */
+int em_plan_last_launches(const em_plan* p, int64_t* launches);
+int64_t em_plan_n_bins(const em_plan* p, int side);
+
+/* One-shot convenience: create, run, destroy. */
+int em_run_accumulate(const em_geometry* g, const em_side* s0, const em_side* s1,
+                      const double* poles, const int64_t* pole_ids, int64_t n_poles,
+                      uint64_t seed, double eps, int64_t max_steps, int64_t n_rep,
+                      const em_options* opt, em_outputs* out);
+
+/* Exit points of n_rep walks from every pole of the plan
+ * (S/backend.py:202-227 generalised to many poles): x_out (n_poles*n_rep, d)
+ * in (pole, replicate) order, steps_out, comp_out likewise. */
+int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                 double* x_out, int64_t* steps_out, int64_t* comp_out, int64_t* err_pole,
+                 int64_t* err_rep);
+
+/* Micro-benchmark used for the roofline denominator: achieved FP32 FFMA
+ * lane-ops/s of an issue-bound kernel on `device` (its own CUDA events). */
+int em_fp32_peak(int device, double* flops_per_s, double* ms);
+
+/* Known-answer hooks for the RNG golden tests: n blocks, inputs
+ * (c0, c1, c2, c3, k0, k1) per block, outputs 4 words per block. */
+int em_philox4x64_blocks(const uint64_t* in6, uint64_t* out4, int n, int device);
+int em_philox4x32_blocks(const uint32_t* in6, uint32_t* out4, int n, int device);
+/* the CUDA toolkit's curand_Philox4x32_10 on the same inputs (cross-check) */
+int em_curand_philox4x32_blocks(const uint32_t* in6, uint32_t* out4, int n, int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

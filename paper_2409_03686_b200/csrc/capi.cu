@@ -1,0 +1,769 @@
+// capi.cu -- C ABI of libexitmeasure_b200.so (declared in
+// include/exitmeasure_b200.h): plans, device buffers, launches.
+//
+// A plan holds one problem (geometry, K^{1/2}, poles, two weight families)
+// resident in HBM: poles as float4 / double rows, anchors as float4 / double,
+// the candidate grids of unstructured families, and the output rows
+// (n_poles x (n0 + n1) int64 counts + three int64 step statistics per pole).
+// Each run zeroes the outputs, launches ONE persistent walk kernel and, for
+// host outputs, copies the rows back.  Nothing here falls back to the CPU: any
+// CUDA failure is returned as EM_ERR_CUDA with the CUDA error string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "em_params.cuh"
+
+namespace em {
+cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s);
+cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
+                       bool ident, int grid, int block, cudaStream_t s);
+cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
+cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
+                                cudaStream_t s);
+cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
+
+struct GridHost {
+  double lo[3];
+  double h;
+  int n[3];
+  std::vector<uint32_t> cell;
+  std::vector<uint32_t> cand;
+};
+bool build_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G);
+}  // namespace em
+
+using namespace em;
+
+static thread_local std::string g_last_error = "";
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define EM_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(EM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// plan
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 16));
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct em_plan {
+  int device = 0, precision = EM_PREC_REF64, chain = EM_CHAIN_WOE;
+  int d = 2, outer = 0, n_holes = 0, n_notch = 0, nh_mode = 2;
+  bool ident = false;
+  int64_t n_poles = 0, n0 = 0, n1 = 0;
+  int grid = 0, block = 256;
+  Ref64Params p64{};
+  F32Params p32{};
+  DevBuf poles, pole_ids, anchors[2], gcell[2], gcand[2];
+  DevBuf counts, stats, misc;  // stats: 3 * n_poles u64; misc: err, ticket, walks
+  DevBuf xo, so, co;           // exits
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int64_t last_walks = 0, last_steps = 0, last_launches = 0;
+  ~em_plan() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int sm_count_of(int dev) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 1;
+  }
+  return cache[dev];
+}
+
+// smallest eigenvalue of a symmetric 2x2 / 3x3 matrix (Jacobi sweeps)
+double sym_min_eig(const double* a_in, int d) {
+  double a[3][3] = {{0}};
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) a[i][j] = a_in[i * d + j];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) off += a[p][q] * a[p][q];
+    if (off < 1e-30) break;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < d; ++k) {
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < d; ++k) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+      }
+  }
+  double m = a[0][0];
+  for (int i = 1; i < d; ++i) m = std::min(m, a[i][i]);
+  return m;
+}
+
+int validate_geometry(const em_geometry* g) {
+  if (!g || !g->gi || !g->gf || !g->comp_side || !g->ksqrt)
+    return fail(EM_ERR_INVALID, "geometry: null pointer");
+  if (g->gi_len < 3) return fail(EM_ERR_INVALID, "geometry: gi needs [d, outer_kind, n_holes]");
+  const int64_t d = g->gi[0], ok = g->gi[1], nh = g->gi[2];
+  const int64_t nn = g->gi_len >= 4 ? g->gi[3] : 0;
+  if (d != 2 && d != 3) return fail(EM_ERR_INVALID, "geometry: dimension must be 2 or 3");
+  if (ok != 0 && ok != 1) return fail(EM_ERR_INVALID, "geometry: outer kind must be 0 (ball) or 1 (box)");
+  if (nh < 0 || nh > EM_MAX_HOLES) return fail(EM_ERR_UNSUPPORTED, "geometry: too many holes");
+  if (nn < 0 || nn > 1) return fail(EM_ERR_INVALID, "geometry: at most one notch");
+  if (nn && (d != 3 || ok != 1)) return fail(EM_ERR_INVALID, "geometry: the notch needs a 3D box");
+  const int64_t need = (d + 1) * (1 + nh) + 2 * nn;
+  if (g->gf_len < need) return fail(EM_ERR_INVALID, "geometry: gf too short");
+  if (g->n_comp < 1 + nh + nn) return fail(EM_ERR_INVALID, "geometry: comp_side too short");
+  for (int64_t c = 0; c < 1 + nh + nn; ++c)
+    if (g->comp_side[c] != 0 && g->comp_side[c] != 1)
+      return fail(EM_ERR_INVALID, "geometry: comp_side entries must be 0 or 1");
+  return EM_OK;
+}
+
+int validate_side(const em_side* s, int d, const char* name, bool used) {
+  if (!s) return fail(EM_ERR_INVALID, std::string(name) + ": null");
+  if (s->wkind != 0)
+    return fail(EM_ERR_UNSUPPORTED, std::string(name) + ": IDW weights are not supported");
+  if (s->n_anchors < 0 || s->n_blk < 0)
+    return fail(EM_ERR_INVALID, std::string(name) + ": negative size");
+  if (used && s->n_anchors == 0)
+    return fail(EM_ERR_INVALID, std::string(name) +
+                                    ": a boundary component maps to this side but it has no "
+                                    "anchors (S/estimator.py:130-131)");
+  if (s->n_anchors > 0 && (!s->anchors || !s->blk || !s->blkf || s->n_blk < 1))
+    return fail(EM_ERR_INVALID, std::string(name) + ": missing anchors or blocks");
+  if (s->n_blk > kMaxBlk) return fail(EM_ERR_UNSUPPORTED, std::string(name) + ": too many blocks");
+  for (int64_t b = 0; b < (s->n_anchors > 0 ? s->n_blk : 0); ++b) {
+    const int64_t kind = s->blk[3 * b], start = s->blk[3 * b + 1], count = s->blk[3 * b + 2];
+    if (start < 0 || count < 1 || start + count > s->n_anchors)
+      return fail(EM_ERR_INVALID, std::string(name) + ": block outside the anchor array");
+    if ((kind == 1 || kind == 2) && d != 2)
+      return fail(EM_ERR_INVALID, std::string(name) + ": circle/square blocks are 2D");
+  }
+  if (s->n_anchors >= (1LL << 31)) return fail(EM_ERR_UNSUPPORTED, "too many anchors");
+  return EM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int em_abi_version(void) { return EM_ABI_VERSION; }
+
+const char* em_last_error(void) { return g_last_error.c_str(); }
+
+int em_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int em_device_info(int device, int* sm_count, int* clock_khz, int* cc_major, int* cc_minor) {
+  cudaDeviceProp prop;
+  EM_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+  if (clock_khz) *clock_khz = clk;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return EM_OK;
+}
+
+int em_plan_destroy(em_plan* p) {
+  if (p) {
+    DeviceGuard dg(p->device);
+    delete p;
+  }
+  return EM_OK;
+}
+
+int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
+                   const double* poles, const int64_t* pole_ids, int64_t n_poles, double eps,
+                   int64_t max_steps, const em_options* opt, em_plan** out) {
+  if (!out) return fail(EM_ERR_INVALID, "out is null");
+  *out = nullptr;
+  int rc = validate_geometry(g);
+  if (rc) return rc;
+  const int d = (int)g->gi[0];
+  const int nh = (int)g->gi[2];
+  const int nn = g->gi_len >= 4 ? (int)g->gi[3] : 0;
+  bool used[2] = {false, false};
+  for (int c = 0; c < 1 + nh + nn; ++c) used[g->comp_side[c]] = true;
+  if ((rc = validate_side(s0, d, "side0", used[0]))) return rc;
+  if ((rc = validate_side(s1, d, "side1", used[1]))) return rc;
+  if (n_poles < 1 || !poles) return fail(EM_ERR_INVALID, "need at least one pole");
+  if (!(eps > 0.0)) return fail(EM_ERR_INVALID, "eps must be positive");
+  if (max_steps < 1) return fail(EM_ERR_INVALID, "max_steps must be >= 1");
+  const em_options dflt{EM_PREC_REF64, EM_CHAIN_WOE, 0, 0, 0, 0};
+  const em_options& o = opt ? *opt : dflt;
+  if (o.precision != EM_PREC_REF64 && o.precision != EM_PREC_FP32)
+    return fail(EM_ERR_INVALID, "unknown precision");
+  if (o.precision == EM_PREC_REF64 && o.chain != EM_CHAIN_WOE)
+    return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
+  int ndev = em_device_count();
+  if (o.device < 0 || o.device >= ndev)
+    return fail(EM_ERR_CUDA, "no such CUDA device (" + std::to_string(ndev) + " visible)");
+  DeviceGuard dg(o.device);
+
+  em_plan* p = new em_plan();
+  p->device = o.device;
+  p->precision = o.precision;
+  p->chain = o.chain;
+  p->d = d;
+  p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
+  p->n_holes = nh;
+  p->n_notch = nn;
+  p->n_poles = n_poles;
+  p->n0 = s0->n_anchors;
+  p->n1 = s1->n_anchors;
+  p->block = o.block > 0 ? o.block : 256;
+  auto bail = [&](int code) {
+    delete p;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess)
+    return bail(fail(EM_ERR_CUDA, std::string("stream/event: ") + cudaGetErrorString(cudaGetLastError())));
+
+  bool ident = true;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) ident = false;
+  p->ident = ident;
+
+  const int64_t row = p->n0 + p->n1;
+  // outputs
+  cudaError_t ce;
+#define EM_ALLOC(buf, bytes)                                                          \
+  if ((ce = (buf).alloc(bytes)) != cudaSuccess)                                       \
+    return bail(fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce)));
+  EM_ALLOC(p->counts, (size_t)n_poles * row * 8);
+  EM_ALLOC(p->stats, (size_t)n_poles * 3 * 8);
+  EM_ALLOC(p->misc, 8 * 8);
+  if (pole_ids) {
+    EM_ALLOC(p->pole_ids, (size_t)n_poles * 8);
+    if (cudaMemcpy(p->pole_ids.p, pole_ids, n_poles * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(EM_ERR_CUDA, "upload pole ids"));
+  }
+
+  WorkOut w{};
+  w.n_poles = n_poles;
+  w.inv_poles = 1.0 / (double)n_poles;
+  w.pole_ids = pole_ids ? p->pole_ids.as<long long>() : nullptr;
+  w.ticket = p->misc.as<unsigned long long>() + 1;
+  w.walks_done = p->misc.as<unsigned long long>() + 2;
+  w.err_key = p->misc.as<unsigned long long>();
+  w.counts = p->counts.as<unsigned long long>();
+  w.row_len = (int)row;
+  w.col_off1 = (int)p->n0;
+  w.ssum = p->stats.as<unsigned long long>();
+  w.ssq = w.ssum + n_poles;
+  w.smax = w.ssq + n_poles;
+
+  const em_side* sides[2] = {s0, s1};
+  if (p->precision == EM_PREC_REF64) {
+    Ref64Params& P = p->p64;
+    P.d = d;
+    P.outer_kind = (int)g->gi[1];
+    P.n_holes = nh;
+    P.n_notch = nn;
+    const int64_t ngf = (d + 1) * (1 + nh) + 2 * nn;
+    for (int64_t i = 0; i < ngf; ++i) P.gf[i] = g->gf[i];
+    for (int c = 0; c < 1 + nh + nn; ++c) P.comp_side[c] = g->comp_side[c];
+    for (int i = 0; i < d * d; ++i) P.ks[i] = g->ksqrt[i];
+    P.eps = eps;
+    P.max_steps = max_steps;
+    EM_ALLOC(p->poles, (size_t)n_poles * d * 8);
+    if (cudaMemcpy(p->poles.p, poles, n_poles * d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(EM_ERR_CUDA, "upload poles"));
+    P.poles = p->poles.as<double>();
+    for (int s = 0; s < 2; ++s) {
+      const em_side* S = sides[s];
+      Side64& D = P.side[s];
+      D.n_anchors = (int)S->n_anchors;
+      D.n_blk = S->n_anchors > 0 ? (int)S->n_blk : 0;
+      D.wkind = S->wkind;
+      for (int b = 0; b < D.n_blk; ++b) {
+        D.kind[b] = (int)S->blk[3 * b];
+        D.start[b] = S->blk[3 * b + 1];
+        D.count[b] = S->blk[3 * b + 2];
+        D.cx[b] = S->blkf[4 * b];
+        D.cy[b] = S->blkf[4 * b + 1];
+        D.radius[b] = S->blkf[4 * b + 3];
+        D.phase[b] = S->blk_phase ? S->blk_phase[b] : 0.0;
+      }
+      if (S->n_anchors > 0) {
+        EM_ALLOC(p->anchors[s], (size_t)S->n_anchors * d * 8);
+        if (cudaMemcpy(p->anchors[s].p, S->anchors, S->n_anchors * d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+          return bail(fail(EM_ERR_CUDA, "upload anchors"));
+        D.anchors = p->anchors[s].as<double>();
+      }
+    }
+    P.w = w;
+  } else {
+    F32Params& P = p->p32;
+    const double* gf = g->gf;
+    P.n_holes = nh;
+    P.has_notch = nn;
+    double scale = 1.0;
+    if (g->gi[1] == 0) {
+      for (int j = 0; j < d; ++j) P.oc[j] = (float)gf[j];
+      P.oR = (float)gf[d];
+      for (int j = 0; j < d; ++j) scale = std::max(scale, std::fabs(gf[j]) + gf[d]);
+    } else {
+      for (int j = 0; j < d; ++j) {
+        P.blo[j] = (float)(gf[j] - gf[d]);
+        P.bhi[j] = (float)(gf[j] + gf[d]);
+        scale = std::max(scale, std::fabs(gf[j]) + gf[d]);
+      }
+    }
+    for (int h = 0; h < nh; ++h) {
+      const int off = d + 1 + h * (d + 1);
+      for (int j = 0; j < d; ++j) P.hc[h][j] = (float)gf[off + j];
+      P.hr[h] = (float)gf[off + d];
+    }
+    if (nn) {
+      const int off = (d + 1) * (1 + nh);
+      P.notch[0] = (float)gf[off];
+      P.notch[1] = (float)gf[off + 1];
+    }
+    for (int c = 0; c < 1 + nh + nn; ++c) P.comp_side[c] = g->comp_side[c];
+    for (int i = 0; i < d * d; ++i) P.A[i] = (float)g->ksqrt[i];
+    for (int i = 0; i < d; ++i) {
+      double n2 = 0.0;
+      for (int k = 0; k < d; ++k) n2 += g->ksqrt[k * d + i] * g->ksqrt[k * d + i];
+      // 1/|A e_i|, rounded down so the face bound stays a lower bound
+      P.g[i] = (float)(1.0 / std::sqrt(n2) * (1.0 - 1e-6));
+    }
+    const double lam = sym_min_eig(g->ksqrt, d);
+    P.m2 = (float)(std::max(0.0, lam) * std::max(0.0, lam) * (1.0 - 1e-4));
+    P.eps = (float)eps;
+    P.shrink_rel = 4.0e-6f;
+    P.shrink_abs = (float)(scale * 1.1920928955078125e-07);
+    P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);
+    std::vector<float> pf(n_poles * 4, 0.0f);
+    for (int64_t i = 0; i < n_poles; ++i)
+      for (int j = 0; j < d; ++j) pf[i * 4 + j] = (float)poles[i * d + j];
+    EM_ALLOC(p->poles, (size_t)n_poles * 16);
+    if (cudaMemcpy(p->poles.p, pf.data(), n_poles * 16, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(EM_ERR_CUDA, "upload poles"));
+    P.poles = p->poles.as<float4>();
+    for (int s = 0; s < 2; ++s) {
+      const em_side* S = sides[s];
+      Side32& D = P.side[s];
+      D.n_anchors = (int)S->n_anchors;
+      D.n_blk = S->n_anchors > 0 ? (int)S->n_blk : 0;
+      D.has_grid = 0;
+      for (int b = 0; b < D.n_blk; ++b) {
+        D.kind[b] = (int)S->blk[3 * b];
+        D.start[b] = (int)S->blk[3 * b + 1];
+        D.count[b] = (int)S->blk[3 * b + 2];
+        D.cx[b] = (float)S->blkf[4 * b];
+        D.cy[b] = (float)S->blkf[4 * b + 1];
+        D.cz[b] = (float)S->blkf[4 * b + 2];
+        D.radius[b] = (float)S->blkf[4 * b + 3];
+        D.phase[b] = (float)(S->blk_phase ? S->blk_phase[b] : 0.0);
+        const double cnt = (double)D.count[b];
+        if (D.kind[b] == BLK_CIRCLE) D.scale[b] = (float)(cnt / (2.0 * M_PI));
+        else if (D.kind[b] == BLK_SQUARE) D.scale[b] = (float)(cnt / (8.0 * S->blkf[4 * b + 3]));
+        else D.scale[b] = 0.0f;
+      }
+      if (S->n_anchors == 0) continue;
+      std::vector<float> af(S->n_anchors * 4, 0.0f);
+      for (int64_t i = 0; i < S->n_anchors; ++i)
+        for (int j = 0; j < d; ++j) af[i * 4 + j] = (float)S->anchors[i * d + j];
+      EM_ALLOC(p->anchors[s], (size_t)S->n_anchors * 16);
+      if (cudaMemcpy(p->anchors[s].p, af.data(), S->n_anchors * 16, cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(EM_ERR_CUDA, "upload anchors"));
+      D.anchors = p->anchors[s].as<float4>();
+      // one generic block covering the family: accelerate with the grid
+      if (D.n_blk == 1 && D.kind[0] == BLK_GENERIC && S->n_anchors > 8) {
+        GridHost G;
+        if (build_grid(S->anchors, S->n_anchors, d, eps, G)) {
+          EM_ALLOC(p->gcell[s], G.cell.size() * 4);
+          EM_ALLOC(p->gcand[s], G.cand.size() * 4);
+          if (cudaMemcpy(p->gcell[s].p, G.cell.data(), G.cell.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+              cudaMemcpy(p->gcand[s].p, G.cand.data(), G.cand.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(EM_ERR_CUDA, "upload grid"));
+          D.has_grid = 1;
+          for (int j = 0; j < 3; ++j) {
+            D.grid.lo[j] = (float)G.lo[j];
+            D.grid.n[j] = G.n[j];
+          }
+          D.grid.inv_h = (float)(1.0 / G.h);
+          D.grid.cell = p->gcell[s].as<unsigned>();
+          D.grid.cand = p->gcand[s].as<unsigned>();
+        }
+      }
+    }
+    P.w = w;
+    p->nh_mode = nh == 0 ? 0 : ((nh == 1 && d == 2 && g->gi[1] == 0) ? 1 : 2);
+  }
+#undef EM_ALLOC
+  // persistent grid: SMs x resident blocks
+  int per_sm = 4;
+  p->grid = o.grid > 0 ? o.grid : sm_count_of(o.device) * per_sm * (256 / p->block > 0 ? 256 / p->block : 1);
+  *out = p;
+  return EM_OK;
+}
+
+static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, int mode,
+                       unsigned long long* counts, unsigned long long* stats, cudaStream_t s) {
+  if (n_rep < 0 || rep_start < 0) return fail(EM_ERR_INVALID, "negative replicate range");
+  const int64_t total = p->n_poles * n_rep;
+  if (n_rep > 0 && total / n_rep != p->n_poles) return fail(EM_ERR_INVALID, "walk count overflows");
+  if ((double)total > 9.0e15) return fail(EM_ERR_INVALID, "walk count too large");
+  WorkOut* w = p->precision == EM_PREC_REF64 ? &p->p64.w : &p->p32.w;
+  w->rep_start = rep_start;
+  w->n_rep = n_rep;
+  w->total = total;
+  w->counts = counts;
+  w->ssum = stats;
+  w->ssq = stats + p->n_poles;
+  w->smax = stats + 2 * p->n_poles;
+  const int64_t row = p->n0 + p->n1;
+  int64_t launches = 0;
+  if (mode == 0) {
+    EM_CUDA(cudaMemsetAsync(counts, 0, (size_t)p->n_poles * row * 8, s));
+    EM_CUDA(cudaMemsetAsync(stats, 0, (size_t)p->n_poles * 3 * 8, s));
+  }
+  EM_CUDA(cudaMemsetAsync(p->misc.p, 0, 64, s));
+  EM_CUDA(cudaMemsetAsync(p->misc.p, 0xff, 8, s));  // err_key = ~0
+  if (total > 0) {
+    const int64_t lanes_needed = (total + 31) / 32 * 32;
+    int grid = p->grid;
+    const int64_t blocks_needed = (lanes_needed + p->block - 1) / p->block;
+    if (blocks_needed < grid) grid = (int)std::max<int64_t>(1, blocks_needed);
+    EM_CUDA(cudaEventRecord(p->ev0, s));
+    cudaError_t e;
+    if (p->precision == EM_PREC_REF64) {
+      p->p64.seed = seed;
+      e = launch_ref64(p->p64, mode, grid, p->block, s);
+    } else {
+      p->p32.key0 = (unsigned)(seed & 0xffffffffULL);
+      p->p32.key1 = (unsigned)(seed >> 32);
+      e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, grid,
+                     p->block, s);
+    }
+    if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("walk kernel launch: ") + cudaGetErrorString(e));
+    EM_CUDA(cudaEventRecord(p->ev1, s));
+    launches = 1;
+  }
+  p->last_launches = launches;
+  p->last_walks = total;
+  return EM_OK;
+}
+
+static int plan_finish(em_plan* p, cudaStream_t s, int64_t n_rep, em_outputs* out,
+                       const unsigned long long* host_stats) {
+  unsigned long long err = ~0ULL;
+  EM_CUDA(cudaMemcpyAsync(&err, p->misc.p, 8, cudaMemcpyDeviceToHost, s));
+  EM_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.0f;
+  if (p->last_launches) {
+    EM_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  }
+  p->last_ms = ms;
+  if (host_stats) {
+    int64_t st = 0;
+    for (int64_t i = 0; i < p->n_poles; ++i) st += (int64_t)host_stats[i];
+    p->last_steps = st;
+  }
+  if (err != ~0ULL) {
+    if (out) {
+      out->err_pole = n_rep > 0 ? (int64_t)(err / (unsigned long long)n_rep) : 0;
+      out->err_rep = n_rep > 0 ? (int64_t)(err % (unsigned long long)n_rep) : 0;
+    }
+    return EM_BUDGET;
+  }
+  if (out) out->err_pole = out->err_rep = -1;
+  return EM_OK;
+}
+
+int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_outputs* out) {
+  if (!p || !out || !out->counts || !out->steps_sum || !out->steps_sq || !out->steps_max)
+    return fail(EM_ERR_INVALID, "plan/outputs null");
+  DeviceGuard dg(p->device);
+  int rc = plan_launch(p, seed, rep_start, n_rep, 0, p->counts.as<unsigned long long>(),
+                       p->stats.as<unsigned long long>(), p->stream);
+  if (rc) return rc;
+  const int64_t row = p->n0 + p->n1;
+  EM_CUDA(cudaMemcpyAsync(out->counts, p->counts.p, (size_t)p->n_poles * row * 8,
+                          cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(out->steps_sum, p->stats.p, p->n_poles * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(out->steps_sq, p->stats.as<char>() + p->n_poles * 8, p->n_poles * 8,
+                          cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(out->steps_max, p->stats.as<char>() + 2 * p->n_poles * 8, p->n_poles * 8,
+                          cudaMemcpyDeviceToHost, p->stream));
+  return plan_finish(p, p->stream, n_rep, out,
+                     reinterpret_cast<const unsigned long long*>(out->steps_sum));
+}
+
+int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                       em_outputs* dev_out, void* stream) {
+  if (!p || !dev_out || !dev_out->counts || !dev_out->steps_sum)
+    return fail(EM_ERR_INVALID, "plan/outputs null");
+  DeviceGuard dg(p->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
+  // steps_sq / steps_max must follow steps_sum contiguously (one stats block)
+  if (dev_out->steps_sq != dev_out->steps_sum + p->n_poles ||
+      dev_out->steps_max != dev_out->steps_sum + 2 * p->n_poles)
+    return fail(EM_ERR_INVALID, "device stats must be one contiguous (3, n_poles) block");
+  int rc = plan_launch(p, seed, rep_start, n_rep, 0,
+                       reinterpret_cast<unsigned long long*>(dev_out->counts),
+                       reinterpret_cast<unsigned long long*>(dev_out->steps_sum), s);
+  if (rc) return rc;
+  return plan_finish(p, s, n_rep, dev_out, nullptr);
+}
+
+int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int64_t* steps) {
+  if (!p) return fail(EM_ERR_INVALID, "plan null");
+  if (kernel_ms) *kernel_ms = p->last_ms;
+  if (walks) *walks = p->last_walks;
+  if (steps) *steps = p->last_steps;
+  return EM_OK;
+}
+
+int em_plan_last_launches(const em_plan* p, int64_t* launches) {
+  if (!p || !launches) return fail(EM_ERR_INVALID, "null");
+  *launches = p->last_launches;
+  return EM_OK;
+}
+
+int64_t em_plan_n_bins(const em_plan* p, int side) {
+  if (!p) return -1;
+  return side == 0 ? p->n0 : p->n1;
+}
+
+int em_run_accumulate(const em_geometry* g, const em_side* s0, const em_side* s1,
+                      const double* poles, const int64_t* pole_ids, int64_t n_poles,
+                      uint64_t seed, double eps, int64_t max_steps, int64_t n_rep,
+                      const em_options* opt, em_outputs* out) {
+  em_plan* p = nullptr;
+  int rc = em_plan_create(g, s0, s1, poles, pole_ids, n_poles, eps, max_steps, opt, &p);
+  if (rc) return rc;
+  rc = em_plan_run(p, seed, 0, n_rep, out);
+  em_plan_destroy(p);
+  return rc;
+}
+
+int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, double* x_out,
+                 int64_t* steps_out, int64_t* comp_out, int64_t* err_pole, int64_t* err_rep) {
+  if (!p || !x_out || !steps_out || !comp_out) return fail(EM_ERR_INVALID, "null");
+  DeviceGuard dg(p->device);
+  const int64_t total = p->n_poles * n_rep;
+  cudaError_t ce;
+  if ((ce = p->xo.alloc((size_t)std::max<int64_t>(total, 1) * p->d * 8)) != cudaSuccess ||
+      (ce = p->so.alloc((size_t)std::max<int64_t>(total, 1) * 8)) != cudaSuccess ||
+      (ce = p->co.alloc((size_t)std::max<int64_t>(total, 1) * 8)) != cudaSuccess)
+    return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+  WorkOut* w = p->precision == EM_PREC_REF64 ? &p->p64.w : &p->p32.w;
+  w->x_out = p->xo.as<double>();
+  w->steps_out = p->so.as<long long>();
+  w->comp_out = p->co.as<long long>();
+  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->counts.as<unsigned long long>(),
+                       p->stats.as<unsigned long long>(), p->stream);
+  if (rc) return rc;
+  if (total > 0) {
+    EM_CUDA(cudaMemcpyAsync(x_out, p->xo.p, total * p->d * 8, cudaMemcpyDeviceToHost, p->stream));
+    EM_CUDA(cudaMemcpyAsync(steps_out, p->so.p, total * 8, cudaMemcpyDeviceToHost, p->stream));
+    EM_CUDA(cudaMemcpyAsync(comp_out, p->co.p, total * 8, cudaMemcpyDeviceToHost, p->stream));
+  }
+  em_outputs o{};
+  rc = plan_finish(p, p->stream, n_rep, &o, nullptr);
+  if (err_pole) *err_pole = o.err_pole;
+  if (err_rep) *err_rep = o.err_rep;
+  return rc;
+}
+
+// ---- chunk-level drop-ins (the reference's _impl contract) ----
+
+int em_walk_exits_chunk(const em_geometry* g, const double* pole_xy, int64_t pole_index,
+                        int64_t rep_start, int64_t rep_end, uint64_t seed, double eps,
+                        int64_t max_steps, int device, double* x_out, int64_t* steps_out,
+                        int64_t* comp_out, int64_t* err_rep) {
+  if (rep_end < rep_start) return fail(EM_ERR_INVALID, "rep_end < rep_start");
+  const em_side empty{nullptr, 0, nullptr, nullptr, 0, 0, 2, nullptr, nullptr};
+  // exits mode never bins: pretend every component maps to side 0 of an
+  // empty family by using a geometry copy whose comp_side is ignored
+  em_options o{EM_PREC_REF64, EM_CHAIN_WOE, device, 0, 0, 0};
+  em_geometry g2 = *g;
+  std::vector<int8_t> cs(std::max<int64_t>(g->n_comp, 1), 0);
+  g2.comp_side = cs.data();
+  g2.n_comp = (int64_t)cs.size();
+  // a dummy one-anchor family keeps validation happy without binning
+  const double dummy[3] = {0, 0, 0};
+  const int64_t blk[3] = {0, 0, 1};
+  const double blkf[4] = {0, 0, 0, 0};
+  const em_side one{dummy, 1, blk, blkf, 1, 0, 2, nullptr, nullptr};
+  em_plan* p = nullptr;
+  const int64_t pid = pole_index;
+  int rc = em_plan_create(&g2, &one, &empty, pole_xy, &pid, 1, eps, max_steps, &o, &p);
+  if (rc) return rc;
+  int64_t ep = -1, er = -1;
+  rc = em_run_exits(p, seed, rep_start, rep_end - rep_start, x_out, steps_out, comp_out, &ep, &er);
+  em_plan_destroy(p);
+  if (err_rep) *err_rep = (rc == EM_BUDGET) ? rep_start + er : -1;
+  if (rc == EM_BUDGET) {
+    for (int64_t i = 0; i < rep_end - rep_start; ++i) comp_out[i] = 0;
+    return EM_OK;
+  }
+  return rc;
+}
+
+int em_accumulate_chunk(const em_geometry* g, const double* pole_xy, int64_t pole_index,
+                        int64_t rep_start, int64_t rep_end, uint64_t seed, double eps,
+                        int64_t max_steps, const em_side* s0, const em_side* s1, int device,
+                        double* out0, double* out1, int64_t* stats, int64_t* err_rep) {
+  if (rep_end < rep_start) return fail(EM_ERR_INVALID, "rep_end < rep_start");
+  em_options o{EM_PREC_REF64, EM_CHAIN_WOE, device, 0, 0, 0};
+  em_plan* p = nullptr;
+  const int64_t pid = pole_index;
+  int rc = em_plan_create(g, s0, s1, pole_xy, &pid, 1, eps, max_steps, &o, &p);
+  if (rc) return rc;
+  const int64_t row = s0->n_anchors + s1->n_anchors;
+  std::vector<int64_t> counts(std::max<int64_t>(row, 1));
+  int64_t ss = 0, sq = 0, sm = 0;
+  em_outputs out{counts.data(), &ss, &sq, &sm, -1, -1};
+  rc = em_plan_run(p, seed, rep_start, rep_end - rep_start, &out);
+  em_plan_destroy(p);
+  if (rc == EM_BUDGET) {
+    if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+    if (err_rep) *err_rep = rep_start + out.err_rep;
+    return EM_OK;
+  }
+  if (rc) return rc;
+  for (int64_t i = 0; i < s0->n_anchors; ++i) out0[i] += (double)counts[i];
+  for (int64_t i = 0; i < s1->n_anchors; ++i) out1[i] += (double)counts[s0->n_anchors + i];
+  if (stats) {
+    stats[0] = ss;
+    stats[1] = sq;
+    stats[2] = sm;
+    stats[3] = 0;
+  }
+  if (err_rep) *err_rep = -1;
+  return EM_OK;
+}
+
+int em_fp32_peak(int device, double* flops_per_s, double* ms_out) {
+  DeviceGuard dg(device);
+  const int sms = sm_count_of(device);
+  float* buf = nullptr;
+  EM_CUDA(cudaMalloc(&buf, 1024 * 4));
+  cudaEvent_t a, b;
+  EM_CUDA(cudaEventCreate(&a));
+  EM_CUDA(cudaEventCreate(&b));
+  const int grid = sms * 8, block = 256, iters = 1 << 14;
+  cudaError_t e = launch_ffma_peak(buf, iters, grid, block, 0);  // warm-up
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, cudaGetErrorString(e));
+  EM_CUDA(cudaEventRecord(a, 0));
+  e = launch_ffma_peak(buf, iters, grid, block, 0);
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, cudaGetErrorString(e));
+  EM_CUDA(cudaEventRecord(b, 0));
+  EM_CUDA(cudaEventSynchronize(b));
+  float ms = 0.0f;
+  EM_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  // one FFMA = one FP32 lane-op in the SURVEY's F_step convention
+  const double ops = (double)grid * block * iters * 8.0;
+  if (flops_per_s) *flops_per_s = ops / (ms * 1e-3);
+  if (ms_out) *ms_out = ms;
+  return EM_OK;
+}
+
+// known-answer hooks for the RNG golden tests
+int em_philox4x64_blocks(const uint64_t* in6, uint64_t* out4, int n, int device) {
+  DeviceGuard dg(device);
+  unsigned long long *din = nullptr, *dout = nullptr;
+  EM_CUDA(cudaMalloc(&din, (size_t)n * 48));
+  EM_CUDA(cudaMalloc(&dout, (size_t)n * 32));
+  EM_CUDA(cudaMemcpy(din, in6, (size_t)n * 48, cudaMemcpyHostToDevice));
+  cudaError_t e = launch_philox64_kat(din, dout, n, 0);
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, cudaGetErrorString(e));
+  EM_CUDA(cudaMemcpy(out4, dout, (size_t)n * 32, cudaMemcpyDeviceToHost));
+  cudaFree(din);
+  cudaFree(dout);
+  return EM_OK;
+}
+
+int em_philox4x32_blocks(const uint32_t* in6, uint32_t* out4, int n, int device) {
+  DeviceGuard dg(device);
+  unsigned *din = nullptr, *dout = nullptr;
+  EM_CUDA(cudaMalloc(&din, (size_t)n * 24));
+  EM_CUDA(cudaMalloc(&dout, (size_t)n * 16));
+  EM_CUDA(cudaMemcpy(din, in6, (size_t)n * 24, cudaMemcpyHostToDevice));
+  cudaError_t e = launch_philox32_kat(din, dout, n, 0);
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, cudaGetErrorString(e));
+  EM_CUDA(cudaMemcpy(out4, dout, (size_t)n * 16, cudaMemcpyDeviceToHost));
+  cudaFree(din);
+  cudaFree(dout);
+  return EM_OK;
+}
+
+}  // extern "C"

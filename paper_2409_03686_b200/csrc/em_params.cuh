@@ -1,0 +1,94 @@
+// em_params.cuh -- kernel parameter blocks shared by the REF64 mirror and the
+// FP32 production kernels, and the host-side plan that owns their buffers.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/exitmeasure_b200.h"
+
+namespace em {
+
+constexpr int kMaxBlk = 16;         // structured anchor blocks per side
+constexpr int kMaxComp = EM_MAX_HOLES + 2;
+constexpr int kGfMax = 4 + 4 * EM_MAX_HOLES + 2;
+
+enum BlkKind { BLK_GENERIC = 0, BLK_CIRCLE = 1, BLK_SQUARE = 2 };
+enum Outer { OUTER_BALL = 0, OUTER_BOX = 1, OUTER_LBOX = 2 };
+
+// Candidate grid for unstructured anchor families (FP32 path).  cell word =
+// offset << 8 | count; count 255 = brute force over the whole family.
+struct Grid32 {
+  float lo[3];
+  float inv_h;
+  int n[3];
+  const unsigned* cell;
+  const unsigned* cand;
+};
+
+struct Side64 {
+  int n_anchors, n_blk, wkind;
+  int kind[kMaxBlk];
+  long long start[kMaxBlk], count[kMaxBlk];
+  double cx[kMaxBlk], cy[kMaxBlk], radius[kMaxBlk], phase[kMaxBlk];
+  const double* anchors;
+};
+
+struct Side32 {
+  int n_anchors, n_blk;
+  int kind[kMaxBlk];
+  int start[kMaxBlk], count[kMaxBlk];
+  float cx[kMaxBlk], cy[kMaxBlk], cz[kMaxBlk], radius[kMaxBlk], phase[kMaxBlk];
+  float scale[kMaxBlk];  // circle: count/2pi, square: count/8h
+  const float4* anchors;
+  int has_grid;
+  Grid32 grid;
+};
+
+// Work distribution and outputs common to every walk kernel.
+struct WorkOut {
+  long long n_poles, rep_start, n_rep, total;  // total = n_poles * n_rep
+  double inv_poles;                            // 1/n_poles for g -> (rep, pole)
+  const long long* pole_ids;                   // RNG pole index per row
+  unsigned long long* ticket;                  // global walk counter
+  unsigned long long* counts;                  // (n_poles, row_len)
+  int row_len, col_off1;                       // side-1 column offset
+  unsigned long long *ssum, *ssq, *smax, *err_key;
+  unsigned long long* walks_done;              // exits binned (diagnostic)
+  // exits mode (em_run_exits / walk_exits_chunk)
+  double* x_out;
+  long long* steps_out;
+  long long* comp_out;
+};
+
+struct Ref64Params {
+  int d, outer_kind, n_holes, n_notch;
+  double gf[kGfMax];
+  signed char comp_side[kMaxComp];
+  double ks[9];
+  double eps;
+  long long max_steps;
+  unsigned long long seed;
+  const double* poles;  // (n_poles, d)
+  Side64 side[2];
+  WorkOut w;
+};
+
+struct F32Params {
+  int n_holes, has_notch;
+  float oc[3], oR;  // ball outer: center, radius
+  float blo[3], bhi[3];  // box / L-box outer: low and high corners
+  float hc[EM_MAX_HOLES][3], hr[EM_MAX_HOLES];
+  float notch[2];
+  signed char comp_side[kMaxComp];
+  float A[9];       // K^{1/2}, row-major
+  float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid
+  float m2;         // sigma_min(A)^2 (hole bound)
+  float eps;
+  float shrink_rel, shrink_abs;  // step safety margins
+  int max_steps;
+  unsigned key0, key1;
+  const float4* poles;
+  Side32 side[2];
+  WorkOut w;
+};
+
+}  // namespace em

@@ -1,0 +1,566 @@
+// walk_f32.cu -- production FP32 walk + exit-binning kernel for sm_100a.
+//
+// One persistent thread per walk slot, register-resident state, lanes refilled
+// from a warp-local pool (em_pool.cuh).  The walk is the reference's
+// walk-on-ellipsoids chain (S/_kernel.pyx:163-197, S/ = /root/reference/pkg/
+// src/exitmeasure/) re-designed for SIMT FP32 issue:
+//
+//  * RNG: Philox4x32-10 keyed (seed) with counter (draw, rep_lo, pole, rep_hi)
+//    -- one block per lane per batch of steps, so RNG is warp-uniform work,
+//    never a divergent per-lane refill.  2D: one 32-bit word per step (an
+//    angle); 3D: two words (z and an angle, Archimedes' projection).  No
+//    rejection loop (the reference's Marsaglia trials diverge on SIMT).
+//  * Step: x <- x + r(x) K^{1/2} u, with r = sd (EM_CHAIN_WOE, the reference
+//    chain) or r = a certified lower bound of the largest inscribed
+//    K^{1/2}-ellipsoid (EM_CHAIN_MAX; exact for planes, closed form for balls
+//    and holes), shrunk by a relative + absolute FP32 margin so no step
+//    leaves the closed domain by more than an ulp.
+//  * Stop: Euclidean sd <= eps (the reference's shell, S/_kernel.pyx:177-180);
+//    points a rounding step outside count as exits too.
+//  * Binning: owner component -> side (S/_kernel.pyx:145-156), then the
+//    nearest anchor of that side's family in O(1): circle/square blocks by
+//    angle / arc length (S/_kernel.pyx:260-313 without the window scan),
+//    unstructured families through a conservative candidate grid.
+//  * Accumulation: int64 global atomics on pole-interleaved rows (see
+//    em_pool.cuh: concurrent walks spread over all rows, so no hot address).
+#include <cuda_runtime.h>
+
+#include "em_params.cuh"
+#include "em_pool.cuh"
+#include "em_rng.cuh"
+
+namespace em {
+namespace f32 {
+
+constexpr float kPi = 3.14159265358979323846f;
+constexpr float kInf = __builtin_huge_valf();
+
+template <int NH>
+__device__ __forceinline__ int n_holes(const F32Params& P) {
+  return NH >= 0 ? NH : P.n_holes;
+}
+
+// Euclidean signed distance e and step scale r at x.
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+__device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
+  constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
+  if (OUTER == OUTER_BALL) {
+    const float v0 = x[0] - P.oc[0], v1 = x[1] - P.oc[1];
+    const float v2 = D == 3 ? x[2] - P.oc[2] : 0.0f;
+    float s2 = v0 * v0 + v1 * v1;
+    if (D == 3) s2 = fmaf(v2, v2, s2);
+    const float s = sqrtf(s2);
+    e = P.oR - s;
+    if (MAXC) {
+      // |x + rAu|^2 <= s^2 + 2 r |Av| + r^2 <= R^2  =>  r <= q / (a + sqrt(a^2 + q))
+      const float* A = P.A;
+      float a0, a1, a2 = 0.0f;
+      if (D == 2) {
+        a0 = fmaf(A[0], v0, A[1] * v1);
+        a1 = fmaf(A[2], v0, A[3] * v1);
+      } else {
+        a0 = fmaf(A[0], v0, fmaf(A[1], v1, A[2] * v2));
+        a1 = fmaf(A[3], v0, fmaf(A[4], v1, A[5] * v2));
+        a2 = fmaf(A[6], v0, fmaf(A[7], v1, A[8] * v2));
+      }
+      float aa = a0 * a0 + a1 * a1;
+      if (D == 3) aa = fmaf(a2, a2, aa);
+      const float q = e * (P.oR + s);
+      r = __fdividef(q, sqrtf(aa) + sqrtf(fmaxf(aa + q, 0.0f)));
+    } else {
+      r = e;
+    }
+  } else {
+    // box / L-box outer: face planes; the maximal ellipsoid touches plane i at
+    // (distance to plane) / |A e_i| = distance * g_i
+    e = kInf;
+    r = kInf;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const float m = fminf(x[i] - P.blo[i], P.bhi[i] - x[i]);
+      e = fminf(e, m);
+      if (MAXC) r = fminf(r, m * P.g[i]);
+    }
+    if (!MAXC) r = e;
+    if (OUTER == OUTER_LBOX) {
+      const float qx = P.notch[0] - x[0], qy = P.notch[1] - x[1];
+      float en;
+      if (qx <= 0.0f && qy <= 0.0f) {
+        en = fmaxf(qx, qy);
+      } else {
+        const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
+        en = sqrtf(fmaf(ax, ax, ay * ay));
+      }
+      e = fminf(e, en);
+      if (MAXC)
+        r = fminf(r, fmaxf(en, fmaxf(qx * P.g[0], qy * P.g[1])));
+      else
+        r = e;
+    }
+  }
+  // ball holes
+  const int nh = n_holes<NH>(P);
+  for (int h = 0; h < nh; ++h) {
+    const float v0 = x[0] - P.hc[h][0], v1 = x[1] - P.hc[h][1];
+    const float v2 = D == 3 ? x[2] - P.hc[h][2] : 0.0f;
+    float s2 = v0 * v0 + v1 * v1;
+    if (D == 3) s2 = fmaf(v2, v2, s2);
+    const float s = sqrtf(s2);
+    const float rho = P.hr[h];
+    const float eh = s - rho;
+    e = fminf(e, eh);
+    if (MAXC) {
+      // min_u |v + rAu|^2 >= s^2 - 2 r |Av| + r^2 m^2 >= rho^2
+      const float* A = P.A;
+      float a0, a1, a2 = 0.0f;
+      if (D == 2) {
+        a0 = fmaf(A[0], v0, A[1] * v1);
+        a1 = fmaf(A[2], v0, A[3] * v1);
+      } else {
+        a0 = fmaf(A[0], v0, fmaf(A[1], v1, A[2] * v2));
+        a1 = fmaf(A[3], v0, fmaf(A[4], v1, A[5] * v2));
+        a2 = fmaf(A[6], v0, fmaf(A[7], v1, A[8] * v2));
+      }
+      float aa = a0 * a0 + a1 * a1;
+      if (D == 3) aa = fmaf(a2, a2, aa);
+      const float q = eh * (s + rho);
+      const float rh = __fdividef(q, sqrtf(aa) + sqrtf(fmaxf(fmaf(-P.m2, q, aa), 0.0f)));
+      r = fminf(r, fmaxf(rh, eh));
+    } else {
+      r = e;
+    }
+  }
+}
+
+// Owner component: argmin of |component distance|, ties to the lowest id
+// (S/_kernel.pyx:145-156).
+template <int D, int OUTER, int NH>
+__device__ __forceinline__ int owner(const F32Params& P, const float* x) {
+  float best;
+  if (OUTER == OUTER_BALL) {
+    const float v0 = x[0] - P.oc[0], v1 = x[1] - P.oc[1];
+    const float v2 = D == 3 ? x[2] - P.oc[2] : 0.0f;
+    best = fabsf(P.oR - sqrtf(v0 * v0 + v1 * v1 + v2 * v2));
+  } else {
+    float m = kInf;
+#pragma unroll
+    for (int i = 0; i < D; ++i) m = fminf(m, fminf(x[i] - P.blo[i], P.bhi[i] - x[i]));
+    best = fabsf(m);
+  }
+  int comp = 0;
+  const int nh = n_holes<NH>(P);
+  for (int h = 0; h < nh; ++h) {
+    const float v0 = x[0] - P.hc[h][0], v1 = x[1] - P.hc[h][1];
+    const float v2 = D == 3 ? x[2] - P.hc[h][2] : 0.0f;
+    const float dd = fabsf(sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - P.hr[h]);
+    if (dd < best) {
+      best = dd;
+      comp = h + 1;
+    }
+  }
+  if (OUTER == OUTER_LBOX) {
+    const float qx = P.notch[0] - x[0], qy = P.notch[1] - x[1];
+    float en;
+    if (qx <= 0.0f && qy <= 0.0f) {
+      en = fmaxf(qx, qy);
+    } else {
+      const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
+      en = sqrtf(fmaf(ax, ax, ay * ay));
+    }
+    if (fabsf(en) < best) comp = nh + 1;
+  }
+  return comp;
+}
+
+__device__ __forceinline__ int wrapi(int k, int count) {
+  k = k % count;
+  return k < 0 ? k + count : k;
+}
+
+template <int D>
+__device__ __forceinline__ float d2_to(const float4 a, const float* x) {
+  const float d0 = x[0] - a.x, d1 = x[1] - a.y;
+  float t = fmaf(d0, d0, d1 * d1);
+  if (D == 3) {
+    const float d2 = x[2] - a.z;
+    t = fmaf(d2, d2, t);
+  }
+  return t;
+}
+
+template <int D>
+__device__ int brute(const Side32& S, const float* x, int start, int count) {
+  float best = kInf;
+  int bi = start;
+  for (int i = start; i < start + count; ++i) {
+    const float t = d2_to<D>(__ldg(&S.anchors[i]), x);
+    if (t < best) {
+      best = t;
+      bi = i;
+    }
+  }
+  return bi;
+}
+
+// Nearest anchor (family-local index) of one side's family.
+template <int D>
+__device__ int nearest_anchor(const Side32& S, const float* x) {
+  if (S.has_grid) {
+    const Grid32& G = S.grid;
+    const int ix = (int)floorf((x[0] - G.lo[0]) * G.inv_h);
+    const int iy = (int)floorf((x[1] - G.lo[1]) * G.inv_h);
+    const int iz = D == 3 ? (int)floorf((x[2] - G.lo[2]) * G.inv_h) : 0;
+    if (ix >= 0 && iy >= 0 && iz >= 0 && ix < G.n[0] && iy < G.n[1] && iz < G.n[2]) {
+      const unsigned w = __ldg(&G.cell[(iz * G.n[1] + iy) * G.n[0] + ix]);
+      const unsigned cnt = w & 255u, off = w >> 8;
+      if (cnt != 255u) {
+        float best = kInf;
+        int bi = 0;
+        for (unsigned j = 0; j < cnt; ++j) {
+          const int a = (int)__ldg(&G.cand[off + j]);
+          const float t = d2_to<D>(__ldg(&S.anchors[a]), x);
+          if (t < best || (t == best && a < bi)) {
+            best = t;
+            bi = a;
+          }
+        }
+        return bi;
+      }
+    }
+    return brute<D>(S, x, 0, S.n_anchors);
+  }
+  float best = kInf;
+  int bi = 0;
+  for (int b = 0; b < S.n_blk; ++b) {
+    int idx;
+    const int count = S.count[b];
+    if (S.kind[b] == BLK_CIRCLE) {
+      const float ang = atan2f(x[1] - S.cy[b], x[0] - S.cx[b]);
+      const float t = fmaf(ang, S.scale[b], -S.phase[b]);
+      idx = S.start[b] + wrapi((int)floorf(t + 0.5f), count);
+    } else if (S.kind[b] == BLK_SQUARE) {
+      const float h = S.radius[b];
+      const float px = x[0] - S.cx[b], py = x[1] - S.cy[b];
+      const float dr = fabsf(px - h), dt = fabsf(py - h), dl = fabsf(px + h), db = fabsf(py + h);
+      const float cpx = fminf(fmaxf(px, -h), h), cpy = fminf(fmaxf(py, -h), h);
+      float s = cpy + h, m = dr;
+      if (dt < m) { m = dt; s = 2.0f * h + (h - cpx); }
+      if (dl < m) { m = dl; s = 4.0f * h + (h - cpy); }
+      if (db < m) { m = db; s = 6.0f * h + (cpx + h); }
+      const float t = fmaf(s, S.scale[b], -S.phase[b]);
+      idx = S.start[b] + wrapi((int)floorf(t + 0.5f), count);
+    } else {
+      idx = brute<D>(S, x, S.start[b], count);
+    }
+    if (S.n_blk == 1) return idx;
+    const float t = d2_to<D>(__ldg(&S.anchors[idx]), x);
+    if (t < best || (t == best && idx < bi)) {
+      best = t;
+      bi = idx;
+    }
+  }
+  return bi;
+}
+
+// Steps per service phase and Philox blocks per batch.
+template <int D>
+struct Batch {
+  static constexpr int kSteps = 4;
+  static constexpr int kBlocks = D == 2 ? 1 : 2;
+};
+
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+__global__ void __launch_bounds__(256, 4) walk_bin_f32_kernel(const F32Params P) {
+  const WorkOut& W = P.w;
+  const PhiloxKey32 key = philox32_schedule(P.key0, P.key1);
+  float x[3] = {0.0f, 0.0f, 0.0f};
+  int steps = 0;
+  unsigned draw = 0, pid = 0;
+  long long pole = 0, rep_off = 0;
+  bool active = false, finished = false;
+  WarpPool wp;
+  pool_init(wp);
+  const float keep = 1.0f - P.shrink_rel;
+  for (;;) {
+    // ---- service: bin finished walks, refill idle lanes ----
+    const unsigned need = __ballot_sync(kFull, !active);
+    if (need) {
+      if (finished) {
+        finished = false;
+        int side = 0;
+        if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
+        else side = P.comp_side[0];
+        const int a = nearest_anchor<D>(P.side[side], x);
+        const int col = side ? W.col_off1 + a : a;
+        atomicAdd(&W.counts[pole * W.row_len + col], 1ULL);
+        const unsigned long long st = (unsigned long long)steps;
+        atomicAdd(&W.ssum[pole], st);
+        atomicAdd(&W.ssq[pole], st * st);
+        atomicMax(&W.smax[pole], st);
+      }
+      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 512u);
+      if (g != kNoWalk) {
+        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
+        const float4 p = __ldg(&P.poles[pole]);
+        x[0] = p.x;
+        x[1] = p.y;
+        x[2] = p.z;
+        pid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
+        steps = 0;
+        draw = 0;
+        active = true;
+      }
+      if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
+    }
+    // ---- a batch of steps on one or two Philox blocks ----
+    const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
+    unsigned wv[4 * Batch<D>::kBlocks];
+#pragma unroll
+    for (int b = 0; b < Batch<D>::kBlocks; ++b) {
+      const uint4 w = philox4x32_10(key, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
+                                    (unsigned)(rep >> 32));
+      wv[4 * b] = w.x;
+      wv[4 * b + 1] = w.y;
+      wv[4 * b + 2] = w.z;
+      wv[4 * b + 3] = w.w;
+    }
+    ++draw;
+#pragma unroll
+    for (int k = 0; k < Batch<D>::kSteps; ++k) {
+      if (!active) break;
+      float e, r;
+      dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+      if (e <= P.eps) {
+        active = false;
+        finished = true;
+        break;
+      }
+      if (steps >= P.max_steps) {
+        active = false;
+        atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
+        break;
+      }
+      float u0, u1, u2 = 0.0f;
+      if (D == 2) {
+        const float th = kPi * sym11_23(wv[k]);
+        __sincosf(th, &u1, &u0);
+      } else {
+        const float z = sym11_23(wv[2 * k]);
+        const float th = kPi * sym11_23(wv[2 * k + 1]);
+        const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+        float sn, cs;
+        __sincosf(th, &sn, &cs);
+        u0 = rho * cs;
+        u1 = rho * sn;
+        u2 = z;
+      }
+      float y0 = u0, y1 = u1, y2 = u2;
+      if (!IDENT) {
+        const float* A = P.A;
+        if (D == 2) {
+          y0 = fmaf(A[0], u0, A[1] * u1);
+          y1 = fmaf(A[2], u0, A[3] * u1);
+        } else {
+          y0 = fmaf(A[0], u0, fmaf(A[1], u1, A[2] * u2));
+          y1 = fmaf(A[3], u0, fmaf(A[4], u1, A[5] * u2));
+          y2 = fmaf(A[6], u0, fmaf(A[7], u1, A[8] * u2));
+        }
+      }
+      const float rs = fmaf(r, keep, -P.shrink_abs);
+      x[0] = fmaf(rs, y0, x[0]);
+      x[1] = fmaf(rs, y1, x[1]);
+      if (D == 3) x[2] = fmaf(rs, y2, x[2]);
+      ++steps;
+    }
+  }
+}
+
+// Exits mode for the FP32 path (em_run_exits with EM_PREC_FP32): same walk,
+// writes the exit point and component instead of binning.
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+__global__ void __launch_bounds__(256, 4) walk_exits_f32_kernel(const F32Params P) {
+  const WorkOut& W = P.w;
+  const PhiloxKey32 key = philox32_schedule(P.key0, P.key1);
+  float x[3] = {0.0f, 0.0f, 0.0f};
+  int steps = 0;
+  unsigned draw = 0, pid = 0;
+  long long pole = 0, rep_off = 0;
+  bool active = false, finished = false;
+  WarpPool wp;
+  pool_init(wp);
+  const float keep = 1.0f - P.shrink_rel;
+  for (;;) {
+    const unsigned need = __ballot_sync(kFull, !active);
+    if (need) {
+      if (finished) {
+        finished = false;
+        const long long o = pole * W.n_rep + rep_off;
+        for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j];
+        W.steps_out[o] = steps;
+        W.comp_out[o] = owner<D, OUTER, NH>(P, x);
+      }
+      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 512u);
+      if (g != kNoWalk) {
+        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
+        const float4 p = __ldg(&P.poles[pole]);
+        x[0] = p.x;
+        x[1] = p.y;
+        x[2] = p.z;
+        pid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
+        steps = 0;
+        draw = 0;
+        active = true;
+      }
+      if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
+    }
+    const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
+    unsigned wv[4 * Batch<D>::kBlocks];
+#pragma unroll
+    for (int b = 0; b < Batch<D>::kBlocks; ++b) {
+      const uint4 w = philox4x32_10(key, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
+                                    (unsigned)(rep >> 32));
+      wv[4 * b] = w.x;
+      wv[4 * b + 1] = w.y;
+      wv[4 * b + 2] = w.z;
+      wv[4 * b + 3] = w.w;
+    }
+    ++draw;
+#pragma unroll
+    for (int k = 0; k < Batch<D>::kSteps; ++k) {
+      if (!active) break;
+      float e, r;
+      dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+      if (e <= P.eps) {
+        active = false;
+        finished = true;
+        break;
+      }
+      if (steps >= P.max_steps) {
+        active = false;
+        atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
+        break;
+      }
+      float u0, u1, u2 = 0.0f;
+      if (D == 2) {
+        const float th = kPi * sym11_23(wv[k]);
+        __sincosf(th, &u1, &u0);
+      } else {
+        const float z = sym11_23(wv[2 * k]);
+        const float th = kPi * sym11_23(wv[2 * k + 1]);
+        const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+        float sn, cs;
+        __sincosf(th, &sn, &cs);
+        u0 = rho * cs;
+        u1 = rho * sn;
+        u2 = z;
+      }
+      float y0 = u0, y1 = u1, y2 = u2;
+      if (!IDENT) {
+        const float* A = P.A;
+        if (D == 2) {
+          y0 = fmaf(A[0], u0, A[1] * u1);
+          y1 = fmaf(A[2], u0, A[3] * u1);
+        } else {
+          y0 = fmaf(A[0], u0, fmaf(A[1], u1, A[2] * u2));
+          y1 = fmaf(A[3], u0, fmaf(A[4], u1, A[5] * u2));
+          y2 = fmaf(A[6], u0, fmaf(A[7], u1, A[8] * u2));
+        }
+      }
+      const float rs = fmaf(r, keep, -P.shrink_abs);
+      x[0] = fmaf(rs, y0, x[0]);
+      x[1] = fmaf(rs, y1, x[1]);
+      if (D == 3) x[2] = fmaf(rs, y2, x[2]);
+      ++steps;
+    }
+  }
+}
+
+}  // namespace f32
+
+// Host dispatch over the instantiated (dimension, outer, holes, chain, K=I)
+// combinations.  nh_mode: 0 = no holes, 1 = exactly one hole, 2 = runtime.
+template <int D, int OUTER, int NH>
+static cudaError_t launch_chain(const F32Params& P, int mode, int chain, bool ident, int grid,
+                                int block, cudaStream_t s) {
+#define EM_LAUNCH(CH, ID)                                                              \
+  do {                                                                                 \
+    if (mode == 0)                                                                     \
+      f32::walk_bin_f32_kernel<D, OUTER, NH, CH, ID><<<grid, block, 0, s>>>(P);        \
+    else                                                                               \
+      f32::walk_exits_f32_kernel<D, OUTER, NH, CH, ID><<<grid, block, 0, s>>>(P);      \
+  } while (0)
+  if (ident)
+    EM_LAUNCH(EM_CHAIN_WOE, true);
+  else if (chain == EM_CHAIN_MAX)
+    EM_LAUNCH(EM_CHAIN_MAX, false);
+  else
+    EM_LAUNCH(EM_CHAIN_WOE, false);
+#undef EM_LAUNCH
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
+                       bool ident, int grid, int block, cudaStream_t s) {
+  if (d == 2) {
+    if (outer == OUTER_BALL) {
+      if (nh_mode == 0) return launch_chain<2, OUTER_BALL, 0>(P, mode, chain, ident, grid, block, s);
+      if (nh_mode == 1) return launch_chain<2, OUTER_BALL, 1>(P, mode, chain, ident, grid, block, s);
+      return launch_chain<2, OUTER_BALL, -1>(P, mode, chain, ident, grid, block, s);
+    }
+    if (outer == OUTER_BOX) {
+      if (nh_mode == 0) return launch_chain<2, OUTER_BOX, 0>(P, mode, chain, ident, grid, block, s);
+      return launch_chain<2, OUTER_BOX, -1>(P, mode, chain, ident, grid, block, s);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (outer == OUTER_BALL) {
+    if (nh_mode == 0) return launch_chain<3, OUTER_BALL, 0>(P, mode, chain, ident, grid, block, s);
+    return launch_chain<3, OUTER_BALL, -1>(P, mode, chain, ident, grid, block, s);
+  }
+  if (outer == OUTER_BOX) {
+    if (nh_mode == 0) return launch_chain<3, OUTER_BOX, 0>(P, mode, chain, ident, grid, block, s);
+    return launch_chain<3, OUTER_BOX, -1>(P, mode, chain, ident, grid, block, s);
+  }
+  if (nh_mode == 0) return launch_chain<3, OUTER_LBOX, 0>(P, mode, chain, ident, grid, block, s);
+  return launch_chain<3, OUTER_LBOX, -1>(P, mode, chain, ident, grid, block, s);
+}
+
+// ---- FP32 issue-rate micro-benchmark (roofline denominator) ----
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], a, b);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += v[i];
+  if (s == 12345.678f) out[threadIdx.x] = s;
+}
+
+cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s) {
+  ffma_peak_kernel<<<grid, block, 0, s>>>(out, iters, 0.999999f, 1e-7f);
+  return cudaGetLastError();
+}
+
+// Philox4x32-10 known-answer hook (compared with curand in the tests).
+__global__ void philox32_kat_kernel(const unsigned* in, unsigned* out, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned* c = in + 6 * i;
+  const PhiloxKey32 k = philox32_schedule(c[4], c[5]);
+  const uint4 w = philox4x32_10(k, c[0], c[1], c[2], c[3]);
+  out[4 * i] = w.x;
+  out[4 * i + 1] = w.y;
+  out[4 * i + 2] = w.z;
+  out[4 * i + 3] = w.w;
+}
+
+cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s) {
+  philox32_kat_kernel<<<(n + 127) / 128, 128, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace em

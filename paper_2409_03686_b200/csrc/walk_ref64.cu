@@ -1,0 +1,345 @@
+// walk_ref64.cu -- bit-exact FP64 mirror of the reference walk kernel.
+//
+// Every expression restates S/_kernel.pyx (S/ = /root/reference/pkg/src/
+// exitmeasure/) with the same operand order; this translation unit is built
+// with -fmad=false so nvcc never contracts a*b+c into an FMA (the reference is
+// compiled by gcc -O2 without FMA), and double sqrt / division are IEEE
+// correctly rounded on the GPU.  The only non-IEEE-exact call, atan2, feeds
+// nothing but the centre of the +-2 candidate window of a uniform circle block
+// (S/_fallback.py:7-9), where an ulp of difference cannot change the winner.
+// Result: for identical packed inputs, counts / exits / steps equal the
+// reference kernel's bit for bit (tests/test_gpu_parity.py).
+//
+// Scheduling is the persistent refill of em_pool.cuh; accumulation is int64
+// atomics, so the result is independent of the schedule.
+#include <cuda_runtime.h>
+
+#include "em_params.cuh"
+#include "em_pool.cuh"
+#include "em_rng.cuh"
+
+namespace em {
+namespace r64 {
+
+__constant__ double kM2PI = 6.283185307179586476925286766559;
+constexpr double kInv53 = 1.0 / 9007199254740992.0;
+constexpr long long kBigIndex = 1LL << 62;
+
+// S/_kernel.pyx:57-81
+__device__ __forceinline__ void sample_direction(int d, unsigned long long seed,
+                                                 unsigned long long& draw,
+                                                 unsigned long long rep,
+                                                 unsigned long long pole, double* u) {
+  for (;;) {
+    u64x4 w = philox4x64_10(seed, 0ULL, draw, 0ULL, rep, pole);
+    draw += 1ULL;
+    double u0 = (double)(w.w0 >> 11) * kInv53;
+    double u1 = (double)(w.w1 >> 11) * kInv53;
+    double v1 = 2.0 * u0 - 1.0;
+    double v2 = 2.0 * u1 - 1.0;
+    double s = v1 * v1 + v2 * v2;
+    if (d == 2) {
+      if (s <= 1.0 && s > 0.0) {
+        double rs = sqrt(s);
+        u[0] = v1 / rs;
+        u[1] = v2 / rs;
+        return;
+      }
+    } else {
+      if (s < 1.0) {
+        double f = 2.0 * sqrt(1.0 - s);
+        u[0] = v1 * f;
+        u[1] = v2 * f;
+        u[2] = 1.0 - 2.0 * s;
+        return;
+      }
+    }
+  }
+}
+
+// S/_kernel.pyx:89-116
+__device__ double outer_signed(const Ref64Params& P, const double* x) {
+  const double* gf = P.gf;
+  const int d = P.d;
+  if (P.outer_kind == 0) {
+    double dx0 = x[0] - gf[0], dx1 = x[1] - gf[1];
+    double t = dx0 * dx0 + dx1 * dx1;
+    if (d == 3) {
+      double dx2 = x[2] - gf[2];
+      t = t + dx2 * dx2;
+    }
+    return gf[d] - sqrt(t);
+  }
+  double h = gf[d];
+  double q0 = fabs(x[0] - gf[0]) - h;
+  double q1 = fabs(x[1] - gf[1]) - h;
+  double m = q0;
+  if (q1 > m) m = q1;
+  double t = (q0 > 0.0 ? q0 : 0.0) * (q0 > 0.0 ? q0 : 0.0) +
+             (q1 > 0.0 ? q1 : 0.0) * (q1 > 0.0 ? q1 : 0.0);
+  if (d == 3) {
+    double q2 = fabs(x[2] - gf[2]) - h;
+    if (q2 > m) m = q2;
+    t = t + (q2 > 0.0 ? q2 : 0.0) * (q2 > 0.0 ? q2 : 0.0);
+  }
+  if (m <= 0.0) return -m;
+  return -sqrt(t);
+}
+
+// S/_kernel.pyx:119-130
+__device__ __forceinline__ double hole_dist(const Ref64Params& P, const double* x, int hole) {
+  const int d = P.d;
+  const int off = d + 1 + hole * (d + 1);
+  double dx0 = x[0] - P.gf[off], dx1 = x[1] - P.gf[off + 1];
+  double t = dx0 * dx0 + dx1 * dx1;
+  if (d == 3) {
+    double dx2 = x[2] - P.gf[off + 2];
+    t = t + dx2 * dx2;
+  }
+  return sqrt(t) - P.gf[off + d];
+}
+
+// L-box notch extension (same expression as oracle/em_oracle.c)
+__device__ __forceinline__ double notch_dist(const Ref64Params& P, const double* x) {
+  const int off = (P.d + 1) * (1 + P.n_holes);
+  double qx = P.gf[off] - x[0];
+  double qy = P.gf[off + 1] - x[1];
+  if (qx <= 0.0 && qy <= 0.0) return qx > qy ? qx : qy;
+  double ax = qx > 0.0 ? qx : 0.0;
+  double ay = qy > 0.0 ? qy : 0.0;
+  return sqrt(ax * ax + ay * ay);
+}
+
+// S/_kernel.pyx:133-142
+__device__ double signed_dist(const Ref64Params& P, const double* x) {
+  double sd = outer_signed(P, x);
+  for (int h = 0; h < P.n_holes; ++h) {
+    double hd = hole_dist(P, x, h);
+    if (hd < sd) sd = hd;
+  }
+  if (P.n_notch) {
+    double nd = notch_dist(P, x);
+    if (nd < sd) sd = nd;
+  }
+  return sd;
+}
+
+// S/_kernel.pyx:145-156
+__device__ int owner_component(const Ref64Params& P, const double* x) {
+  double best = fabs(outer_signed(P, x));
+  int comp = 0;
+  for (int h = 0; h < P.n_holes; ++h) {
+    double dd = fabs(hole_dist(P, x, h));
+    if (dd < best) {
+      best = dd;
+      comp = h + 1;
+    }
+  }
+  if (P.n_notch) {
+    double dd = fabs(notch_dist(P, x));
+    if (dd < best) comp = P.n_holes + 1;
+  }
+  return comp;
+}
+
+// S/_kernel.pyx:204-216
+__device__ __forceinline__ void lex_update(const double* x, int d, const double* anchors,
+                                           long long g, double& best_d2, long long& best_gi) {
+  const double* a = anchors + g * d;
+  double dx0 = x[0] - __ldg(a), dx1 = x[1] - __ldg(a + 1);
+  double t = dx0 * dx0 + dx1 * dx1;
+  if (d == 3) {
+    double dx2 = x[2] - __ldg(a + 2);
+    t = t + dx2 * dx2;
+  }
+  if (t < best_d2 || (t == best_d2 && g < best_gi)) {
+    best_d2 = t;
+    best_gi = g;
+  }
+}
+
+// S/_kernel.pyx:219-231
+__device__ __forceinline__ double square_signed(double cx, double cy, double h, const double* x) {
+  double q0 = fabs(x[0] - cx) - h;
+  double q1 = fabs(x[1] - cy) - h;
+  double m = q0;
+  if (q1 > m) m = q1;
+  if (m <= 0.0) return -m;
+  double t = (q0 > 0.0 ? q0 : 0.0) * (q0 > 0.0 ? q0 : 0.0) +
+             (q1 > 0.0 ? q1 : 0.0) * (q1 > 0.0 ? q1 : 0.0);
+  return -sqrt(t);
+}
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  if (v < lo) return lo;
+  if (v > hi) return hi;
+  return v;
+}
+
+__device__ __forceinline__ long long wrap(long long k, long long count) {
+  k = k % count;
+  if (k < 0) k += count;
+  return k;
+}
+
+// S/_kernel.pyx:242-320.  Extension: a block phase p (anchors at spacing*(k+p))
+// shifts the centre of the +-2 window by -p; the window still holds the
+// minimiser and its ties, so the lexicographic winner is unchanged and equals
+// the brute-force rule (S/weights.py:74-87).
+__device__ long long assign_anchor(const double* x, int d, const Side64& s) {
+  double best_d2 = 1e308;
+  long long best_gi = kBigIndex;
+  for (int b = 0; b < s.n_blk; ++b) {
+    const int kind = s.kind[b];
+    const long long start = s.start[b], count = s.count[b];
+    const double cx = s.cx[b], cy = s.cy[b], radius = s.radius[b], phase = s.phase[b];
+    if (kind == BLK_CIRCLE) {
+      double px = x[0] - cx, py = x[1] - cy;
+      double ang = atan2(py, px);
+      double t = ang * ((double)count / kM2PI);
+      if (phase != 0.0) t = t - phase;
+      long long k = wrap((long long)floor(t + 0.5), count);
+      for (int off = -2; off < 3; ++off)
+        lex_update(x, d, s.anchors, start + wrap(k + off, count), best_d2, best_gi);
+    } else if (kind == BLK_SQUARE) {
+      double spacing = 8.0 * radius / (double)count;
+      if (fabs(square_signed(cx, cy, radius, x)) <= 0.125 * spacing) {
+        double px = x[0] - cx, py = x[1] - cy;
+        double dr = fabs(px - radius), dt = fabs(py - radius);
+        double dl = fabs(px + radius), db = fabs(py + radius);
+        int edge = 0;
+        double m = dr, sarc;
+        if (dt < m) { m = dt; edge = 1; }
+        if (dl < m) { m = dl; edge = 2; }
+        if (db < m) { m = db; edge = 3; }
+        double cpx = clampd(px, -radius, radius), cpy = clampd(py, -radius, radius);
+        if (edge == 0) sarc = cpy + radius;
+        else if (edge == 1) sarc = 2.0 * radius + (radius - cpx);
+        else if (edge == 2) sarc = 4.0 * radius + (radius - cpy);
+        else sarc = 6.0 * radius + (cpx + radius);
+        double t = sarc * ((double)count / (8.0 * radius));
+        if (phase != 0.0) t = t - phase;
+        long long k = wrap((long long)floor(t + 0.5), count);
+        for (int off = -2; off < 3; ++off)
+          lex_update(x, d, s.anchors, start + wrap(k + off, count), best_d2, best_gi);
+      } else {
+        for (long long idx = 0; idx < count; ++idx)
+          lex_update(x, d, s.anchors, start + idx, best_d2, best_gi);
+      }
+    } else {
+      for (long long idx = 0; idx < count; ++idx)
+        lex_update(x, d, s.anchors, start + idx, best_d2, best_gi);
+    }
+  }
+  return best_gi;
+}
+
+// mode 0: accumulate counts + step statistics (accumulate_chunk / run_accumulate)
+// mode 1: write exit points, steps, components (walk_exits_chunk / run_exits)
+template <int MODE>
+__global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
+  const WorkOut& W = P.w;
+  const int d = P.d;
+  double x[3] = {0.0, 0.0, 0.0};
+  double u[3];
+  unsigned long long draw = 0, rep = 0, pid = 0;
+  long long steps = 0, pole = 0, rep_off = 0;
+  bool active = false;
+  WarpPool wp;
+  pool_init(wp);
+  for (;;) {
+    const unsigned need = __ballot_sync(kFull, !active);
+    if (need) {
+      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 256u);
+      if (g != kNoWalk) {
+        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
+        rep = (unsigned long long)(W.rep_start + rep_off);
+        pid = W.pole_ids ? (unsigned long long)W.pole_ids[pole] : (unsigned long long)pole;
+        for (int j = 0; j < d; ++j) x[j] = P.poles[pole * d + j];
+        draw = 0;
+        steps = 0;
+        active = true;
+      }
+      if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
+    }
+    if (!active) continue;
+    // S/_kernel.pyx:176-197
+    const double sd = signed_dist(P, x);
+    if (sd <= P.eps) {
+      active = false;
+      if (MODE == 0) {
+        const int comp = owner_component(P, x);
+        const int side = P.comp_side[comp];
+        const long long winner = assign_anchor(x, d, P.side[side]);
+        const long long col = side ? W.col_off1 + winner : winner;
+        atomicAdd(&W.counts[pole * W.row_len + col], 1ULL);
+        atomicAdd(&W.ssum[pole], (unsigned long long)steps);
+        atomicAdd(&W.ssq[pole], (unsigned long long)(steps * steps));
+        atomicMax(&W.smax[pole], (unsigned long long)steps);
+      } else {
+        const long long o = pole * W.n_rep + rep_off;
+        for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
+        W.steps_out[o] = steps;
+        W.comp_out[o] = owner_component(P, x);
+      }
+      continue;
+    }
+    if (steps >= P.max_steps) {
+      active = false;
+      atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
+      if (MODE == 1) {
+        const long long o = pole * W.n_rep + rep_off;
+        for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
+        W.steps_out[o] = steps;
+        W.comp_out[o] = 0;
+      }
+      continue;
+    }
+    sample_direction(d, P.seed, draw, rep, pid, u);
+    const double* k = P.ks;
+    if (d == 2) {
+      double y0 = k[0] * u[0] + k[1] * u[1];
+      double y1 = k[2] * u[0] + k[3] * u[1];
+      x[0] = x[0] + sd * y0;
+      x[1] = x[1] + sd * y1;
+    } else {
+      double y0 = k[0] * u[0] + k[1] * u[1] + k[2] * u[2];
+      double y1 = k[3] * u[0] + k[4] * u[1] + k[5] * u[2];
+      double y2 = k[6] * u[0] + k[7] * u[1] + k[8] * u[2];
+      x[0] = x[0] + sd * y0;
+      x[1] = x[1] + sd * y1;
+      x[2] = x[2] + sd * y2;
+    }
+    steps = steps + 1;
+  }
+}
+
+}  // namespace r64
+
+cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s) {
+  if (mode == 0)
+    r64::walk_ref64_kernel<0><<<grid, block, 0, s>>>(P);
+  else
+    r64::walk_ref64_kernel<1><<<grid, block, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+// Known-answer hook: Philox4x64-10 blocks for golden-vector tests.
+__global__ void philox64_kat_kernel(const unsigned long long* in, unsigned long long* out, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long* c = in + 6 * i;
+  u64x4 w = philox4x64_10(c[4], c[5], c[0], c[1], c[2], c[3]);  // (c0..c3, k0, k1)
+  out[4 * i] = w.w0;
+  out[4 * i + 1] = w.w1;
+  out[4 * i + 2] = w.w2;
+  out[4 * i + 3] = w.w3;
+}
+
+cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
+                                cudaStream_t s) {
+  philox64_kat_kernel<<<(n + 127) / 128, 128, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace em

@@ -1,0 +1,263 @@
+"""CUDA library vs the reference (golden fixtures) and the oracle -- B200 only.
+
+REF64 (the FP64 mirror) must be BIT-EXACT: exits, steps, components, count
+rows and step statistics equal the reference kernel's.  FP32 (production) is
+held to the statistical bar of SURVEY.md Appendix B plus exact row sums.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import (CASE_NAMES, bonferroni_z, case, exceed_quantile, poisson_cell_probs_disk,
+                     row_chi2_pvalues, side_tuple, two_sample_z)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2409_03686_b200 import _native, backend
+
+    _native.require_device(0)
+    return backend
+
+
+def test_library_loaded_from_tree(B):
+    import sys
+
+    from paper_2409_03686_b200 import _native
+
+    assert _native.device_count() >= 1
+    info = _native.device_info(0)
+    assert info["cc"][0] == 10, info  # sm_100
+    assert "libexitmeasure_b200" in str(_native.LIB_PATH)
+    assert "paper_2409_03686_b200" in sys.modules
+
+
+def test_philox4x64_matches_numpy_golden(B, golden_philox):
+    from paper_2409_03686_b200 import _native
+
+    g = golden_philox
+    rows = []
+    for key, ctr in zip(g["keys"], g["counters"]):
+        c = [int(v) for v in ctr]
+        c[0] = (c[0] + 1) % 2**64
+        if c[0] == 0:
+            c[1] = (c[1] + 1) % 2**64
+        rows.append(c + [int(key), 0])
+    out = _native.philox4x64_blocks(np.array(rows, dtype=np.uint64))
+    assert np.array_equal(out, g["numpy_raw"])
+    rin = g["ref_in"]  # (seed, k1, c0, c1, c2, c3)
+    rows = np.stack([rin[:, 2], rin[:, 3], rin[:, 4], rin[:, 5], rin[:, 0], rin[:, 1]], axis=1)
+    assert np.array_equal(_native.philox4x64_blocks(rows), g["ref_out"])
+
+
+def test_philox4x32_known_answers(B):
+    """Random123's published Philox4x32-10 known-answer vectors (kat_vectors):
+    zero / all-ones / pi-digit counters and keys."""
+    from paper_2409_03686_b200 import _native
+
+    rows = np.array([
+        [0, 0, 0, 0, 0, 0],
+        [0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff],
+        [0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344, 0xa4093822, 0x299f31d0],
+    ], dtype=np.uint32)
+    expect = np.array([
+        [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8],
+        [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd],
+        [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1],
+    ], dtype=np.uint32)
+    assert np.array_equal(_native.philox4x32_blocks(rows), expect)
+    assert np.array_equal(_native.philox4x32_blocks(rows, curand=True), expect)
+    rng = np.random.default_rng(5)
+    many = rng.integers(0, 2**32, size=(4096, 6), dtype=np.uint64).astype(np.uint32)
+    assert np.array_equal(_native.philox4x32_blocks(many),
+                          _native.philox4x32_blocks(many, curand=True))
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_ref64_walk_exits_bit_identical(B, golden_cases, name):
+    c = case(golden_cases, name)
+    x, st, comp, err = B.walk_exits_chunk(c["gi"], c["gf"], c["comp_side"], c["ksqrt"],
+                                          c["pole"], 2, 10, 210, 99, float(c["eps"]), 10**6)
+    assert err == -1
+    assert np.array_equal(x, c["x"])
+    assert np.array_equal(st, c["steps"])
+    assert np.array_equal(comp, c["comp"])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_ref64_accumulate_bit_identical(B, golden_cases, name):
+    c = case(golden_cases, name)
+    o0 = np.zeros(c["a0"].shape[0])
+    o1 = np.zeros(c["a1"].shape[0])
+    stats = B.accumulate_chunk(c["gi"], c["gf"], c["comp_side"], c["ksqrt"], c["pole"], 0, 0,
+                               3000, 7, float(c["eps"]), 10**6, *side_tuple(c, 0),
+                               *side_tuple(c, 1), o0, o1)
+    assert np.array_equal(o0, c["out0"]) and np.array_equal(o1, c["out1"])
+    assert list(stats) == [int(v) for v in c["stats"]]
+
+
+def test_ref64_budget_error_first_replicate(B, golden_cases):
+    c = case(golden_cases, "annulus")
+    res = B.accumulate_chunk(c["gi"], c["gf"], c["comp_side"], np.eye(2), np.array([0.95, 0.0]),
+                             0, 0, 50, 1, 1e-10, 2, *side_tuple(c, 0), *side_tuple(c, 1),
+                             np.zeros(c["a0"].shape[0]), np.zeros(c["a1"].shape[0]))
+    assert res[4] == int(golden_cases["budget_err"]) >= 0
+
+
+def test_ref64_chunk_split_invariance(B, golden_cases):
+    """T/test_backend.py:162-181 on the GPU path."""
+    c = case(golden_cases, "annulus")
+
+    def run(splits):
+        o0 = np.zeros(c["a0"].shape[0])
+        o1 = np.zeros(c["a1"].shape[0])
+        for r0, r1 in splits:
+            B.accumulate_chunk(c["gi"], c["gf"], c["comp_side"], np.eye(2), np.array([0.9, 0.0]),
+                               0, r0, r1, 3, 1e-8, 10**6, *side_tuple(c, 0), *side_tuple(c, 1),
+                               o0, o1)
+        return o0, o1
+
+    a = run([(0, 1000)])
+    b = run([(0, 137), (137, 640), (640, 1000)])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def _cfg(golden_cfg, idx):
+    from paper_2409_03686_b200 import configs
+
+    pre = f"cfg{idx}."
+    return configs.get(idx).subset(golden_cfg[pre + "poles"].shape[0],
+                                   int(golden_cfg[pre + "n_rep"]))
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_ref64_baseline_configs_bit_identical(B, golden_cfg, idx):
+    """The package's structured bins (phased circle / square blocks, generic
+    Fibonacci family) + the REF64 kernel reproduce the reference's
+    brute-force count rows and step statistics exactly."""
+    cfg = _cfg(golden_cfg, idx)
+    pre = f"cfg{idx}."
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    r = B.run_accumulate(cfg.dom, golden_cfg[pre + "ksqrt"], cfg.poles, cfg.seed, cfg.eps, 10**6,
+                         cfg.n_rep, s0, s1, precision="ref64")
+    assert np.array_equal(r.raw0, golden_cfg[pre + "raw0"])
+    assert np.array_equal(r.raw1, golden_cfg[pre + "raw1"])
+    assert np.array_equal(r.steps_sum, golden_cfg[pre + "steps_sum"])
+    assert np.array_equal(r.steps_sq_sum, golden_cfg[pre + "steps_sq"])
+    assert np.array_equal(r.steps_max, golden_cfg[pre + "steps_max"])
+
+
+def test_ref64_lbox_bit_identical_to_oracle(B, oracle):
+    """cfg5 (no reference expression): GPU mirror == C oracle, bit for bit."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(5).subset(8, 64)
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, 3, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 3, cfg.eps)
+    r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, cfg.n_rep,
+                         s0, s1, precision="ref64")
+    raw0, raw1, ss, sq, sm, _, err = oracle.run_accumulate_packed(
+        geom.gi, geom.gf, geom.comp_side, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
+        cfg.n_rep, (s0.anchors, s0.blk, s0.blkf), (s1.anchors, s1.blk, s1.blkf))
+    assert err is None
+    assert np.array_equal(r.raw0, raw0) and np.array_equal(r.raw1, raw1)
+    assert np.array_equal(r.steps_sum, ss) and np.array_equal(r.steps_max, sm)
+
+
+@pytest.mark.parametrize("precision", ["ref64", "fp32"])
+def test_row_shards_reproduce_full_run(B, precision):
+    """Rows sharded cyclically (pole i -> shard i mod 2) with their global
+    pole ids reproduce the single-run counts exactly."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(3).subset(16, 500)
+    s0 = B.pack_side(cfg.fam0, 2, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 2, cfg.eps)
+    full = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
+                            cfg.n_rep, s0, s1, precision=precision)
+    merged = np.zeros_like(full.counts)
+    for r in range(2):
+        ids = np.arange(r, cfg.n_poles, 2)
+        part = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles[ids], cfg.seed, cfg.eps,
+                                10**6, cfg.n_rep, s0, s1, precision=precision, pole_ids=ids)
+        merged[ids] = part.counts
+    assert np.array_equal(merged, full.counts)
+
+
+# ---------------------------------------------------------------------------
+# FP32 production kernel: statistical parity
+
+
+@pytest.mark.parametrize("chain", ["woe", "max"])
+def test_fp32_cfg1_matches_poisson_kernel(B, chain):
+    """cfg1 at full scale: every entry within the Bonferroni z of the exact
+    cell-integrated Poisson kernel, exceedances of |z|>4 within the 99.9%
+    quantile, exact row sums."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(1)
+    s0 = B.pack_side(cfg.fam0, 2, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 2, cfg.eps)
+    n = 10**5
+    r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, n, s0, s1,
+                         precision="fp32", chain=chain)
+    assert np.array_equal(r.counts.sum(1), np.full(cfg.n_poles, n))
+    zs = []
+    for i, p in enumerate(cfg.poles):
+        pj = poisson_cell_probs_disk(p, 128)
+        zs.append((r.raw1[i] / n - pj) / np.sqrt(pj * (1 - pj) / n))
+    z = np.abs(np.array(zs))
+    m = z.size
+    assert z.max() <= bonferroni_z(m), z.max()
+    assert int((z > 4).sum()) <= exceed_quantile(m)
+
+
+@pytest.mark.parametrize("idx,n_poles,n_fp32,n_ref", [(2, 32, 200_000, 20_000),
+                                                      (3, 32, 200_000, 20_000),
+                                                      (4, 16, 100_000, 10_000),
+                                                      (5, 8, 50_000, 2_000)])
+@pytest.mark.parametrize("chain", ["woe", "max"])
+def test_fp32_matches_oracle_statistically(B, oracle, idx, n_poles, n_fp32, n_ref, chain):
+    """FP32 counts vs the oracle's FP64 reference chain at reduced size:
+    exact row sums, max |z| under Bonferroni, |z|>4 exceedances under the
+    99.9% binomial quantile, per-row chi^2 homogeneity p-values not
+    collapsed (min p > 1e-4 / rows)."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(idx).subset(n_poles)
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, n_fp32,
+                         s0, s1, precision="fp32", chain=chain)
+    assert np.array_equal(r.counts.sum(1), np.full(cfg.n_poles, n_fp32))
+    raw0, raw1, *_ = oracle.run_accumulate_packed(
+        geom.gi, geom.gf, geom.comp_side, cfg.kt.k_sqrt, cfg.poles, cfg.seed + 1, cfg.eps, 10**6,
+        n_ref, (s0.anchors, s0.blk, s0.blkf), (s1.anchors, s1.blk, s1.blkf))
+    ref = np.concatenate([raw0, raw1], axis=1)
+    z = np.abs(two_sample_z(r.counts, n_fp32, ref, n_ref))
+    m = z.size
+    assert z.max() <= bonferroni_z(m), (z.max(), np.unravel_index(z.argmax(), z.shape))
+    assert int((z > 4).sum()) <= exceed_quantile(m)
+    p = row_chi2_pvalues(r.counts, n_fp32, ref, n_ref)
+    assert p.min() > 1e-4 / len(p), p.min()
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4, 5])
+def test_fp32_exits_stay_in_closure(B, idx):
+    """FP32 exit points lie within the eps-shell, up to 4 ulps outside."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.geometry import dist_to_boundary
+
+    cfg = configs.get(idx)
+    for pole_index in (0, cfg.n_poles // 2):
+        x, steps, comp = B.run_exits(cfg.dom, cfg.kt.k_sqrt, cfg.poles[pole_index], pole_index,
+                                     cfg.seed, cfg.eps, 10**6, 4000, precision="fp32")
+        sd = np.array([dist_to_boundary(cfg.dom, p) for p in x])
+        assert sd.max() <= cfg.eps * (1 + 1e-5) + 1e-7
+        assert sd.min() >= -4 * 2.0**-23, sd.min()
+        assert steps.min() >= 1
