@@ -23,7 +23,7 @@
 namespace em {
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s);
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
-                       bool ident, int grid, int block, cudaStream_t s);
+                       bool ident, int bink, int grid, int block, cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
@@ -81,7 +81,7 @@ struct DevBuf {
 
 struct em_plan {
   int device = 0, precision = EM_PREC_REF64, chain = EM_CHAIN_WOE;
-  int d = 2, outer = 0, n_holes = 0, n_notch = 0, nh_mode = 2;
+  int d = 2, outer = 0, n_holes = 0, n_notch = 0, nh_mode = 2, bink = 0;
   bool ident = false;
   int64_t n_poles = 0, n0 = 0, n1 = 0;
   int grid = 0, block = 256;
@@ -264,6 +264,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     return fail(EM_ERR_INVALID, "unknown precision");
   if (o.precision == EM_PREC_REF64 && o.chain != EM_CHAIN_WOE)
     return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
+  if (o.precision == EM_PREC_FP32 && o.block > 0 && o.block != 256)
+    return fail(EM_ERR_UNSUPPORTED, "the FP32 kernel runs 256-thread blocks");
   int ndev = em_device_count();
   if (o.device < 0 || o.device >= ndev)
     return fail(EM_ERR_CUDA, "no such CUDA device (" + std::to_string(ndev) + " visible)");
@@ -315,7 +317,6 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   w.inv_poles = 1.0 / (double)n_poles;
   w.pole_ids = pole_ids ? p->pole_ids.as<long long>() : nullptr;
   w.ticket = p->misc.as<unsigned long long>() + 1;
-  w.walks_done = p->misc.as<unsigned long long>() + 2;
   w.err_key = p->misc.as<unsigned long long>();
   w.counts = p->counts.as<unsigned long long>();
   w.row_len = (int)row;
@@ -462,6 +463,28 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     }
     P.w = w;
     p->nh_mode = nh == 0 ? 0 : ((nh == 1 && d == 2 && g->gi[1] == 0) ? 1 : 2);
+    // binner kind: one structured block per used side -> closed form
+    {
+      int kinds[2] = {-1, -1};
+      bool uniform = true;
+      for (int s2 = 0; s2 < 2; ++s2) {
+        if (!used[s2]) continue;
+        const Side32& D = P.side[s2];
+        int k = -1;
+        if (D.n_blk == 1 && D.kind[0] == BLK_CIRCLE) k = 1;
+        else if (D.n_blk == 1 && D.kind[0] == BLK_SQUARE) k = 2;
+        else if (D.has_grid) k = 3;
+        kinds[s2] = k;
+        if (k < 0) uniform = false;
+      }
+      int k = -1;
+      for (int s2 = 0; s2 < 2; ++s2)
+        if (used[s2]) {
+          if (k < 0) k = kinds[s2];
+          else if (k != kinds[s2]) uniform = false;
+        }
+      p->bink = (uniform && k > 0) ? k : 0;
+    }
   }
 #undef EM_ALLOC
   // persistent grid: SMs x resident blocks
@@ -481,6 +504,14 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   w->rep_start = rep_start;
   w->n_rep = n_rep;
   w->total = total;
+  // chunk size: enough chunks for ~8 per resident warp, 32..2048 replicates
+  {
+    const double warps = (double)p->grid * (p->block / 32);
+    long long rb = 32;
+    while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
+    w->rb = rb;
+    w->n_chunks = (unsigned long long)p->n_poles * (unsigned long long)((n_rep + rb - 1) / rb);
+  }
   w->counts = counts;
   w->ssum = stats;
   w->ssq = stats + p->n_poles;
@@ -506,8 +537,9 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     } else {
       p->p32.key0 = (unsigned)(seed & 0xffffffffULL);
       p->p32.key1 = (unsigned)(seed >> 32);
-      e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, grid,
-                     p->block, s);
+      p->p32.rk = philox32_schedule(p->p32.key0, p->p32.key1);
+      e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, p->bink,
+                     grid, p->block, s);
     }
     if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("walk kernel launch: ") + cudaGetErrorString(e));
     EM_CUDA(cudaEventRecord(p->ev1, s));

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/exitmeasure_b200.h"
+#include "em_rng.cuh"
 
 namespace em {
 
@@ -46,13 +47,14 @@ struct Side32 {
 // Work distribution and outputs common to every walk kernel.
 struct WorkOut {
   long long n_poles, rep_start, n_rep, total;  // total = n_poles * n_rep
-  double inv_poles;                            // 1/n_poles for g -> (rep, pole)
+  long long rb;                                // replicates per chunk
+  unsigned long long n_chunks;                 // n_poles * ceil(n_rep / rb)
+  double inv_poles;                            // 1/n_poles for chunk -> (block, pole)
   const long long* pole_ids;                   // RNG pole index per row
-  unsigned long long* ticket;                  // global walk counter
+  unsigned long long* ticket;                  // global chunk counter
   unsigned long long* counts;                  // (n_poles, row_len)
   int row_len, col_off1;                       // side-1 column offset
   unsigned long long *ssum, *ssq, *smax, *err_key;
-  unsigned long long* walks_done;              // exits binned (diagnostic)
   // exits mode (em_run_exits / walk_exits_chunk)
   double* x_out;
   long long* steps_out;
@@ -86,6 +88,7 @@ struct F32Params {
   float shrink_rel, shrink_abs;  // step safety margins
   int max_steps;
   unsigned key0, key1;
+  PhiloxKey32 rk;   // round keys of (key0, key1), set per run on the host
   const float4* poles;
   Side32 side[2];
   WorkOut w;

@@ -1,86 +1,122 @@
 // em_pool.cuh -- persistent-lane work distribution shared by the walk kernels.
 //
-// Walk ids g in [0, n_poles * n_rep) are pole-interleaved (pole = g mod M,
-// replicate = g div M), so the walks in flight at any moment are spread over
-// every pole: pole-dependent walk lengths balance out and exit atomics spread
-// over all M count rows.  Each warp claims CHUNK consecutive ids from one
-// global counter at a time (one atomic per CHUNK walks) and hands them to its
-// lanes as they finish, so a lane whose walk ended restarts immediately
-// instead of idling until the warp's longest walk ends (lockstep
-// without refill runs at 0.33 lane efficiency).  Results never depend on this
-// schedule: every walk's RNG stream is keyed by (seed, pole, replicate) and
-// all accumulations are integer.
+// Work unit = a CHUNK: (pole p, replicates [b*RB, b*RB + RB) of that pole),
+// chunk id c = b * n_poles + p, so consecutive chunk ids cycle over the poles
+// and the walks in flight at any moment are spread over all count rows
+// (pole-dependent walk lengths balance out; exit atomics spread over every
+// row).  A warp claims one chunk at a time with ONE global atomic and hands
+// its replicates to lanes as they finish, so a lane whose walk ended restarts
+// immediately instead of idling until the warp's longest walk ends (SURVEY F5:
+// lockstep without refill runs at 0.33 lane efficiency).  Because a lane's
+// consecutive walks mostly share a pole, per-pole step statistics are summed
+// in registers and flushed with one atomic triple per pole change instead of
+// three contended atomics per walk.  Results never depend on this schedule:
+// every walk's RNG stream is keyed by (seed, pole, replicate) and all
+// accumulations are integer.
 #pragma once
 #include "em_params.cuh"
 
 namespace em {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr unsigned long long kNoWalk = ~0ULL;
 
 struct WarpPool {
-  unsigned long long next, end;
+  long long rep0;    // first replicate offset of the current chunk
+  int pole;          // pole row of the current chunk
+  int next, end;     // next / one-past-last replicate index inside the chunk
   bool exhausted;
 };
 
 __device__ __forceinline__ void pool_init(WarpPool& wp) {
+  wp.rep0 = 0;
+  wp.pole = 0;
   wp.next = 0;
   wp.end = 0;
   wp.exhausted = false;
 }
 
-// Called by all 32 lanes (converged).  Lanes set in need_mask receive a walk
-// id or kNoWalk.
-__device__ __forceinline__ unsigned long long pool_take(WarpPool& wp, unsigned need_mask,
-                                                        unsigned long long* ticket,
-                                                        unsigned long long total,
-                                                        unsigned chunk) {
+// Called by all 32 lanes (converged).  Lanes set in need_mask receive
+// (pole, replicate offset) and return true, or return false (no work now).
+__device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, const WorkOut& W,
+                                          int& pole, long long& rep_off) {
   const int lane = threadIdx.x & 31;
-  const unsigned n_need = __popc(need_mask);
-  const unsigned rank = __popc(need_mask & ((1u << lane) - 1u));
+  const int n_need = __popc(need_mask);
+  const int rank = __popc(need_mask & ((1u << lane) - 1u));
   const bool me = (need_mask >> lane) & 1u;
-  const unsigned long long avail = wp.end - wp.next;
-  unsigned long long my = kNoWalk;
-  if (me && rank < avail) my = wp.next + rank;
+  const int avail = wp.end - wp.next;
+  bool got = false;
+  if (me && rank < avail) {
+    pole = wp.pole;
+    rep_off = wp.rep0 + wp.next + rank;
+    got = true;
+  }
   if (avail >= n_need) {
     wp.next += n_need;
-    return my;
+    return got;
   }
   wp.next = wp.end;
-  if (wp.exhausted) return my;
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(ticket, (unsigned long long)chunk);
-  base = __shfl_sync(kFull, base, 0);
-  if (base >= total) {
+  if (wp.exhausted) return got;
+  unsigned long long c = 0;
+  if (lane == 0) c = atomicAdd(W.ticket, 1ULL);
+  c = __shfl_sync(kFull, c, 0);
+  if (c >= W.n_chunks) {
     wp.exhausted = true;
-    return my;
+    return got;
   }
-  const unsigned long long end = base + chunk < total ? base + chunk : total;
-  const unsigned long long rem = n_need - avail;
-  if (me && rank >= avail) {
-    const unsigned long long gg = base + (rank - avail);
-    my = gg < end ? gg : kNoWalk;
+  // chunk c -> (replicate block b, pole p); exact for c < 2^53
+  long long b = (long long)((double)c * W.inv_poles);
+  long long p = (long long)c - b * W.n_poles;
+  if (p < 0) {
+    b -= 1;
+    p += W.n_poles;
+  } else if (p >= W.n_poles) {
+    b += 1;
+    p -= W.n_poles;
   }
-  wp.next = base + rem < end ? base + rem : end;
-  wp.end = end;
-  return my;
+  const long long r0 = b * W.rb;
+  const int valid = (int)(W.n_rep - r0 < W.rb ? W.n_rep - r0 : W.rb);
+  const int rem = n_need - avail;
+  if (me && rank >= avail && rank - avail < valid) {
+    pole = (int)p;
+    rep_off = r0 + (rank - avail);
+    got = true;
+  }
+  wp.pole = (int)p;
+  wp.rep0 = r0;
+  wp.next = rem < valid ? rem : valid;
+  wp.end = valid;
+  return got;
 }
 
-// g -> (replicate offset, pole row); exact for g < 2^53.
-__device__ __forceinline__ void split_walk(unsigned long long g, long long n_poles,
-                                           double inv_poles, long long& rep_off,
-                                           long long& pole) {
-  long long q = (long long)((double)g * inv_poles);
-  long long r = (long long)g - q * n_poles;
-  if (r < 0) {
-    q -= 1;
-    r += n_poles;
-  } else if (r >= n_poles) {
-    q += 1;
-    r -= n_poles;
+// Per-lane step statistics of the pole the lane is currently walking.
+struct StepAcc {
+  int pole;
+  unsigned long long sum, sq, mx;
+};
+
+__device__ __forceinline__ void acc_init(StepAcc& a) {
+  a.pole = -1;
+  a.sum = a.sq = a.mx = 0;
+}
+
+__device__ __forceinline__ void acc_flush(StepAcc& a, const WorkOut& W) {
+  if (a.pole >= 0 && a.sum + a.mx > 0) {
+    atomicAdd(&W.ssum[a.pole], a.sum);
+    atomicAdd(&W.ssq[a.pole], a.sq);
+    atomicMax(&W.smax[a.pole], a.mx);
   }
-  rep_off = q;
-  pole = r;
+  a.sum = a.sq = a.mx = 0;
+}
+
+__device__ __forceinline__ void acc_add(StepAcc& a, const WorkOut& W, int pole,
+                                        unsigned long long steps) {
+  if (pole != a.pole) {
+    acc_flush(a, W);
+    a.pole = pole;
+  }
+  a.sum += steps;
+  a.sq += steps * steps;
+  a.mx = steps > a.mx ? steps : a.mx;
 }
 
 }  // namespace em

@@ -51,17 +51,21 @@ __host__ __device__ inline PhiloxKey32 philox32_schedule(unsigned key0, unsigned
   return s;
 }
 
+// One 32x32 -> 64 multiply (IMAD.WIDE.U32) yields both halves of a round's
+// product; the round keys come from K (kernel params: constant-bank operands
+// of the LOP3s), so a block costs 20 IMAD.WIDE + 20 LOP3.
 __device__ __forceinline__ uint4 philox4x32_10(const PhiloxKey32& K, unsigned c0, unsigned c1,
                                                unsigned c2, unsigned c3) {
   const unsigned M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    unsigned hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
-    unsigned hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
-    unsigned n0 = hi1 ^ c1 ^ K.k0[r], n2 = hi0 ^ c3 ^ K.k1[r];
-    c0 = n0;
+    const unsigned long long p0 = (unsigned long long)M0 * c0;
+    const unsigned long long p1 = (unsigned long long)M1 * c2;
+    const unsigned hi0 = (unsigned)(p0 >> 32), lo0 = (unsigned)p0;
+    const unsigned hi1 = (unsigned)(p1 >> 32), lo1 = (unsigned)p1;
+    c0 = hi1 ^ c1 ^ K.k0[r];
     c1 = lo1;
-    c2 = n2;
+    c2 = hi0 ^ c3 ^ K.k1[r];
     c3 = lo0;
   }
   return make_uint4(c0, c1, c2, c3);

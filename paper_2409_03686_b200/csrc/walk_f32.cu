@@ -172,9 +172,10 @@ __device__ __forceinline__ int owner(const F32Params& P, const float* x) {
   return comp;
 }
 
+// k in [-count, 2 count): wrap without an integer division
 __device__ __forceinline__ int wrapi(int k, int count) {
-  k = k % count;
-  return k < 0 ? k + count : k;
+  k = k < 0 ? k + count : k;
+  return k >= count ? k - count : k;
 }
 
 template <int D>
@@ -262,162 +263,221 @@ __device__ int nearest_anchor(const Side32& S, const float* x) {
   return bi;
 }
 
-// Steps per service phase and Philox blocks per batch.
+// Binner kinds, fixed at compile time per plan (capi.cu picks the kind):
+//   BIN_ANY    -- runtime walk over the side's blocks (nearest_anchor above)
+//   BIN_CIRCLE -- every used side is ONE uniform circle block: index by angle
+//   BIN_SQUARE -- every used side is ONE uniform square block: index by arc
+//   BIN_GRID   -- every used side is ONE generic family with a candidate grid
+// Side fields are selected branch-free from the two constant-bank copies, so
+// nothing is indexed dynamically in parameter space.
+enum BinKind { BIN_ANY = 0, BIN_CIRCLE = 1, BIN_SQUARE = 2, BIN_GRID = 3 };
+
+template <class T>
+__device__ __forceinline__ T pick(int side, T a, T b) {
+  return side ? b : a;
+}
+
+template <int D, int BINK>
+__device__ __forceinline__ int bin_exit(const F32Params& P, int side, const float* x) {
+  const Side32& S0 = P.side[0];
+  const Side32& S1 = P.side[1];
+  if (BINK == BIN_CIRCLE) {
+    const float ang = atan2f(x[1] - pick(side, S0.cy[0], S1.cy[0]),
+                             x[0] - pick(side, S0.cx[0], S1.cx[0]));
+    const float t = fmaf(ang, pick(side, S0.scale[0], S1.scale[0]),
+                         -pick(side, S0.phase[0], S1.phase[0]));
+    return wrapi((int)floorf(t + 0.5f), pick(side, S0.count[0], S1.count[0]));
+  } else if (BINK == BIN_SQUARE) {
+    const float h = pick(side, S0.radius[0], S1.radius[0]);
+    const float px = x[0] - pick(side, S0.cx[0], S1.cx[0]);
+    const float py = x[1] - pick(side, S0.cy[0], S1.cy[0]);
+    const float dr = fabsf(px - h), dt = fabsf(py - h), dl = fabsf(px + h), db = fabsf(py + h);
+    const float cpx = fminf(fmaxf(px, -h), h), cpy = fminf(fmaxf(py, -h), h);
+    float s = cpy + h, m = dr;
+    if (dt < m) { m = dt; s = 2.0f * h + (h - cpx); }
+    if (dl < m) { m = dl; s = 4.0f * h + (h - cpy); }
+    if (db < m) { m = db; s = 6.0f * h + (cpx + h); }
+    const float t = fmaf(s, pick(side, S0.scale[0], S1.scale[0]),
+                         -pick(side, S0.phase[0], S1.phase[0]));
+    return wrapi((int)floorf(t + 0.5f), pick(side, S0.count[0], S1.count[0]));
+  } else if (BINK == BIN_GRID) {
+    const float4* anchors = pick(side, S0.anchors, S1.anchors);
+    const float inv_h = pick(side, S0.grid.inv_h, S1.grid.inv_h);
+    const int ix = (int)floorf((x[0] - pick(side, S0.grid.lo[0], S1.grid.lo[0])) * inv_h);
+    const int iy = (int)floorf((x[1] - pick(side, S0.grid.lo[1], S1.grid.lo[1])) * inv_h);
+    const int iz = D == 3 ? (int)floorf((x[2] - pick(side, S0.grid.lo[2], S1.grid.lo[2])) * inv_h) : 0;
+    const int nx = pick(side, S0.grid.n[0], S1.grid.n[0]);
+    const int ny = pick(side, S0.grid.n[1], S1.grid.n[1]);
+    const int nz = pick(side, S0.grid.n[2], S1.grid.n[2]);
+    const int na = pick(side, S0.n_anchors, S1.n_anchors);
+    unsigned off = 0, cnt = 255u;
+    if (ix >= 0 && iy >= 0 && iz >= 0 && ix < nx && iy < ny && iz < nz) {
+      const unsigned w = __ldg(&pick(side, S0.grid.cell, S1.grid.cell)[(iz * ny + iy) * nx + ix]);
+      cnt = w & 255u;
+      off = w >> 8;
+    }
+    const unsigned* cand = pick(side, S0.grid.cand, S1.grid.cand);
+    const bool brute = cnt == 255u;
+    const int n = brute ? na : (int)cnt;
+    float best = kInf;
+    int bi = 0;
+    for (int j = 0; j < n; ++j) {
+      const int a = brute ? j : (int)__ldg(&cand[off + j]);
+      const float t = d2_to<D>(__ldg(&anchors[a]), x);
+      if (t < best || (t == best && a < bi)) {
+        best = t;
+        bi = a;
+      }
+    }
+    return bi;
+  } else {
+    return nearest_anchor<D>(side ? S1 : S0, x);
+  }
+}
+
+// Steps per service phase and Philox blocks per batch: 2D uses one 32-bit
+// word per step (4 steps per block), 3D two words (2 steps per block).
 template <int D>
 struct Batch {
   static constexpr int kSteps = 4;
   static constexpr int kBlocks = D == 2 ? 1 : 2;
 };
 
-template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
-__global__ void __launch_bounds__(256, 4) walk_bin_f32_kernel(const F32Params P) {
-  const WorkOut& W = P.w;
-  const PhiloxKey32 key = philox32_schedule(P.key0, P.key1);
-  float x[3] = {0.0f, 0.0f, 0.0f};
-  int steps = 0;
-  unsigned draw = 0, pid = 0;
-  long long pole = 0, rep_off = 0;
-  bool active = false, finished = false;
-  WarpPool wp;
-  pool_init(wp);
-  const float keep = 1.0f - P.shrink_rel;
-  for (;;) {
-    // ---- service: bin finished walks, refill idle lanes ----
-    const unsigned need = __ballot_sync(kFull, !active);
-    if (need) {
-      if (finished) {
-        finished = false;
-        int side = 0;
-        if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
-        else side = P.comp_side[0];
-        const int a = nearest_anchor<D>(P.side[side], x);
-        const int col = side ? W.col_off1 + a : a;
-        atomicAdd(&W.counts[pole * W.row_len + col], 1ULL);
-        const unsigned long long st = (unsigned long long)steps;
-        atomicAdd(&W.ssum[pole], st);
-        atomicAdd(&W.ssq[pole], st * st);
-        atomicMax(&W.smax[pole], st);
-      }
-      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 512u);
-      if (g != kNoWalk) {
-        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
-        const float4 p = __ldg(&P.poles[pole]);
-        x[0] = p.x;
-        x[1] = p.y;
-        x[2] = p.z;
-        pid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
-        steps = 0;
-        draw = 0;
-        active = true;
-      }
-      if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
-    }
-    // ---- a batch of steps on one or two Philox blocks ----
-    const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
-    unsigned wv[4 * Batch<D>::kBlocks];
-#pragma unroll
-    for (int b = 0; b < Batch<D>::kBlocks; ++b) {
-      const uint4 w = philox4x32_10(key, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
-                                    (unsigned)(rep >> 32));
-      wv[4 * b] = w.x;
-      wv[4 * b + 1] = w.y;
-      wv[4 * b + 2] = w.z;
-      wv[4 * b + 3] = w.w;
-    }
-    ++draw;
-#pragma unroll
-    for (int k = 0; k < Batch<D>::kSteps; ++k) {
-      if (!active) break;
-      float e, r;
-      dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-      if (e <= P.eps) {
-        active = false;
-        finished = true;
-        break;
-      }
-      if (steps >= P.max_steps) {
-        active = false;
-        atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
-        break;
-      }
-      float u0, u1, u2 = 0.0f;
-      if (D == 2) {
-        const float th = kPi * sym11_23(wv[k]);
-        __sincosf(th, &u1, &u0);
-      } else {
-        const float z = sym11_23(wv[2 * k]);
-        const float th = kPi * sym11_23(wv[2 * k + 1]);
-        const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
-        float sn, cs;
-        __sincosf(th, &sn, &cs);
-        u0 = rho * cs;
-        u1 = rho * sn;
-        u2 = z;
-      }
-      float y0 = u0, y1 = u1, y2 = u2;
-      if (!IDENT) {
-        const float* A = P.A;
-        if (D == 2) {
-          y0 = fmaf(A[0], u0, A[1] * u1);
-          y1 = fmaf(A[2], u0, A[3] * u1);
-        } else {
-          y0 = fmaf(A[0], u0, fmaf(A[1], u1, A[2] * u2));
-          y1 = fmaf(A[3], u0, fmaf(A[4], u1, A[5] * u2));
-          y2 = fmaf(A[6], u0, fmaf(A[7], u1, A[8] * u2));
-        }
-      }
-      const float rs = fmaf(r, keep, -P.shrink_abs);
-      x[0] = fmaf(rs, y0, x[0]);
-      x[1] = fmaf(rs, y1, x[1]);
-      if (D == 3) x[2] = fmaf(rs, y2, x[2]);
-      ++steps;
+// One walk-on-ellipsoids step from x (r from dist()): direction from the RNG
+// word(s), y = K^{1/2} u, x += rs y with rs = r shrunk by the FP32 safety
+// margin, or rs = 0 for a lane that is not walking (branch-free: the warp
+// issues the same instructions whether or not every lane is live).
+template <int D, bool IDENT>
+__device__ __forceinline__ void step(const F32Params& P, float* x, float rs, unsigned w0,
+                                     unsigned w1) {
+  float u0, u1, u2 = 0.0f;
+  if (D == 2) {
+    const float th = kPi * sym11_23(w0);
+    __sincosf(th, &u1, &u0);
+  } else {
+    const float z = sym11_23(w0);
+    const float th = kPi * sym11_23(w1);
+    const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+    float sn, cs;
+    __sincosf(th, &sn, &cs);
+    u0 = rho * cs;
+    u1 = rho * sn;
+    u2 = z;
+  }
+  float y0 = u0, y1 = u1, y2 = u2;
+  if (!IDENT) {
+    if (D == 2) {
+      y0 = fmaf(P.A[0], u0, P.A[1] * u1);
+      y1 = fmaf(P.A[2], u0, P.A[3] * u1);
+    } else {
+      y0 = fmaf(P.A[0], u0, fmaf(P.A[1], u1, P.A[2] * u2));
+      y1 = fmaf(P.A[3], u0, fmaf(P.A[4], u1, P.A[5] * u2));
+      y2 = fmaf(P.A[6], u0, fmaf(P.A[7], u1, P.A[8] * u2));
     }
   }
+  x[0] = fmaf(rs, y0, x[0]);
+  x[1] = fmaf(rs, y1, x[1]);
+  if (D == 3) x[2] = fmaf(rs, y2, x[2]);
 }
 
-// Exits mode for the FP32 path (em_run_exits with EM_PREC_FP32): same walk,
-// writes the exit point and component instead of binning.
-template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
-__global__ void __launch_bounds__(256, 4) walk_exits_f32_kernel(const F32Params P) {
+// lane status
+enum : int { ST_IDLE = 0, ST_WALK = 1, ST_DONE = 2, ST_FAIL = 3 };
+
+constexpr int kWarps = 8;   // 256 threads per block
+constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
+
+// Bin one exit (owner component -> side -> nearest anchor), count it, and
+// add its step count to this lane's per-pole accumulator.
+template <int D, int OUTER, int NH, int BINK>
+__device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
+                                       StepAcc& acc) {
   const WorkOut& W = P.w;
-  const PhiloxKey32 key = philox32_schedule(P.key0, P.key1);
+  int side;
+  if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
+  else side = P.comp_side[0];
+  const int a = bin_exit<D, BINK>(P, side, x);
+  const int col = side ? W.col_off1 + a : a;
+  atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+  acc_add(acc, W, pole, (unsigned long long)steps);
+}
+
+// MODE 0: bin exits into the count rows + per-pole step statistics
+// MODE 1: write exit points / steps / components (em_run_exits)
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK>
+__global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
+  const WorkOut& W = P.w;
+  __shared__ float4 q_x[kWarps][kQueue];  // exit point, pole (as int bits in .w)
+  __shared__ int q_s[kWarps][kQueue];     // steps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int qn = 0;  // queued exits of this warp (warp-uniform)
   float x[3] = {0.0f, 0.0f, 0.0f};
-  int steps = 0;
+  float px = 0.0f, py = 0.0f, pz = 0.0f;  // this lane's cached pole (start point)
+  int cpole = -1;
+  int steps = 0, pole = 0, st = ST_IDLE;
   unsigned draw = 0, pid = 0;
-  long long pole = 0, rep_off = 0;
-  bool active = false, finished = false;
+  long long rep_off = 0;
   WarpPool wp;
   pool_init(wp);
+  StepAcc acc;
+  acc_init(acc);
   const float keep = 1.0f - P.shrink_rel;
   for (;;) {
-    const unsigned need = __ballot_sync(kFull, !active);
+    // ---- service: retire finished walks, refill idle lanes ----
+    const unsigned need = __ballot_sync(kFull, st != ST_WALK);
     if (need) {
-      if (finished) {
-        finished = false;
-        const long long o = pole * W.n_rep + rep_off;
+      if (MODE == 0) {
+        const unsigned done = __ballot_sync(kFull, st == ST_DONE);
+        if (done) {
+          if (st == ST_DONE) {
+            const int slot = qn + __popc(done & lt);
+            q_x[warp][slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
+            q_s[warp][slot] = steps;
+          }
+          qn += __popc(done);
+          __syncwarp();
+          if (qn >= 32) {  // bin 32 queued exits with every lane active
+            const int slot = qn - 32 + lane;
+            const float4 e = q_x[warp][slot];
+            const float ex[3] = {e.x, e.y, e.z};
+            retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][slot], acc);
+            qn -= 32;
+            __syncwarp();
+          }
+        }
+      } else if (st == ST_DONE) {
+        const long long o = (long long)pole * W.n_rep + rep_off;
         for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
-      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 512u);
-      if (g != kNoWalk) {
-        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
-        const float4 p = __ldg(&P.poles[pole]);
-        x[0] = p.x;
-        x[1] = p.y;
-        x[2] = p.z;
+      if (st == ST_FAIL)
+        atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
+      st = st == ST_WALK ? ST_WALK : ST_IDLE;
+      if (pool_take(wp, need, W, pole, rep_off)) {
+        if (pole != cpole) {
+          const float4 p = __ldg(&P.poles[pole]);
+          px = p.x;
+          py = p.y;
+          pz = p.z;
+          cpole = pole;
+        }
+        x[0] = px;
+        x[1] = py;
+        x[2] = pz;
         pid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
         steps = 0;
         draw = 0;
-        active = true;
+        st = ST_WALK;
       }
-      if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
+      if (wp.exhausted && __ballot_sync(kFull, st == ST_WALK) == 0) break;
     }
+    // ---- a batch of steps on one or two Philox blocks, branch-free ----
     const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
     unsigned wv[4 * Batch<D>::kBlocks];
 #pragma unroll
     for (int b = 0; b < Batch<D>::kBlocks; ++b) {
-      const uint4 w = philox4x32_10(key, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
+      const uint4 w = philox4x32_10(P.rk, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
                                     (unsigned)(rep >> 32));
       wv[4 * b] = w.x;
       wv[4 * b + 1] = w.y;
@@ -425,69 +485,48 @@ __global__ void __launch_bounds__(256, 4) walk_exits_f32_kernel(const F32Params 
       wv[4 * b + 3] = w.w;
     }
     ++draw;
+    bool walking = st == ST_WALK;
 #pragma unroll
     for (int k = 0; k < Batch<D>::kSteps; ++k) {
-      if (!active) break;
       float e, r;
       dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-      if (e <= P.eps) {
-        active = false;
-        finished = true;
-        break;
-      }
-      if (steps >= P.max_steps) {
-        active = false;
-        atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
-        break;
-      }
-      float u0, u1, u2 = 0.0f;
-      if (D == 2) {
-        const float th = kPi * sym11_23(wv[k]);
-        __sincosf(th, &u1, &u0);
-      } else {
-        const float z = sym11_23(wv[2 * k]);
-        const float th = kPi * sym11_23(wv[2 * k + 1]);
-        const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
-        float sn, cs;
-        __sincosf(th, &sn, &cs);
-        u0 = rho * cs;
-        u1 = rho * sn;
-        u2 = z;
-      }
-      float y0 = u0, y1 = u1, y2 = u2;
-      if (!IDENT) {
-        const float* A = P.A;
-        if (D == 2) {
-          y0 = fmaf(A[0], u0, A[1] * u1);
-          y1 = fmaf(A[2], u0, A[3] * u1);
-        } else {
-          y0 = fmaf(A[0], u0, fmaf(A[1], u1, A[2] * u2));
-          y1 = fmaf(A[3], u0, fmaf(A[4], u1, A[5] * u2));
-          y2 = fmaf(A[6], u0, fmaf(A[7], u1, A[8] * u2));
-        }
-      }
-      const float rs = fmaf(r, keep, -P.shrink_abs);
-      x[0] = fmaf(rs, y0, x[0]);
-      x[1] = fmaf(rs, y1, x[1]);
-      if (D == 3) x[2] = fmaf(rs, y2, x[2]);
-      ++steps;
+      const bool stop = walking && e <= P.eps;
+      const bool over = walking && !stop && steps >= P.max_steps;
+      st = stop ? ST_DONE : (over ? ST_FAIL : st);
+      walking = walking && !stop && !over;
+      const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
+      if (D == 2)
+        step<D, IDENT>(P, x, rs, wv[k], 0u);
+      else
+        step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
+      steps += walking ? 1 : 0;
     }
+  }
+  if (MODE == 0) {
+    if (lane < qn) {  // drain the queue
+      const float4 e = q_x[warp][lane];
+      const float ex[3] = {e.x, e.y, e.z};
+      retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][lane], acc);
+    }
+    acc_flush(acc, W);
   }
 }
 
 }  // namespace f32
 
-// Host dispatch over the instantiated (dimension, outer, holes, chain, K=I)
-// combinations.  nh_mode: 0 = no holes, 1 = exactly one hole, 2 = runtime.
-template <int D, int OUTER, int NH>
+// Host dispatch over the instantiated (dimension, outer, holes, chain, K=I,
+// binner) combinations.  nh_mode: 0 = no holes, 1 = exactly one hole, 2 =
+// runtime count.  Specialised binners exist where a BASELINE config needs
+// them; everything else takes BIN_ANY.
+template <int D, int OUTER, int NH, int BINK>
 static cudaError_t launch_chain(const F32Params& P, int mode, int chain, bool ident, int grid,
                                 int block, cudaStream_t s) {
 #define EM_LAUNCH(CH, ID)                                                              \
   do {                                                                                 \
     if (mode == 0)                                                                     \
-      f32::walk_bin_f32_kernel<D, OUTER, NH, CH, ID><<<grid, block, 0, s>>>(P);        \
+      f32::walk_f32_kernel<D, OUTER, NH, CH, ID, 0, BINK><<<grid, block, 0, s>>>(P);   \
     else                                                                               \
-      f32::walk_exits_f32_kernel<D, OUTER, NH, CH, ID><<<grid, block, 0, s>>>(P);      \
+      f32::walk_f32_kernel<D, OUTER, NH, CH, ID, 1, f32::BIN_ANY><<<grid, block, 0, s>>>(P); \
   } while (0)
   if (ident)
     EM_LAUNCH(EM_CHAIN_WOE, true);
@@ -499,30 +538,48 @@ static cudaError_t launch_chain(const F32Params& P, int mode, int chain, bool id
   return cudaGetLastError();
 }
 
+template <int D, int OUTER, int NH, int B1, int B2>
+static cudaError_t launch_bin(const F32Params& P, int mode, int chain, bool ident, int bink,
+                              int grid, int block, cudaStream_t s) {
+  if (mode == 0 && bink == B1 && B1 != f32::BIN_ANY)
+    return launch_chain<D, OUTER, NH, B1>(P, mode, chain, ident, grid, block, s);
+  if (mode == 0 && bink == B2 && B2 != f32::BIN_ANY)
+    return launch_chain<D, OUTER, NH, B2>(P, mode, chain, ident, grid, block, s);
+  return launch_chain<D, OUTER, NH, f32::BIN_ANY>(P, mode, chain, ident, grid, block, s);
+}
+
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
-                       bool ident, int grid, int block, cudaStream_t s) {
+                       bool ident, int bink, int grid, int block, cudaStream_t s) {
+  using namespace f32;
+  if (block != 32 * kWarps) return cudaErrorInvalidConfiguration;
   if (d == 2) {
     if (outer == OUTER_BALL) {
-      if (nh_mode == 0) return launch_chain<2, OUTER_BALL, 0>(P, mode, chain, ident, grid, block, s);
-      if (nh_mode == 1) return launch_chain<2, OUTER_BALL, 1>(P, mode, chain, ident, grid, block, s);
-      return launch_chain<2, OUTER_BALL, -1>(P, mode, chain, ident, grid, block, s);
+      if (nh_mode == 0)
+        return launch_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+      if (nh_mode == 1)
+        return launch_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+      return launch_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
     }
     if (outer == OUTER_BOX) {
-      if (nh_mode == 0) return launch_chain<2, OUTER_BOX, 0>(P, mode, chain, ident, grid, block, s);
-      return launch_chain<2, OUTER_BOX, -1>(P, mode, chain, ident, grid, block, s);
+      if (nh_mode == 0)
+        return launch_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(P, mode, chain, ident, bink, grid, block, s);
+      return launch_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
     }
     return cudaErrorInvalidValue;
   }
   if (outer == OUTER_BALL) {
-    if (nh_mode == 0) return launch_chain<3, OUTER_BALL, 0>(P, mode, chain, ident, grid, block, s);
-    return launch_chain<3, OUTER_BALL, -1>(P, mode, chain, ident, grid, block, s);
+    if (nh_mode == 0)
+      return launch_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+    return launch_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
   }
   if (outer == OUTER_BOX) {
-    if (nh_mode == 0) return launch_chain<3, OUTER_BOX, 0>(P, mode, chain, ident, grid, block, s);
-    return launch_chain<3, OUTER_BOX, -1>(P, mode, chain, ident, grid, block, s);
+    if (nh_mode == 0)
+      return launch_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+    return launch_bin<3, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
   }
-  if (nh_mode == 0) return launch_chain<3, OUTER_LBOX, 0>(P, mode, chain, ident, grid, block, s);
-  return launch_chain<3, OUTER_LBOX, -1>(P, mode, chain, ident, grid, block, s);
+  if (nh_mode == 0)
+    return launch_bin<3, OUTER_LBOX, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+  return launch_bin<3, OUTER_LBOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
 }
 
 // ---- FP32 issue-rate micro-benchmark (roofline denominator) ----
@@ -550,7 +607,7 @@ __global__ void philox32_kat_kernel(const unsigned* in, unsigned* out, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned* c = in + 6 * i;
-  const PhiloxKey32 k = philox32_schedule(c[4], c[5]);
+  const PhiloxKey32 k = philox32_schedule(c[4], c[5]);  // KAT only
   const uint4 w = philox4x32_10(k, c[0], c[1], c[2], c[3]);
   out[4 * i] = w.x;
   out[4 * i + 1] = w.y;

@@ -243,16 +243,17 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   double x[3] = {0.0, 0.0, 0.0};
   double u[3];
   unsigned long long draw = 0, rep = 0, pid = 0;
-  long long steps = 0, pole = 0, rep_off = 0;
+  long long steps = 0, rep_off = 0;
+  int pole = 0;
   bool active = false;
   WarpPool wp;
   pool_init(wp);
+  StepAcc acc;
+  acc_init(acc);
   for (;;) {
     const unsigned need = __ballot_sync(kFull, !active);
     if (need) {
-      const unsigned long long g = pool_take(wp, need, W.ticket, W.total, 256u);
-      if (g != kNoWalk) {
-        split_walk(g, W.n_poles, W.inv_poles, rep_off, pole);
+      if (pool_take(wp, need, W, pole, rep_off)) {
         rep = (unsigned long long)(W.rep_start + rep_off);
         pid = W.pole_ids ? (unsigned long long)W.pole_ids[pole] : (unsigned long long)pole;
         for (int j = 0; j < d; ++j) x[j] = P.poles[pole * d + j];
@@ -272,12 +273,10 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
         const int side = P.comp_side[comp];
         const long long winner = assign_anchor(x, d, P.side[side]);
         const long long col = side ? W.col_off1 + winner : winner;
-        atomicAdd(&W.counts[pole * W.row_len + col], 1ULL);
-        atomicAdd(&W.ssum[pole], (unsigned long long)steps);
-        atomicAdd(&W.ssq[pole], (unsigned long long)(steps * steps));
-        atomicMax(&W.smax[pole], (unsigned long long)steps);
+        atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+        acc_add(acc, W, pole, (unsigned long long)steps);
       } else {
-        const long long o = pole * W.n_rep + rep_off;
+        const long long o = (long long)pole * W.n_rep + rep_off;
         for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = owner_component(P, x);
@@ -286,9 +285,9 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     }
     if (steps >= P.max_steps) {
       active = false;
-      atomicMin(W.err_key, (unsigned long long)(pole * W.n_rep + rep_off));
+      atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
       if (MODE == 1) {
-        const long long o = pole * W.n_rep + rep_off;
+        const long long o = (long long)pole * W.n_rep + rep_off;
         for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = 0;
@@ -312,6 +311,7 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     }
     steps = steps + 1;
   }
+  if (MODE == 0) acc_flush(acc, W);
 }
 
 }  // namespace r64

@@ -28,6 +28,24 @@ def two_sample_z(c1, n1, c2, n2):
     return z
 
 
+def exact_two_sample_p(c1, n1, c2, n2):
+    """Entry-wise exact conditional test of equal binomial rates: given the
+    pooled count T = c1 + c2, c1 ~ Binomial(T, n1/(n1+n2)) under H0; two-
+    sided p-value.  Valid at any count (Appendix B's low-count caveat)."""
+    from scipy.stats import binom
+
+    c1 = np.asarray(c1, dtype=float)
+    c2 = np.asarray(c2, dtype=float)
+    t = c1 + c2
+    q = n1 / (n1 + n2)
+    lo = binom.cdf(c1, t, q)
+    hi = binom.sf(c1 - 1, t, q)
+    return np.minimum(1.0, 2.0 * np.minimum(lo, hi))
+
+
+P_Z4 = 6.334248366623996e-05  # two-sided P(|Z| > 4)
+
+
 def bonferroni_z(m_entries, alpha=0.05):
     """Two-sided Bonferroni threshold Phi^-1(1 - alpha/(2m))."""
     from scipy.stats import norm

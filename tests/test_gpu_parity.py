@@ -216,16 +216,19 @@ def test_fp32_cfg1_matches_poisson_kernel(B, chain):
     assert int((z > 4).sum()) <= exceed_quantile(m)
 
 
-@pytest.mark.parametrize("idx,n_poles,n_fp32,n_ref", [(2, 32, 200_000, 20_000),
-                                                      (3, 32, 200_000, 20_000),
-                                                      (4, 16, 100_000, 10_000),
-                                                      (5, 8, 50_000, 2_000)])
+@pytest.mark.parametrize("idx,n_poles,n_fp32,n_ref", [(2, 32, 400_000, 50_000),
+                                                      (3, 32, 400_000, 30_000),
+                                                      (4, 16, 200_000, 10_000),
+                                                      (5, 8, 100_000, 2_000)])
 @pytest.mark.parametrize("chain", ["woe", "max"])
 def test_fp32_matches_oracle_statistically(B, oracle, idx, n_poles, n_fp32, n_ref, chain):
-    """FP32 counts vs the oracle's FP64 reference chain at reduced size:
-    exact row sums, max |z| under Bonferroni, |z|>4 exceedances under the
-    99.9% binomial quantile, per-row chi^2 homogeneity p-values not
-    collapsed (min p > 1e-4 / rows)."""
+    """FP32 counts vs the oracle's FP64 reference chain at reduced size
+    (SURVEY.md Appendix B): exact row sums; entry-wise EXACT conditional
+    binomial tests -- min p above the Bonferroni level 0.01/MN, and the
+    number of entries with p < P(|Z|>4) within the 99.9% binomial quantile of
+    a perfect implementation; per-row chi^2 homogeneity p-values not
+    collapsed."""
+    from helpers import P_Z4, exact_two_sample_p
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(idx).subset(n_poles)
@@ -239,12 +242,13 @@ def test_fp32_matches_oracle_statistically(B, oracle, idx, n_poles, n_fp32, n_re
         geom.gi, geom.gf, geom.comp_side, cfg.kt.k_sqrt, cfg.poles, cfg.seed + 1, cfg.eps, 10**6,
         n_ref, (s0.anchors, s0.blk, s0.blkf), (s1.anchors, s1.blk, s1.blkf))
     ref = np.concatenate([raw0, raw1], axis=1)
-    z = np.abs(two_sample_z(r.counts, n_fp32, ref, n_ref))
-    m = z.size
-    assert z.max() <= bonferroni_z(m), (z.max(), np.unravel_index(z.argmax(), z.shape))
-    assert int((z > 4).sum()) <= exceed_quantile(m)
-    p = row_chi2_pvalues(r.counts, n_fp32, ref, n_ref)
-    assert p.min() > 1e-4 / len(p), p.min()
+    p = exact_two_sample_p(r.counts, n_fp32, ref, n_ref)
+    m = p.size
+    worst = np.unravel_index(p.argmin(), p.shape)
+    assert p.min() >= 0.01 / m, (p.min(), worst, r.counts[worst], ref[worst])
+    assert int((p < P_Z4).sum()) <= exceed_quantile(m)
+    rows = row_chi2_pvalues(r.counts, n_fp32, ref, n_ref)
+    assert rows.min() > 1e-3 / len(rows), rows.min()
 
 
 @pytest.mark.parametrize("idx", [2, 3, 4, 5])
