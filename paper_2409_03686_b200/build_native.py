@@ -32,7 +32,8 @@ NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 UNITS = [
     # (source, extra flags)
     ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]),
-    ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false"]),
+    ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false",
+                     f"-DEM_BATCH_STEPS={os.environ.get('EM_BATCH_STEPS', '8')}"]),
     ("capi.cu", []),
     ("kat_curand.cu", []),
 ]

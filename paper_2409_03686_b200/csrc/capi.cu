@@ -497,6 +497,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
 static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, int mode,
                        unsigned long long* counts, unsigned long long* stats, cudaStream_t s) {
   if (n_rep < 0 || rep_start < 0) return fail(EM_ERR_INVALID, "negative replicate range");
+  if (p->precision == EM_PREC_FP32 && n_rep > 2147483647LL)
+    return fail(EM_ERR_UNSUPPORTED, "FP32 path: at most 2^31-1 replicates per pole per run");
   const int64_t total = p->n_poles * n_rep;
   if (n_rep > 0 && total / n_rep != p->n_poles) return fail(EM_ERR_INVALID, "walk count overflows");
   if ((double)total > 9.0e15) return fail(EM_ERR_INVALID, "walk count too large");

@@ -37,8 +37,9 @@ __device__ __forceinline__ void pool_init(WarpPool& wp) {
 
 // Called by all 32 lanes (converged).  Lanes set in need_mask receive
 // (pole, replicate offset) and return true, or return false (no work now).
+template <class RepT>
 __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, const WorkOut& W,
-                                          int& pole, long long& rep_off) {
+                                          int& pole, RepT& rep_off) {
   const int lane = threadIdx.x & 31;
   const int n_need = __popc(need_mask);
   const int rank = __popc(need_mask & ((1u << lane) - 1u));
@@ -47,7 +48,7 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
   bool got = false;
   if (me && rank < avail) {
     pole = wp.pole;
-    rep_off = wp.rep0 + wp.next + rank;
+    rep_off = (RepT)(wp.rep0 + wp.next + rank);
     got = true;
   }
   if (avail >= n_need) {
@@ -78,7 +79,7 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
   const int rem = n_need - avail;
   if (me && rank >= avail && rank - avail < valid) {
     pole = (int)p;
-    rep_off = r0 + (rank - avail);
+    rep_off = (RepT)(r0 + (rank - avail));
     got = true;
   }
   wp.pole = (int)p;

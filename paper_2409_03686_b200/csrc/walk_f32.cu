@@ -337,26 +337,36 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
 
 // Steps per service phase and Philox blocks per batch: 2D uses one 32-bit
 // word per step (4 steps per block), 3D two words (2 steps per block).
+#ifndef EM_BATCH_STEPS
+#define EM_BATCH_STEPS 8
+#endif
 template <int D>
 struct Batch {
-  static constexpr int kSteps = 4;
-  static constexpr int kBlocks = D == 2 ? 1 : 2;
+  static constexpr int kSteps = EM_BATCH_STEPS;
+  static constexpr int kBlocks = D == 2 ? EM_BATCH_STEPS / 4 : EM_BATCH_STEPS / 2;
 };
 
 // One walk-on-ellipsoids step from x (r from dist()): direction from the RNG
 // word(s), y = K^{1/2} u, x += rs y with rs = r shrunk by the FP32 safety
 // margin, or rs = 0 for a lane that is not walking (branch-free: the warp
 // issues the same instructions whether or not every lane is live).
+// Uniform angle on the circle from a word's top 23 bits with ONE FFMA:
+// f = 1 + m/2^23 in [1,2) -> theta = 2 pi f - 3 pi in [-pi, pi).  The 2^23
+// angles are equally spaced around the circle, so the offset is irrelevant.
+__device__ __forceinline__ float angle23(unsigned w) {
+  const float f = __uint_as_float(0x3f800000u | (w >> 9));
+  return fmaf(f, 6.283185307179586f, -9.42477796076938f);
+}
+
 template <int D, bool IDENT>
 __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, unsigned w0,
                                      unsigned w1) {
   float u0, u1, u2 = 0.0f;
   if (D == 2) {
-    const float th = kPi * sym11_23(w0);
-    __sincosf(th, &u1, &u0);
+    __sincosf(angle23(w0), &u1, &u0);
   } else {
     const float z = sym11_23(w0);
-    const float th = kPi * sym11_23(w1);
+    const float th = angle23(w1);
     const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
     float sn, cs;
     __sincosf(th, &sn, &cs);
@@ -414,95 +424,115 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
   float x[3] = {0.0f, 0.0f, 0.0f};
   float px = 0.0f, py = 0.0f, pz = 0.0f;  // this lane's cached pole (start point)
   int cpole = -1;
-  int steps = 0, pole = 0, st = ST_IDLE;
-  unsigned draw = 0, pid = 0;
-  long long rep_off = 0;
+  unsigned cpid = 0;
+  int steps = 0, pole = 0, rep_off = 0;
+  unsigned draw = 0, rep_lo = 0, rep_hi = 0;
+  bool walking = false, done = false, failed = false;
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
   acc_init(acc);
   const float keep = 1.0f - P.shrink_rel;
+  constexpr int K = Batch<D>::kSteps;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
-    const unsigned need = __ballot_sync(kFull, st != ST_WALK);
+    const unsigned need = __ballot_sync(kFull, !walking);
     if (need) {
       if (MODE == 0) {
-        const unsigned done = __ballot_sync(kFull, st == ST_DONE);
+        const unsigned dm = __ballot_sync(kFull, done);
         if (done) {
-          if (st == ST_DONE) {
-            const int slot = qn + __popc(done & lt);
-            q_x[warp][slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
-            q_s[warp][slot] = steps;
-          }
-          qn += __popc(done);
-          __syncwarp();
-          if (qn >= 32) {  // bin 32 queued exits with every lane active
-            const int slot = qn - 32 + lane;
-            const float4 e = q_x[warp][slot];
-            const float ex[3] = {e.x, e.y, e.z};
-            retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][slot], acc);
-            qn -= 32;
-            __syncwarp();
-          }
+          const int slot = qn + __popc(dm & lt);
+          q_x[warp][slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
+          q_s[warp][slot] = steps;
         }
-      } else if (st == ST_DONE) {
+        qn += __popc(dm);
+        if (qn >= 32) {  // bin 32 queued exits with every lane active
+          __syncwarp();
+          const int slot = qn - 32 + lane;
+          const float4 e = q_x[warp][slot];
+          const float ex[3] = {e.x, e.y, e.z};
+          retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][slot], acc);
+          qn -= 32;
+          __syncwarp();
+        }
+      } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
         for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
-      if (st == ST_FAIL)
+      if (failed)
         atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
-      st = st == ST_WALK ? ST_WALK : ST_IDLE;
+      done = failed = false;
       if (pool_take(wp, need, W, pole, rep_off)) {
         if (pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
           px = p.x;
           py = p.y;
           pz = p.z;
+          cpid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
           cpole = pole;
         }
         x[0] = px;
         x[1] = py;
         x[2] = pz;
-        pid = W.pole_ids ? (unsigned)W.pole_ids[pole] : (unsigned)pole;
+        const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
+        rep_lo = (unsigned)rep;
+        rep_hi = (unsigned)(rep >> 32);
         steps = 0;
         draw = 0;
-        st = ST_WALK;
+        walking = true;
       }
-      if (wp.exhausted && __ballot_sync(kFull, st == ST_WALK) == 0) break;
+      if (wp.exhausted && __ballot_sync(kFull, walking) == 0) break;
     }
-    // ---- a batch of steps on one or two Philox blocks, branch-free ----
-    const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
+    // ---- a batch of K steps on one or two Philox blocks, branch-free ----
     unsigned wv[4 * Batch<D>::kBlocks];
 #pragma unroll
     for (int b = 0; b < Batch<D>::kBlocks; ++b) {
-      const uint4 w = philox4x32_10(P.rk, draw * Batch<D>::kBlocks + b, (unsigned)rep, pid,
-                                    (unsigned)(rep >> 32));
+      const uint4 w = philox4x32_10(P.rk, draw * Batch<D>::kBlocks + b, rep_lo, cpid, rep_hi);
       wv[4 * b] = w.x;
       wv[4 * b + 1] = w.y;
       wv[4 * b + 2] = w.z;
       wv[4 * b + 3] = w.w;
     }
     ++draw;
-    bool walking = st == ST_WALK;
+    if (__all_sync(kFull, steps + K <= P.max_steps)) {
+      // fast path: no lane can reach the step budget inside this batch
 #pragma unroll
-    for (int k = 0; k < Batch<D>::kSteps; ++k) {
-      float e, r;
-      dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-      const bool stop = walking && e <= P.eps;
-      const bool over = walking && !stop && steps >= P.max_steps;
-      st = stop ? ST_DONE : (over ? ST_FAIL : st);
-      walking = walking && !stop && !over;
-      const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
-      if (D == 2)
-        step<D, IDENT>(P, x, rs, wv[k], 0u);
-      else
-        step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
-      steps += walking ? 1 : 0;
+      for (int k = 0; k < K; ++k) {
+        float e, r;
+        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+        const bool stop = walking && e <= P.eps;
+        done = done || stop;
+        walking = walking && !stop;
+        const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
+        if (D == 2)
+          step<D, IDENT>(P, x, rs, wv[k], 0u);
+        else
+          step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
+        steps += walking;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        float e, r;
+        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+        const bool stop = walking && e <= P.eps;
+        const bool over = walking && !stop && steps >= P.max_steps;
+        done = done || stop;
+        failed = failed || over;
+        walking = walking && !stop && !over;
+        const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
+        if (D == 2)
+          step<D, IDENT>(P, x, rs, wv[k], 0u);
+        else
+          step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
+        steps += walking;
+      }
     }
   }
   if (MODE == 0) {
+    __syncwarp();
     if (lane < qn) {  // drain the queue
       const float4 e = q_x[warp][lane];
       const float ex[3] = {e.x, e.y, e.z};
