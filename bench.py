@@ -39,12 +39,13 @@ sys.path.insert(0, str(ROOT))
 # sqrt/rsqrt/div/sin/cos are XU ops, counted separately; RNG separately).
 # Derivation per term is in DESIGN.md ("F_step of the implemented kernels").
 F_STEP = {
-    # (cfg, chain): (fp32 ops, xu ops)
-    (1, "woe"): (15, 3), (1, "max"): (15, 3),
-    (2, "woe"): (19, 2), (2, "max"): (23, 2),
-    (3, "woe"): (27, 4), (3, "max"): (49, 8),
-    (4, "woe"): (32, 4), (4, "max"): (50, 6),
-    (5, "woe"): (35, 4), (5, "max"): (45, 4),
+    # (cfg, chain): (fp32 ops, xu ops) -- DESIGN.md "F_step of the implemented
+    # kernels" derives each entry term by term from walk_f32.cu
+    (1, "woe"): (13, 3), (1, "max"): (13, 3),   # K = I: both chains are the sphere step
+    (2, "woe"): (18, 2), (2, "max"): (21, 2),
+    (3, "woe"): (24, 4), (3, "max"): (58, 10),
+    (4, "woe"): (31, 4), (4, "max"): (51, 7),
+    (5, "woe"): (43, 4), (5, "max"): (53, 4),
 }
 
 
@@ -177,7 +178,7 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
     return walks / dt, float(ss.sum()) / dt, "port", dt, float(ss.sum()) / walks
 
 
-REF_SAMPLE = {1: 10_000, 2: 4096, 3: 256, 4: 64, 5: 16}
+REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
 
 
 def run_reference(args):

@@ -58,19 +58,66 @@ static int fail(int code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 // plan
 
+// Per-device caching allocator: plans come and go per API call (the one-shot
+// run_accumulate creates and destroys one), so device buffers, streams and
+// events are recycled instead of paying cudaMalloc/cudaFree (which also
+// synchronises the device) on every call.
+struct BufCache {
+  std::mutex mu;
+  std::vector<std::pair<size_t, void*>> free_bufs;  // (capacity, ptr) per device below
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+static BufCache& cache_of(int dev) {
+  static std::mutex mu;
+  static std::vector<BufCache*> caches;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)caches.size() <= dev) caches.resize(dev + 1, nullptr);
+  if (!caches[dev]) caches[dev] = new BufCache();
+  return *caches[dev];
+}
+
+static size_t round_cap(size_t n) {
+  size_t c = 256;
+  while (c < n) c <<= 1;
+  return c;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  ~DevBuf() {
-    if (p) cudaFree(p);
+  int dev = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (!p) return;
+    BufCache& c = cache_of(dev);
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.free_bufs.push_back({bytes, p});
+    p = nullptr;
+    bytes = 0;
   }
   cudaError_t alloc(size_t n) {
     if (n <= bytes && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 16));
-    if (e == cudaSuccess) bytes = n;
+    release();
+    cudaGetDevice(&dev);
+    const size_t cap = round_cap(std::max<size_t>(n, 16));
+    {
+      BufCache& c = cache_of(dev);
+      std::lock_guard<std::mutex> lk(c.mu);
+      for (size_t i = 0; i < c.free_bufs.size(); ++i)
+        if (c.free_bufs[i].first == cap) {
+          p = c.free_bufs[i].second;
+          bytes = cap;
+          c.free_bufs.erase(c.free_bufs.begin() + i);
+          return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(&p, cap);
+    if (e == cudaSuccess) bytes = cap;
+    else p = nullptr;
     return e;
   }
   template <class T>
@@ -78,6 +125,44 @@ struct DevBuf {
     return reinterpret_cast<T*>(p);
   }
 };
+
+static cudaStream_t take_stream(int dev) {
+  BufCache& c = cache_of(dev);
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.streams.empty()) {
+      cudaStream_t s = c.streams.back();
+      c.streams.pop_back();
+      return s;
+    }
+  }
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return s;
+}
+
+static cudaEvent_t take_event(int dev) {
+  BufCache& c = cache_of(dev);
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.events.empty()) {
+      cudaEvent_t e = c.events.back();
+      c.events.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+static void give_back(int dev, cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1) {
+  BufCache& c = cache_of(dev);
+  std::lock_guard<std::mutex> lk(c.mu);
+  if (s) c.streams.push_back(s);
+  if (e0) c.events.push_back(e0);
+  if (e1) c.events.push_back(e1);
+}
 
 struct em_plan {
   int device = 0, precision = EM_PREC_REF64, chain = EM_CHAIN_WOE;
@@ -94,11 +179,7 @@ struct em_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_walks = 0, last_steps = 0, last_launches = 0;
-  ~em_plan() {
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
-  }
+  ~em_plan() { give_back(device, stream, ev0, ev1); }
 };
 
 namespace {
@@ -158,6 +239,36 @@ double sym_min_eig(const double* a_in, int d) {
   double m = a[0][0];
   for (int i = 1; i < d; ++i) m = std::min(m, a[i][i]);
   return m;
+}
+
+// Host-side cache of candidate grids: building one is a deterministic
+// function of (anchors, d, eps) and costs up to ~0.1-1 s for 8k anchors, so
+// repeated plans over the same bins (one per API call) reuse it.
+bool cached_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G) {
+  uint64_t h = 1469598103934665603ULL;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ULL;
+  };
+  mix(anchors, (size_t)m * d * sizeof(double));
+  mix(&m, sizeof(m));
+  mix(&d, sizeof(d));
+  mix(&eps, sizeof(eps));
+  static std::mutex mu;
+  static std::vector<std::pair<uint64_t, GridHost>> lru;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : lru)
+      if (e.first == h) {
+        G = e.second;
+        return true;
+      }
+  }
+  if (!build_grid(anchors, m, d, eps, G)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (lru.size() >= 8) lru.erase(lru.begin());
+  lru.push_back({h, G});
+  return true;
 }
 
 int validate_geometry(const em_geometry* g) {
@@ -287,8 +398,10 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     delete p;
     return code;
   };
-  if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess)
+  p->stream = take_stream(o.device);
+  p->ev0 = take_event(o.device);
+  p->ev1 = take_event(o.device);
+  if (!p->stream || !p->ev0 || !p->ev1)
     return bail(fail(EM_ERR_CUDA, std::string("stream/event: ") + cudaGetErrorString(cudaGetLastError())));
 
   bool ident = true;
@@ -444,7 +557,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       // one generic block covering the family: accelerate with the grid
       if (D.n_blk == 1 && D.kind[0] == BLK_GENERIC && S->n_anchors > 8) {
         GridHost G;
-        if (build_grid(S->anchors, S->n_anchors, d, eps, G)) {
+        if (cached_grid(S->anchors, S->n_anchors, d, eps, G)) {
           EM_ALLOC(p->gcell[s], G.cell.size() * 4);
           EM_ALLOC(p->gcand[s], G.cand.size() * 4);
           if (cudaMemcpy(p->gcell[s].p, G.cell.data(), G.cell.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||

@@ -1,0 +1,76 @@
+"""Row sharding of the exit-measure matrix across GPUs.
+
+Rows of A (poles) are independent, and every walk's RNG stream is keyed by
+its GLOBAL pole id, so any partition of the rows reproduces the single-GPU
+counts exactly.  Poles go to ranks cyclically (pole i -> rank i mod N), which
+balances pole-dependent walk lengths (SURVEY hard part 9).  The one exchange
+step is an all-gather of the int64 count rows and step statistics over
+torch.distributed -- NCCL over NVLink/NVSwitch on the GPU box, gloo in the CPU
+tests.  One process per GPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .backend import AccumulateResult, Plan, pack_geometry
+
+
+def shard_rows(n_poles: int, world: int, rank: int) -> np.ndarray:
+    """Global pole ids owned by ``rank`` (cyclic)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return np.arange(rank, n_poles, world, dtype=np.int64)
+
+
+def gather_rows(local, n_poles: int, world: int, group=None):
+    """All-gather per-rank row blocks (shard order from shard_rows) into the
+    full (n_poles, ...) tensor on every rank.  ``local`` is a torch tensor
+    whose first dimension is this rank's shard length."""
+    import torch
+    import torch.distributed as dist
+
+    m_pad = -(-n_poles // world)
+    pad = torch.zeros((m_pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    out = torch.empty((n_poles,) + tuple(local.shape[1:]), dtype=local.dtype,
+                      device=local.device)
+    for r in range(world):
+        ids = torch.as_tensor(shard_rows(n_poles, world, r), device=local.device)
+        out[ids] = parts[r][: ids.numel()]
+    return out
+
+
+def run_accumulate_sharded(dom, ksqrt, poles, seed: int, eps: float, max_steps: int,
+                           n_rep: int, side0, side1, *, precision: str | None = None,
+                           chain: str | None = None, group=None) -> AccumulateResult:
+    """run_accumulate over all ranks of the default (or given) process group:
+    each rank walks its cyclic row shard on its own GPU (LOCAL_RANK), the
+    rows are all-gathered, and every rank returns the full result."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    poles = np.ascontiguousarray(poles, dtype=np.float64)
+    ids = shard_rows(poles.shape[0], world, rank)
+    geom = pack_geometry(dom)
+    with Plan(geom, ksqrt, poles[ids], eps, max_steps, side0, side1, precision, chain, device,
+              pole_ids=ids) as plan:
+        res = plan.run(seed, n_rep)
+    dev = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    counts = torch.as_tensor(res.counts, device=dev)
+    stats = torch.as_tensor(np.stack([res.steps_sum, res.steps_sq_sum, res.steps_max], 1),
+                            device=dev)
+    full_counts = gather_rows(counts, poles.shape[0], world, group).cpu().numpy()
+    full_stats = gather_rows(stats, poles.shape[0], world, group).cpu().numpy()
+    n0 = side0.size
+    return AccumulateResult(full_counts[:, :n0].astype(np.float64),
+                            full_counts[:, n0:].astype(np.float64), full_stats[:, 0].copy(),
+                            full_stats[:, 1].copy(), full_stats[:, 2].copy(), 0, full_counts,
+                            res.kernel_ms)

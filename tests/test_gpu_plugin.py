@@ -1,0 +1,88 @@
+"""The drop-in: the UNMODIFIED reference package (oracle/_ref) with this
+backend installed produces the reference's own results bit for bit -- mc_rem
+bundles and the CLI's CSV outputs (the T/test_backend.py:177-195 criterion,
+here compiled-CPU vs CUDA instead of compiled vs fallback).  B200 only."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "oracle" / "_ref"
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not (REF / "exitmeasure").exists():
+        pytest.skip("oracle/_ref not built")
+    sys.path.insert(0, str(REF))
+    import exitmeasure.backend as rb
+
+    return rb
+
+
+def _annulus_bundle(n=4000, seed=17):
+    from exitmeasure.conductivity import identity_tensor
+    from exitmeasure.estimator import make_measurements, mc_rem
+    from exitmeasure.geometry import catalog, circle_points, side_points
+    from exitmeasure.walk import WalkConfig
+    from exitmeasure.weights import voronoi_family
+
+    dom = catalog("annulus")
+    fam1 = voronoi_family(side_points(dom, "gamma1", [40]), dom)
+    fam0 = voronoi_family(side_points(dom, "gamma0", [80]), dom)
+    poles = circle_points(np.zeros(2), 0.95, 8).points
+    meas = make_measurements(dom, poles, np.zeros(8))
+    return mc_rem(dom, identity_tensor(2), meas, fam1, fam0, WalkConfig(eps=1e-8, seed=seed), n)
+
+
+def test_mc_rem_bit_identical_through_plugin(ref):
+    from paper_2409_03686_b200 import plugin
+
+    saved = (ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND)
+    cpu = _annulus_bundle()
+    try:
+        plugin.install(precision="ref64", module=ref)
+        assert ref.BACKEND == "cuda-ref64"
+        gpu = _annulus_bundle()
+    finally:
+        ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND = saved
+    for name in ("a0", "a1", "lambda_nu", "steps_mean", "steps_std", "steps_max"):
+        assert np.array_equal(getattr(cpu, name), getattr(gpu, name)), name
+
+
+def test_budget_error_is_the_reference_class(ref):
+    from exitmeasure.errors import WalkBudgetError
+    from exitmeasure.geometry import catalog
+    from exitmeasure.walk import WalkConfig, batch_exits
+    from exitmeasure.conductivity import identity_tensor
+
+    from paper_2409_03686_b200 import plugin
+
+    saved = (ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND)
+    try:
+        plugin.install(precision="ref64", module=ref)
+        with pytest.raises(WalkBudgetError):
+            batch_exits(catalog("annulus"), identity_tensor(2), [0.95, 0.0],
+                        WalkConfig(eps=1e-10, seed=1, max_steps=1), 64)
+    finally:
+        ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND = saved
+
+
+def test_cli_outputs_byte_identical(ref, tmp_path):
+    outs = []
+    env = dict(os.environ, PYTHONPATH=f"{REF}:{ROOT}")
+    for label, mod in (("cpu", "exitmeasure.cli"), ("gpu", "paper_2409_03686_b200.plugin")):
+        out = tmp_path / label
+        cmd = [sys.executable, "-m", mod, "--example", "ex5_2", "--solution", "sol2d_2",
+               "--n", "2000", "--seed", "9", "--r", "1:3", "--out", str(out)]
+        proc = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+        assert proc.returncode == 0, proc.stderr[-3000:]
+        outs.append(out)
+    for name in ("eigenvalues.csv", "density.csv", "eigvecs.csv", "tsvd.csv", "residuals.csv"):
+        assert (outs[0] / name).read_bytes() == (outs[1] / name).read_bytes(), name
