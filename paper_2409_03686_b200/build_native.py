@@ -33,7 +33,8 @@ UNITS = [
     # (source, extra flags)
     ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]),
     ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false",
-                     f"-DEM_BATCH_STEPS={os.environ.get('EM_BATCH_STEPS', '8')}"]),
+                     f"-DEM_BATCH_STEPS={os.environ.get('EM_BATCH_STEPS', '8')}",
+                     f"-DEM_MIN_BLOCKS={os.environ.get('EM_MIN_BLOCKS', '4')}"]),
     ("capi.cu", []),
     ("kat_curand.cu", []),
 ]

@@ -25,6 +25,7 @@ cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cu
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
                        bool ident, int bink, int grid, int block, cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
+cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
@@ -602,6 +603,11 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
 #undef EM_ALLOC
   // persistent grid: SMs x resident blocks
   int per_sm = 4;
+  if (p->precision == EM_PREC_FP32) {
+    int nb = 0;
+    if (f32_blocks_per_sm(p->d, p->outer, p->nh_mode, p->chain, p->ident, p->bink, &nb) == cudaSuccess && nb > 0)
+      per_sm = nb;
+  }
   p->grid = o.grid > 0 ? o.grid : sm_count_of(o.device) * per_sm * (256 / p->block > 0 ? 256 / p->block : 1);
   *out = p;
   return EM_OK;

@@ -413,8 +413,11 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 
 // MODE 0: bin exits into the count rows + per-pole step statistics
 // MODE 1: write exit points / steps / components (em_run_exits)
+#ifndef EM_MIN_BLOCKS
+#define EM_MIN_BLOCKS 4
+#endif
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK>
-__global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
+__global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
   __shared__ float4 q_x[kWarps][kQueue];  // exit point, pole (as int bits in .w)
   __shared__ int q_s[kWarps][kQueue];     // steps
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
   unsigned cpid = 0;
   int steps = 0, pole = 0, rep_off = 0;
   unsigned draw = 0, rep_lo = 0, rep_hi = 0;
-  bool walking = false, done = false, failed = false;
+  bool walking = false, inflight = false, failed = false;
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
@@ -438,6 +441,7 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
     if (need) {
+      const bool done = inflight && !walking && !failed;
       if (MODE == 0) {
         const unsigned dm = __ballot_sync(kFull, done);
         if (done) {
@@ -463,7 +467,10 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
       }
       if (failed)
         atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
-      done = failed = false;
+      if (!walking) {
+        failed = false;
+        inflight = false;
+      }
       if (pool_take(wp, need, W, pole, rep_off)) {
         if (pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
         steps = 0;
         draw = 0;
         walking = true;
+        inflight = true;
       }
       if (wp.exhausted && __ballot_sync(kFull, walking) == 0) break;
     }
@@ -502,9 +510,7 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
       for (int k = 0; k < K; ++k) {
         float e, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        const bool stop = walking && e <= P.eps;
-        done = done || stop;
-        walking = walking && !stop;
+        walking = walking && e > P.eps;
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
         if (D == 2)
           step<D, IDENT>(P, x, rs, wv[k], 0u);
@@ -519,7 +525,6 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
         const bool stop = walking && e <= P.eps;
         const bool over = walking && !stop && steps >= P.max_steps;
-        done = done || stop;
         failed = failed || over;
         walking = walking && !stop && !over;
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
@@ -548,68 +553,68 @@ __global__ void __launch_bounds__(256, 4) walk_f32_kernel(const F32Params P) {
 // binner) combinations.  nh_mode: 0 = no holes, 1 = exactly one hole, 2 =
 // runtime count.  Specialised binners exist where a BASELINE config needs
 // them; everything else takes BIN_ANY.
+using F32Kernel = void (*)(F32Params);
+
 template <int D, int OUTER, int NH, int BINK>
-static cudaError_t launch_chain(const F32Params& P, int mode, int chain, bool ident, int grid,
-                                int block, cudaStream_t s) {
-#define EM_LAUNCH(CH, ID)                                                              \
-  do {                                                                                 \
-    if (mode == 0)                                                                     \
-      f32::walk_f32_kernel<D, OUTER, NH, CH, ID, 0, BINK><<<grid, block, 0, s>>>(P);   \
-    else                                                                               \
-      f32::walk_f32_kernel<D, OUTER, NH, CH, ID, 1, f32::BIN_ANY><<<grid, block, 0, s>>>(P); \
-  } while (0)
-  if (ident)
-    EM_LAUNCH(EM_CHAIN_WOE, true);
-  else if (chain == EM_CHAIN_MAX)
-    EM_LAUNCH(EM_CHAIN_MAX, false);
-  else
-    EM_LAUNCH(EM_CHAIN_WOE, false);
-#undef EM_LAUNCH
-  return cudaGetLastError();
+static F32Kernel pick_chain(int mode, int chain, bool ident) {
+  using namespace f32;
+  if (mode != 0) {
+    if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 1, BIN_ANY>;
+    if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 1, BIN_ANY>;
+    return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 1, BIN_ANY>;
+  }
+  if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 0, BINK>;
+  if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 0, BINK>;
+  return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 0, BINK>;
 }
 
 template <int D, int OUTER, int NH, int B1, int B2>
-static cudaError_t launch_bin(const F32Params& P, int mode, int chain, bool ident, int bink,
-                              int grid, int block, cudaStream_t s) {
-  if (mode == 0 && bink == B1 && B1 != f32::BIN_ANY)
-    return launch_chain<D, OUTER, NH, B1>(P, mode, chain, ident, grid, block, s);
-  if (mode == 0 && bink == B2 && B2 != f32::BIN_ANY)
-    return launch_chain<D, OUTER, NH, B2>(P, mode, chain, ident, grid, block, s);
-  return launch_chain<D, OUTER, NH, f32::BIN_ANY>(P, mode, chain, ident, grid, block, s);
+static F32Kernel pick_bin(int mode, int chain, bool ident, int bink) {
+  if (mode == 0 && bink == B1 && B1 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B1>(mode, chain, ident);
+  if (mode == 0 && bink == B2 && B2 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B2>(mode, chain, ident);
+  return pick_chain<D, OUTER, NH, f32::BIN_ANY>(mode, chain, ident);
+}
+
+static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bool ident, int bink) {
+  using namespace f32;
+  if (d == 2) {
+    if (outer == OUTER_BALL) {
+      if (nh_mode == 0) return pick_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
+      if (nh_mode == 1) return pick_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
+      return pick_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
+    }
+    if (outer == OUTER_BOX) {
+      if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink);
+      return pick_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
+    }
+    return nullptr;
+  }
+  if (outer == OUTER_BALL) {
+    if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
+    return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
+  }
+  if (outer == OUTER_BOX) {
+    if (nh_mode == 0) return pick_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
+    return pick_bin<3, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
+  }
+  if (nh_mode == 0) return pick_bin<3, OUTER_LBOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
+  return pick_bin<3, OUTER_LBOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
 }
 
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
                        bool ident, int bink, int grid, int block, cudaStream_t s) {
-  using namespace f32;
-  if (block != 32 * kWarps) return cudaErrorInvalidConfiguration;
-  if (d == 2) {
-    if (outer == OUTER_BALL) {
-      if (nh_mode == 0)
-        return launch_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-      if (nh_mode == 1)
-        return launch_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-      return launch_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-    }
-    if (outer == OUTER_BOX) {
-      if (nh_mode == 0)
-        return launch_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(P, mode, chain, ident, bink, grid, block, s);
-      return launch_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-    }
-    return cudaErrorInvalidValue;
-  }
-  if (outer == OUTER_BALL) {
-    if (nh_mode == 0)
-      return launch_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-    return launch_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-  }
-  if (outer == OUTER_BOX) {
-    if (nh_mode == 0)
-      return launch_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-    return launch_bin<3, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-  }
-  if (nh_mode == 0)
-    return launch_bin<3, OUTER_LBOX, 0, BIN_GRID, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
-  return launch_bin<3, OUTER_LBOX, -1, BIN_ANY, BIN_ANY>(P, mode, chain, ident, bink, grid, block, s);
+  if (block != 32 * f32::kWarps) return cudaErrorInvalidConfiguration;
+  F32Kernel k = pick_f32(d, outer, nh_mode, mode, chain, ident, bink);
+  if (!k) return cudaErrorInvalidValue;
+  k<<<grid, block, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink,
+                              int* nb) {
+  F32Kernel k = pick_f32(d, outer, nh_mode, 0, chain, ident, bink);
+  if (!k) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
 }
 
 // ---- FP32 issue-rate micro-benchmark (roofline denominator) ----
