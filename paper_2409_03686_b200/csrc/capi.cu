@@ -484,27 +484,30 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     const double* gf = g->gf;
     P.n_holes = nh;
     P.has_notch = nn;
+    // kernel frame: origin at the ball centre / the box's low corner
+    double frame[3] = {0.0, 0.0, 0.0};
     double scale = 1.0;
     if (g->gi[1] == 0) {
-      for (int j = 0; j < d; ++j) P.oc[j] = (float)gf[j];
+      for (int j = 0; j < d; ++j) frame[j] = gf[j];
       P.oR = (float)gf[d];
-      for (int j = 0; j < d; ++j) scale = std::max(scale, std::fabs(gf[j]) + gf[d]);
+      scale = std::max(scale, gf[d]);
     } else {
       for (int j = 0; j < d; ++j) {
-        P.blo[j] = (float)(gf[j] - gf[d]);
-        P.bhi[j] = (float)(gf[j] + gf[d]);
-        scale = std::max(scale, std::fabs(gf[j]) + gf[d]);
+        frame[j] = gf[j] - gf[d];
+        P.bhi[j] = (float)(2.0 * gf[d]);
       }
+      scale = std::max(scale, 2.0 * gf[d]);
     }
+    for (int j = 0; j < 3; ++j) P.frame[j] = (float)frame[j];
     for (int h = 0; h < nh; ++h) {
       const int off = d + 1 + h * (d + 1);
-      for (int j = 0; j < d; ++j) P.hc[h][j] = (float)gf[off + j];
+      for (int j = 0; j < d; ++j) P.hc[h][j] = (float)(gf[off + j] - frame[j]);
       P.hr[h] = (float)gf[off + d];
     }
     if (nn) {
       const int off = (d + 1) * (1 + nh);
-      P.notch[0] = (float)gf[off];
-      P.notch[1] = (float)gf[off + 1];
+      P.notch[0] = (float)(gf[off] - frame[0]);
+      P.notch[1] = (float)(gf[off + 1] - frame[1]);
     }
     for (int c = 0; c < 1 + nh + nn; ++c) P.comp_side[c] = g->comp_side[c];
     for (int i = 0; i < d * d; ++i) P.A[i] = (float)g->ksqrt[i];
@@ -522,7 +525,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);
     std::vector<float> pf(n_poles * 4, 0.0f);
     for (int64_t i = 0; i < n_poles; ++i)
-      for (int j = 0; j < d; ++j) pf[i * 4 + j] = (float)poles[i * d + j];
+      for (int j = 0; j < d; ++j) pf[i * 4 + j] = (float)(poles[i * d + j] - frame[j]);
     EM_ALLOC(p->poles, (size_t)n_poles * 16);
     if (cudaMemcpy(p->poles.p, pf.data(), n_poles * 16, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(EM_ERR_CUDA, "upload poles"));

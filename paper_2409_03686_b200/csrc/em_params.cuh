@@ -76,10 +76,13 @@ struct Ref64Params {
 
 struct F32Params {
   int n_holes, has_notch;
-  float oc[3], oR;  // ball outer: center, radius
-  float blo[3], bhi[3];  // box / L-box outer: low and high corners
-  float hc[EM_MAX_HOLES][3], hr[EM_MAX_HOLES];
-  float notch[2];
+  // The kernel works in a frame where the outer ball's centre / the box's low
+  // corner is the origin (saves the per-step x - c); world = frame + offset.
+  float frame[3];
+  float oR;      // ball outer: radius
+  float bhi[3];  // box / L-box outer: widths (the box is [0, bhi] in the frame)
+  float hc[EM_MAX_HOLES][3], hr[EM_MAX_HOLES];  // hole centres in the frame
+  float notch[2];                               // notch corner in the frame
   signed char comp_side[kMaxComp];
   float A[9];       // K^{1/2}, row-major
   float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid

@@ -45,8 +45,9 @@ template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   if (OUTER == OUTER_BALL) {
-    const float v0 = x[0] - P.oc[0], v1 = x[1] - P.oc[1];
-    const float v2 = D == 3 ? x[2] - P.oc[2] : 0.0f;
+    // kernel frame: the outer ball is centred at the origin
+    const float v0 = x[0], v1 = x[1];
+    const float v2 = D == 3 ? x[2] : 0.0f;
     float s2 = v0 * v0 + v1 * v1;
     if (D == 3) s2 = fmaf(v2, v2, s2);
     const float s = sqrtf(s2);
@@ -77,7 +78,8 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
     r = kInf;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      const float m = fminf(x[i] - P.blo[i], P.bhi[i] - x[i]);
+      // kernel frame: the box is [0, bhi_i] in every axis
+      const float m = fminf(x[i], P.bhi[i] - x[i]);
       e = fminf(e, m);
       if (MAXC) r = fminf(r, m * P.g[i]);
     }
@@ -138,13 +140,13 @@ template <int D, int OUTER, int NH>
 __device__ __forceinline__ int owner(const F32Params& P, const float* x) {
   float best;
   if (OUTER == OUTER_BALL) {
-    const float v0 = x[0] - P.oc[0], v1 = x[1] - P.oc[1];
-    const float v2 = D == 3 ? x[2] - P.oc[2] : 0.0f;
+    const float v0 = x[0], v1 = x[1];
+    const float v2 = D == 3 ? x[2] : 0.0f;
     best = fabsf(P.oR - sqrtf(v0 * v0 + v1 * v1 + v2 * v2));
   } else {
     float m = kInf;
 #pragma unroll
-    for (int i = 0; i < D; ++i) m = fminf(m, fminf(x[i] - P.blo[i], P.bhi[i] - x[i]));
+    for (int i = 0; i < D; ++i) m = fminf(m, fminf(x[i], P.bhi[i] - x[i]));
     best = fabsf(m);
   }
   int comp = 0;
@@ -405,7 +407,8 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
   int side;
   if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
   else side = P.comp_side[0];
-  const int a = bin_exit<D, BINK>(P, side, x);
+  const float xw[3] = {x[0] + P.frame[0], x[1] + P.frame[1], D == 3 ? x[2] + P.frame[2] : 0.0f};
+  const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
   acc_add(acc, W, pole, (unsigned long long)steps);
@@ -423,6 +426,8 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
   __shared__ int q_s[kWarps][kQueue];     // steps
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  float4* const qx = q_x[warp];
+  int* const qs = q_s[warp];
   int qn = 0;  // queued exits of this warp (warp-uniform)
   float x[3] = {0.0f, 0.0f, 0.0f};
   float px = 0.0f, py = 0.0f, pz = 0.0f;  // this lane's cached pole (start point)
@@ -430,7 +435,8 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
   unsigned cpid = 0;
   int steps = 0, pole = 0, rep_off = 0;
   unsigned draw = 0, rep_lo = 0, rep_hi = 0;
-  bool walking = false, inflight = false, failed = false;
+  // lane flags as ints (bools become byte-packed PRMT traffic in SASS)
+  int walking = 0, inflight = 0, failed = 0;
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
@@ -441,35 +447,37 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
     if (need) {
-      const bool done = inflight && !walking && !failed;
+      const int done = inflight & (walking ^ 1) & (failed ^ 1);
       if (MODE == 0) {
         const unsigned dm = __ballot_sync(kFull, done);
-        if (done) {
-          const int slot = qn + __popc(dm & lt);
-          q_x[warp][slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
-          q_s[warp][slot] = steps;
-        }
-        qn += __popc(dm);
-        if (qn >= 32) {  // bin 32 queued exits with every lane active
-          __syncwarp();
-          const int slot = qn - 32 + lane;
-          const float4 e = q_x[warp][slot];
-          const float ex[3] = {e.x, e.y, e.z};
-          retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][slot], acc);
-          qn -= 32;
-          __syncwarp();
+        if (dm) {
+          if (done) {
+            const int slot = qn + __popc(dm & lt);
+            qx[slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
+            qs[slot] = steps;
+          }
+          qn += __popc(dm);
+          if (qn >= 32) {  // bin 32 queued exits with every lane active
+            __syncwarp();
+            const int slot = qn - 32 + lane;
+            const float4 e = qx[slot];
+            const float ex[3] = {e.x, e.y, e.z};
+            retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), qs[slot], acc);
+            qn -= 32;
+            __syncwarp();
+          }
         }
       } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
-        for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j];
+        for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j] + (double)P.frame[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
       if (failed)
         atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
       if (!walking) {
-        failed = false;
-        inflight = false;
+        failed = 0;
+        inflight = 0;
       }
       if (pool_take(wp, need, W, pole, rep_off)) {
         if (pole != cpole) {
@@ -488,8 +496,8 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         rep_hi = (unsigned)(rep >> 32);
         steps = 0;
         draw = 0;
-        walking = true;
-        inflight = true;
+        walking = 1;
+        inflight = 1;
       }
       if (wp.exhausted && __ballot_sync(kFull, walking) == 0) break;
     }
@@ -510,7 +518,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
       for (int k = 0; k < K; ++k) {
         float e, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        walking = walking && e > P.eps;
+        walking &= (e > P.eps);
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
         if (D == 2)
           step<D, IDENT>(P, x, rs, wv[k], 0u);
@@ -523,10 +531,10 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
       for (int k = 0; k < K; ++k) {
         float e, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        const bool stop = walking && e <= P.eps;
-        const bool over = walking && !stop && steps >= P.max_steps;
-        failed = failed || over;
-        walking = walking && !stop && !over;
+        const int stop = walking & (e <= P.eps);
+        const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
+        failed |= over;
+        walking &= (stop ^ 1) & (over ^ 1);
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
         if (D == 2)
           step<D, IDENT>(P, x, rs, wv[k], 0u);
