@@ -95,7 +95,7 @@ typedef struct {
   const int64_t* blk;
   const double* blkf;
   int64_t n_blk;
-  int32_t wkind; /* 0 voronoi (1 idw: EM_ERR_UNSUPPORTED in this ABI version) */
+  int32_t wkind; /* 0 voronoi, 1 idw (REF64 only, via em_plan_run_raw) */
   int32_t idw_power;
   const double* idw_radii;
   const double* blk_phase;
@@ -168,6 +168,17 @@ int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int6
  * any zeroing/packing kernels) */
 int em_plan_last_launches(const em_plan* p, int64_t* launches);
 int64_t em_plan_n_bins(const em_plan* p, int side);
+
+/* Fractional rows (REF64 only; required for IDW weight families, valid for
+ * Voronoi too): raw0 (n_poles, n0) and raw1 (n_poles, n1) doubles.  With
+ * init0/init1 the sums continue in place from those values in replicate
+ * order (the chunk contract, S/_kernel.pyx:451-461); without, every `chunk`
+ * replicates (8192 in the reference driver) start a zeroed partial that is
+ * folded into the row in chunk order (S/backend.py:159-198), so fractional
+ * IDW rows match the reference bit for bit.  stats (3, n_poles). */
+int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, int64_t chunk,
+                    const double* init0, const double* init1, double* raw0, double* raw1,
+                    int64_t* stats, int64_t* idw_fallbacks, int64_t* err_pole, int64_t* err_rep);
 
 /* One-shot convenience: create, run, destroy. */
 int em_run_accumulate(const em_geometry* g, const em_side* s0, const em_side* s1,

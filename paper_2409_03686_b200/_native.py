@@ -101,6 +101,8 @@ def lib():
                                ctypes.POINTER(EmOptions), ctypes.POINTER(EmOutputs)],
                               ctypes.c_int),
         "em_run_exits": ([_p, _u64, _i64, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
+        "em_plan_run_raw": ([_p, _u64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p],
+                            ctypes.c_int),
         "em_fp32_peak": ([ctypes.c_int, _p, _p], ctypes.c_int),
         "em_philox4x64_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "em_philox4x32_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),

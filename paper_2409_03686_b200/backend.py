@@ -182,12 +182,8 @@ class _Marshal:
                          sp.idw_power, getattr(sp, "blk_phase", None))
 
 
-def _check_idw(*sides):
-    for s in sides:
-        if int(getattr(s, "weights_kind", 0)) != 0:
-            raise NotImplementedError(
-                "IDW weight families are not implemented on the GPU path yet "
-                "(SURVEY.md §8f item 4); use Voronoi families")
+def _has_idw(*sides) -> bool:
+    return any(int(getattr(s, "weights_kind", 0)) != 0 for s in sides)
 
 
 # ---------------------------------------------------------------------------
@@ -221,10 +217,6 @@ def accumulate_chunk(gi, gf, comp_side, ksqrt, pole_xy, pole_index, rep_start, r
                      device: int | None = None):
     """Drop-in for _kernel.accumulate_chunk: out0/out1 += counts; returns
     (steps_sum, steps_sq_sum, steps_max, idw_fallbacks, err)."""
-    if int(wkind0) != 0 or int(wkind1) != 0:
-        raise NotImplementedError(
-            "IDW weight families are not implemented on the GPU path yet "
-            "(SURVEY.md §8f item 4); use Voronoi families")
     m = _Marshal()
     g = m.geometry(gi, gf, comp_side, ksqrt)
     pole = m.arr(pole_xy, np.float64)
@@ -281,7 +273,9 @@ class Plan:
         chain = (chain or default_chain(precision)).lower()
         if chain not in _CHAINS:
             raise ValidationError(f"unknown chain {chain!r}")
-        _check_idw(side0, side1)
+        self.idw = _has_idw(side0, side1)
+        if self.idw and _PRECISIONS[precision] != N.EM_PREC_REF64:
+            raise ValidationError("IDW weight families run on the bit-exact REF64 path only")
         self.device = default_device() if device is None else int(device)
         N.require_device(self.device)
         self.precision, self.chain = precision, chain
@@ -324,7 +318,27 @@ class Plan:
     def __exit__(self, *exc):
         self.close()
 
+    def run_raw(self, seed: int, n_rep: int, rep_start: int = 0,
+                chunk: int = CHUNK) -> AccumulateResult:
+        """Fractional rows (IDW families; REF64), summed with the reference
+        driver's per-CHUNK partials in job order -- bit-identical rows."""
+        raw0 = np.zeros((self.n_poles, self.n0))
+        raw1 = np.zeros((self.n_poles, self.n1))
+        stats = np.zeros((3, self.n_poles), dtype=np.int64)
+        fb, ep, er = ctypes.c_int64(0), ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = N.check(N.lib().em_plan_run_raw(self._h, int(seed) & (2**64 - 1), int(rep_start),
+                                             int(n_rep), int(chunk), None, None, N.ptr(raw0),
+                                             N.ptr(raw1), N.ptr(stats), ctypes.byref(fb),
+                                             ctypes.byref(ep), ctypes.byref(er)),
+                     "em_plan_run_raw")
+        if rc == N.EM_BUDGET:
+            raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
+        return AccumulateResult(raw0, raw1, stats[0].copy(), stats[1].copy(), stats[2].copy(),
+                                int(fb.value))
+
     def run(self, seed: int, n_rep: int, rep_start: int = 0) -> AccumulateResult:
+        if self.idw:
+            return self.run_raw(seed, n_rep, rep_start)
         row = self.n0 + self.n1
         counts = np.zeros((self.n_poles, row), dtype=np.int64)
         stats = np.zeros((3, self.n_poles), dtype=np.int64)

@@ -24,6 +24,12 @@ namespace em {
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s);
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
                        bool ident, int bink, int grid, int block, cudaStream_t s);
+cudaError_t launch_idw(const Ref64Params& P, const double* x, const long long* comp,
+                       long long n_poles, long long n_rep, long long chunk,
+                       const double* a0, const double* r0, int n0, int pw0, int wk0,
+                       const double* a1, const double* r1, int n1, int pw1, int wk1, int* kind,
+                       long long* idx, double* total, int* side, double* out0, double* out1,
+                       const double* init0, const double* init1, cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
@@ -176,6 +182,9 @@ struct em_plan {
   DevBuf poles, pole_ids, anchors[2], gcell[2], gcand[2];
   DevBuf counts, stats, misc;  // stats: 3 * n_poles u64; misc: err, ticket, walks
   DevBuf xo, so, co;           // exits
+  DevBuf radii[2];             // IDW supports (REF64)
+  DevBuf ikind, iidx, itot, iside, iraw0, iraw1, iinit0, iinit1;
+  int wkind[2] = {0, 0}, idw_power[2] = {2, 2};
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
@@ -294,8 +303,10 @@ int validate_geometry(const em_geometry* g) {
 
 int validate_side(const em_side* s, int d, const char* name, bool used) {
   if (!s) return fail(EM_ERR_INVALID, std::string(name) + ": null");
-  if (s->wkind != 0)
-    return fail(EM_ERR_UNSUPPORTED, std::string(name) + ": IDW weights are not supported");
+  if (s->wkind != 0 && s->wkind != 1)
+    return fail(EM_ERR_INVALID, std::string(name) + ": weight kind must be 0 (voronoi) or 1 (idw)");
+  if (s->wkind == 1 && s->n_anchors > 0 && (!s->idw_radii || s->idw_power < 1 || s->idw_power > 8))
+    return fail(EM_ERR_INVALID, std::string(name) + ": IDW needs radii and a power in 1..8");
   if (s->n_anchors < 0 || s->n_blk < 0)
     return fail(EM_ERR_INVALID, std::string(name) + ": negative size");
   if (used && s->n_anchors == 0)
@@ -376,6 +387,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     return fail(EM_ERR_INVALID, "unknown precision");
   if (o.precision == EM_PREC_REF64 && o.chain != EM_CHAIN_WOE)
     return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
+  if (o.precision != EM_PREC_REF64 && (s0->wkind == 1 || s1->wkind == 1))
+    return fail(EM_ERR_UNSUPPORTED, "IDW weight families run on the REF64 path only");
   if (o.precision == EM_PREC_FP32 && o.block > 0 && o.block != 256)
     return fail(EM_ERR_UNSUPPORTED, "the FP32 kernel runs 256-thread blocks");
   int ndev = em_device_count();
@@ -470,6 +483,13 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         D.cy[b] = S->blkf[4 * b + 1];
         D.radius[b] = S->blkf[4 * b + 3];
         D.phase[b] = S->blk_phase ? S->blk_phase[b] : 0.0;
+      }
+      p->wkind[s] = S->wkind;
+      p->idw_power[s] = S->idw_power;
+      if (S->n_anchors > 0 && S->wkind == 1) {
+        EM_ALLOC(p->radii[s], (size_t)S->n_anchors * 8);
+        if (cudaMemcpy(p->radii[s].p, S->idw_radii, S->n_anchors * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+          return bail(fail(EM_ERR_CUDA, "upload idw radii"));
       }
       if (S->n_anchors > 0) {
         EM_ALLOC(p->anchors[s], (size_t)S->n_anchors * d * 8);
@@ -796,6 +816,91 @@ int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, do
   return rc;
 }
 
+int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, int64_t chunk,
+                    const double* init0, const double* init1, double* raw0, double* raw1,
+                    int64_t* stats, int64_t* idw_fallbacks, int64_t* err_pole, int64_t* err_rep) {
+  if (!p || !raw0 || !raw1 || !stats) return fail(EM_ERR_INVALID, "null");
+  if (p->precision != EM_PREC_REF64) return fail(EM_ERR_UNSUPPORTED, "raw rows need REF64");
+  if (n_rep < 0 || rep_start < 0) return fail(EM_ERR_INVALID, "negative replicate range");
+  DeviceGuard dg(p->device);
+  const int64_t total = p->n_poles * n_rep;
+  const int d = p->d;
+  cudaError_t ce;
+  const size_t nw = (size_t)std::max<int64_t>(total, 1);
+  if ((ce = p->xo.alloc(nw * d * 8)) != cudaSuccess || (ce = p->so.alloc(nw * 8)) != cudaSuccess ||
+      (ce = p->co.alloc(nw * 8)) != cudaSuccess || (ce = p->ikind.alloc(nw * 4)) != cudaSuccess ||
+      (ce = p->iidx.alloc(nw * 8)) != cudaSuccess || (ce = p->itot.alloc(nw * 8)) != cudaSuccess ||
+      (ce = p->iside.alloc(nw * 4)) != cudaSuccess ||
+      (ce = p->iraw0.alloc((size_t)std::max<int64_t>(p->n_poles * p->n0, 1) * 8)) != cudaSuccess ||
+      (ce = p->iraw1.alloc((size_t)std::max<int64_t>(p->n_poles * p->n1, 1) * 8)) != cudaSuccess)
+    return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+  WorkOut* w = &p->p64.w;
+  w->x_out = p->xo.as<double>();
+  w->steps_out = p->so.as<long long>();
+  w->comp_out = p->co.as<long long>();
+  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->counts.as<unsigned long long>(),
+                       p->stats.as<unsigned long long>(), p->stream);
+  if (rc) return rc;
+  const double* d_init0 = nullptr;
+  const double* d_init1 = nullptr;
+  if (init0 && init1) {
+    if ((ce = p->iinit0.alloc((size_t)std::max<int64_t>(p->n_poles * p->n0, 1) * 8)) != cudaSuccess ||
+        (ce = p->iinit1.alloc((size_t)std::max<int64_t>(p->n_poles * p->n1, 1) * 8)) != cudaSuccess)
+      return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+    EM_CUDA(cudaMemcpyAsync(p->iinit0.p, init0, p->n_poles * p->n0 * 8, cudaMemcpyHostToDevice, p->stream));
+    EM_CUDA(cudaMemcpyAsync(p->iinit1.p, init1, p->n_poles * p->n1 * 8, cudaMemcpyHostToDevice, p->stream));
+    d_init0 = p->iinit0.as<double>();
+    d_init1 = p->iinit1.as<double>();
+  }
+  // budget check before binning: outputs are meaningless after a failure
+  unsigned long long err = ~0ULL;
+  EM_CUDA(cudaMemcpyAsync(&err, p->misc.p, 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaStreamSynchronize(p->stream));
+  if (err != ~0ULL) {
+    if (err_pole) *err_pole = n_rep > 0 ? (int64_t)(err / (unsigned long long)n_rep) : 0;
+    if (err_rep) *err_rep = n_rep > 0 ? (int64_t)(err % (unsigned long long)n_rep) : 0;
+    return EM_BUDGET;
+  }
+  const Side64& S0 = p->p64.side[0];
+  const Side64& S1 = p->p64.side[1];
+  cudaError_t e = launch_idw(p->p64, p->xo.as<double>(), p->co.as<long long>(), p->n_poles, n_rep,
+                             chunk > 0 ? chunk : std::max<int64_t>(n_rep, 1),
+                             S0.anchors, p->radii[0].as<double>(), (int)p->n0, p->idw_power[0], p->wkind[0],
+                             S1.anchors, p->radii[1].as<double>(), (int)p->n1, p->idw_power[1], p->wkind[1],
+                             p->ikind.as<int>(), p->iidx.as<long long>(), p->itot.as<double>(),
+                             p->iside.as<int>(), p->iraw0.as<double>(), p->iraw1.as<double>(),
+                             d_init0, d_init1, p->stream);
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("idw kernels: ") + cudaGetErrorString(e));
+  EM_CUDA(cudaMemcpyAsync(raw0, p->iraw0.p, p->n_poles * p->n0 * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(raw1, p->iraw1.p, p->n_poles * p->n1 * 8, cudaMemcpyDeviceToHost, p->stream));
+  std::vector<long long> steps(nw);
+  std::vector<double> tot(nw);
+  if (total > 0) {
+    EM_CUDA(cudaMemcpyAsync(steps.data(), p->so.p, total * 8, cudaMemcpyDeviceToHost, p->stream));
+    EM_CUDA(cudaMemcpyAsync(tot.data(), p->itot.p, total * 8, cudaMemcpyDeviceToHost, p->stream));
+  }
+  EM_CUDA(cudaStreamSynchronize(p->stream));
+  int64_t fb = 0;
+  for (int64_t i = 0; i < p->n_poles; ++i) {
+    int64_t ss = 0, sq = 0, sm = 0;
+    for (int64_t r = 0; r < n_rep; ++r) {
+      const int64_t st = steps[i * n_rep + r];
+      ss += st;
+      sq += st * st;
+      sm = st > sm ? st : sm;
+      if (tot[i * n_rep + r] < 0.0) ++fb;
+    }
+    stats[i] = ss;
+    stats[p->n_poles + i] = sq;
+    stats[2 * p->n_poles + i] = sm;
+  }
+  if (idw_fallbacks) *idw_fallbacks = fb;
+  if (err_pole) *err_pole = -1;
+  if (err_rep) *err_rep = -1;
+  p->last_launches = 3;
+  return EM_OK;
+}
+
 // ---- chunk-level drop-ins (the reference's _impl contract) ----
 
 int em_walk_exits_chunk(const em_geometry* g, const double* pole_xy, int64_t pole_index,
@@ -841,6 +946,30 @@ int em_accumulate_chunk(const em_geometry* g, const double* pole_xy, int64_t pol
   const int64_t pid = pole_index;
   int rc = em_plan_create(g, s0, s1, pole_xy, &pid, 1, eps, max_steps, &o, &p);
   if (rc) return rc;
+  if (s0->wkind == 1 || s1->wkind == 1) {
+    // fractional weights: accumulate in place from out0/out1, walk order
+    std::vector<double> r0(std::max<int64_t>(s0->n_anchors, 1)), r1(std::max<int64_t>(s1->n_anchors, 1));
+    int64_t st[3] = {0, 0, 0}, fb = 0, ep = -1, er = -1;
+    rc = em_plan_run_raw(p, seed, rep_start, rep_end - rep_start, 0, out0, out1, r0.data(),
+                         r1.data(), st, &fb, &ep, &er);
+    em_plan_destroy(p);
+    if (rc == EM_BUDGET) {
+      if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+      if (err_rep) *err_rep = rep_start + er;
+      return EM_OK;
+    }
+    if (rc) return rc;
+    for (int64_t i = 0; i < s0->n_anchors; ++i) out0[i] = r0[i];
+    for (int64_t i = 0; i < s1->n_anchors; ++i) out1[i] = r1[i];
+    if (stats) {
+      stats[0] = st[0];
+      stats[1] = st[1];
+      stats[2] = st[2];
+      stats[3] = fb;
+    }
+    if (err_rep) *err_rep = -1;
+    return EM_OK;
+  }
   const int64_t row = s0->n_anchors + s1->n_anchors;
   std::vector<int64_t> counts(std::max<int64_t>(row, 1));
   int64_t ss = 0, sq = 0, sm = 0;

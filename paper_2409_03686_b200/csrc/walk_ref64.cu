@@ -316,6 +316,152 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
 
 }  // namespace r64
 
+// ---------------------------------------------------------------------------
+// IDW weight families (S/_kernel.pyx:323-369), bit-exact.
+//
+// After the exits kernel (MODE 1) has written every walk's exit point and
+// component, idw_prep computes per walk what the reference's scalar loop
+// decides first: the anchor it sits on (r < 1e-14), the Voronoi fallback
+// winner (no support covers it), or the normaliser `total` -- summed in anchor
+// order exactly as the reference does.  idw_scatter then gives each
+// (pole, anchor) one thread that walks the pole's walks in replicate order
+// and adds w/total (or 1.0) sequentially, restarting a partial sum at every
+// CHUNK boundary and folding it into the row in chunk order -- the
+// reference driver's per-task zeroed buffers merged in job order
+// (S/backend.py:159-198).  With `init` (the chunk API) the sum continues
+// in place from the caller's values (S/_kernel.pyx:451-461 writes `out +=`).
+// Voronoi sides in a mixed family pair add 1.0 at the winner.
+
+struct IdwSide {
+  const double* anchors;
+  const double* radii;
+  int n, power, wkind;
+};
+
+enum : int { IDW_NORMAL = 0, IDW_AT = 1, IDW_WINNER = 2 };
+
+__global__ void idw_prep_kernel(const Ref64Params P, const double* x, const long long* comp,
+                                long long n_walks, IdwSide s0, IdwSide s1, int* kind,
+                                long long* idx, double* total, int* side_out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n_walks) return;
+  const int d = P.d;
+  double xw[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < d; ++k) xw[k] = x[j * d + k];
+  const int side = P.comp_side[comp[j]];
+  side_out[j] = side;
+  const IdwSide& S = side ? s1 : s0;
+  if (S.wkind == 0) {
+    kind[j] = IDW_WINNER;
+    idx[j] = r64::assign_anchor(xw, d, P.side[side]);
+    total[j] = 0.0;
+    return;
+  }
+  double tot = 0.0;
+  for (int i = 0; i < S.n; ++i) {
+    const double* a = S.anchors + (long long)i * d;
+    double dx0 = xw[0] - a[0], dx1 = xw[1] - a[1];
+    double d2 = dx0 * dx0 + dx1 * dx1;
+    if (d == 3) {
+      double dx2 = xw[2] - a[2];
+      d2 = d2 + dx2 * dx2;
+    }
+    const double r = sqrt(d2);
+    if (r < 1e-14) {
+      kind[j] = IDW_AT;
+      idx[j] = i;
+      return;
+    }
+    double base = S.radii[i] - r;
+    if (base > 0.0) {
+      base = base / (S.radii[i] * r);
+      double w = base;
+      for (int q = 0; q < S.power - 1; ++q) w = w * base;
+      tot = tot + w;
+    }
+  }
+  if (tot == 0.0) {
+    kind[j] = IDW_WINNER;
+    idx[j] = r64::assign_anchor(xw, d, P.side[side]);
+    total[j] = -1.0;  // marks a fallback (counted in idw_fallbacks)
+    return;
+  }
+  kind[j] = IDW_NORMAL;
+  total[j] = tot;
+}
+
+__global__ void idw_scatter_kernel(const Ref64Params P, const double* x, long long n_poles,
+                                   long long n_rep, long long chunk, IdwSide s0, IdwSide s1,
+                                   const int* kind, const long long* idx, const double* total,
+                                   const int* side_of, double* out0, double* out1,
+                                   const double* init0, const double* init1) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long per_pole = (long long)s0.n + s1.n;
+  if (t >= n_poles * per_pole) return;
+  const long long pole = t / per_pole;
+  int i = (int)(t % per_pole);
+  int side = 0;
+  if (i >= s0.n) {
+    side = 1;
+    i -= s0.n;
+  }
+  const IdwSide& S = side ? s1 : s0;
+  double* out = side ? out1 : out0;
+  const double* init = side ? init1 : init0;
+  const int d = P.d;
+  const double* a = S.anchors + (long long)i * d;
+  double row = init ? init[pole * S.n + i] : 0.0;
+  for (long long c0 = 0; c0 < n_rep; c0 += chunk) {
+    const long long c1 = c0 + chunk < n_rep ? c0 + chunk : n_rep;
+    double part = 0.0;
+    double* acc = init ? &row : &part;
+    for (long long r = c0; r < c1; ++r) {
+      const long long j = pole * n_rep + r;
+      if (side_of[j] != side) continue;
+      const int k = kind[j];
+      if (k != IDW_NORMAL) {
+        if (idx[j] == i) *acc += 1.0;
+        continue;
+      }
+      const double* xw = x + j * d;
+      double dx0 = xw[0] - a[0], dx1 = xw[1] - a[1];
+      double d2 = dx0 * dx0 + dx1 * dx1;
+      if (d == 3) {
+        double dx2 = xw[2] - a[2];
+        d2 = d2 + dx2 * dx2;
+      }
+      const double rr = sqrt(d2);
+      double base = S.radii[i] - rr;
+      if (base > 0.0) {
+        base = base / (S.radii[i] * rr);
+        double w = base;
+        for (int q = 0; q < S.power - 1; ++q) w = w * base;
+        *acc += w / total[j];
+      }
+    }
+    if (!init) row += part;
+  }
+  out[pole * S.n + i] = row;
+}
+
+cudaError_t launch_idw(const Ref64Params& P, const double* x, const long long* comp,
+                       long long n_poles, long long n_rep, long long chunk,
+                       const double* a0, const double* r0, int n0, int pw0, int wk0,
+                       const double* a1, const double* r1, int n1, int pw1, int wk1, int* kind,
+                       long long* idx, double* total, int* side, double* out0, double* out1,
+                       const double* init0, const double* init1, cudaStream_t s) {
+  const IdwSide s0{a0, r0, n0, pw0, wk0}, s1{a1, r1, n1, pw1, wk1};
+  const long long nw = n_poles * n_rep;
+  if (nw > 0)
+    idw_prep_kernel<<<(unsigned)((nw + 127) / 128), 128, 0, s>>>(P, x, comp, nw, s0, s1, kind,
+                                                                  idx, total, side);
+  const long long nt = n_poles * ((long long)n0 + n1);
+  if (nt > 0)
+    idw_scatter_kernel<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(
+        P, x, n_poles, n_rep, chunk, s0, s1, kind, idx, total, side, out0, out1, init0, init1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s) {
   if (mode == 0)
     r64::walk_ref64_kernel<0><<<grid, block, 0, s>>>(P);

@@ -45,3 +45,8 @@ def oracle():
 
     O.lib()
     return O
+
+
+@pytest.fixture(scope="session")
+def golden_idw():
+    return _load("idw.npz")

@@ -13,6 +13,9 @@ Fixtures:
   cases.npz       the six geometry/K cases of T/test_backend.py:65-72:
                   walk_exits_chunk and accumulate_chunk outputs of the
                   reference kernel, plus a budget-error case
+  idw.npz         IDW families (annulus, square_hole): accumulate_chunk from
+                  non-zero initial rows, and run_accumulate over 2 x 10000
+                  walks (per-8192-chunk partial sums)
   baseline_cfg.npz  BASELINE cfg1-cfg4 in the reference expression
                    at reduced size: run_accumulate
                   count rows and step statistics
@@ -129,6 +132,43 @@ def main():
                                 side1.idw_radii, 2, np.zeros(side0.size), np.zeros(side1.size))
     data["budget_err"] = np.int64(res[4])
     np.savez_compressed(OUT / "cases.npz", **data)
+
+    # ---- IDW weight families (T/test_backend.py:132-140 cases; S/_kernel.pyx:323-369) ----
+    from exitmeasure.geometry import side_points as _sp
+    from exitmeasure.weights import idw_radii_for
+
+    idw = {}
+    for name, dom, kt, pole, eps in (cases[1], cases[3]):
+        d = dom.dimension
+        a1 = _sp(dom, "gamma1", [60] * len(dom.gamma1))
+        s1 = backend.pack_side(a1, d, eps, "idw", idw_radii_for(a1), 2)
+        a0 = _sp(dom, "gamma0", [80 * len(dom.gamma0)])
+        s0 = backend.pack_side(a0, d, eps, "idw", idw_radii_for(a0), 3)
+        g = backend.pack_geometry(dom)
+        ks = np.ascontiguousarray(kt.k_sqrt)
+        pole = np.asarray(pole, dtype=float)
+        # chunk contract: in place from non-zero initial values
+        o0 = np.linspace(0.0, 1.0, s0.size)
+        o1 = np.linspace(0.5, 2.0, s1.size)
+        init0, init1 = o0.copy(), o1.copy()
+        st = impl.accumulate_chunk(g.gi, g.gf, g.comp_side, ks, pole, 0, 0, 3000, 7, eps, 10**6,
+                                   s0.anchors, s0.blk, s0.blkf, 1, s0.idw_radii, s0.idw_power,
+                                   s1.anchors, s1.blk, s1.blkf, 1, s1.idw_radii, s1.idw_power,
+                                   o0, o1)
+        # driver: two poles x 10000 walks (two 8192-chunks per pole)
+        poles2 = np.stack([pole, pole * 0.9])
+        r = backend.run_accumulate(dom, ks, poles2, 11, eps, 10**6, 10000, s0, s1, threads=4)
+        pre = "idw_" + name + "."
+        idw.update({pre + "gi": g.gi, pre + "gf": g.gf, pre + "comp_side": g.comp_side,
+                    pre + "ksqrt": ks, pre + "pole": pole, pre + "eps": np.float64(eps),
+                    pre + "a0": s0.anchors, pre + "blk0": s0.blk, pre + "blkf0": s0.blkf,
+                    pre + "r0": s0.idw_radii, pre + "a1": s1.anchors, pre + "blk1": s1.blk,
+                    pre + "blkf1": s1.blkf, pre + "r1": s1.idw_radii,
+                    pre + "init0": init0, pre + "init1": init1, pre + "out0": o0,
+                    pre + "out1": o1, pre + "stats": np.array(st, dtype=np.int64),
+                    pre + "poles2": poles2, pre + "raw0": r.raw0, pre + "raw1": r.raw1,
+                    pre + "rsteps": r.steps_sum, pre + "rfb": np.int64(r.idw_fallbacks)})
+    np.savez_compressed(OUT / "idw.npz", **idw)
 
     # ---- BASELINE configs in the reference expression (reduced size) ----
     sys.path.insert(0, str(ROOT))

@@ -265,3 +265,25 @@ def test_fp32_exits_stay_in_closure(B, idx):
         assert sd.max() <= cfg.eps * (1 + 1e-5) + 1e-7
         assert sd.min() >= -4 * 2.0**-23, sd.min()
         assert steps.min() >= 1
+
+
+@pytest.mark.parametrize("name", ["annulus", "square_hole"])
+def test_ref64_idw_bit_identical(B, golden_idw, name):
+    """IDW on the GPU: same rows as the reference bit for bit, in place from
+    non-zero initial values (chunk API) and through the batched driver with
+    the reference's per-8192-chunk partial sums."""
+    c = case(golden_idw, "idw_" + name)
+    o0, o1 = c["init0"].copy(), c["init1"].copy()
+    st = B.accumulate_chunk(c["gi"], c["gf"], c["comp_side"], c["ksqrt"], c["pole"], 0, 0, 3000,
+                            7, float(c["eps"]), 10**6, c["a0"], c["blk0"], c["blkf0"], 1, c["r0"],
+                            3, c["a1"], c["blk1"], c["blkf1"], 1, c["r1"], 2, o0, o1)
+    assert np.array_equal(o0, c["out0"]) and np.array_equal(o1, c["out1"])
+    assert list(st) == [int(v) for v in c["stats"]]
+    geom = B.GeomPack(c["gi"], c["gf"], c["comp_side"])
+    s0 = B.SidePack(c["a0"], c["blk0"], c["blkf0"], 1, c["r0"], 3)
+    s1 = B.SidePack(c["a1"], c["blk1"], c["blkf1"], 1, c["r1"], 2)
+    with B.Plan(geom, c["ksqrt"], c["poles2"], float(c["eps"]), 10**6, s0, s1,
+                precision="ref64") as plan:
+        r = plan.run(11, 10000)
+    assert np.array_equal(r.raw0, c["raw0"]) and np.array_equal(r.raw1, c["raw1"])
+    assert np.array_equal(r.steps_sum, c["rsteps"]) and r.idw_fallbacks == int(c["rfb"])

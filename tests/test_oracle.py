@@ -151,3 +151,28 @@ def test_lbox_distance_and_walks(oracle):
         geom.gi, geom.gf, geom.comp_side, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
         cfg.n_rep, (s0.anchors, s0.blk, s0.blkf), (s1.anchors, s1.blk, s1.blkf))
     assert np.array_equal(raw0.sum(1) + raw1.sum(1), np.full(6, 300.0))
+
+
+def _idw_sides(c):
+    return ((c["a0"], c["blk0"], c["blkf0"], 1, c["r0"], 3),
+            (c["a1"], c["blk1"], c["blkf1"], 1, c["r1"], 2))
+
+
+@pytest.mark.parametrize("name", ["annulus", "square_hole"])
+def test_idw_bit_identical_to_reference(oracle, golden_idw, name):
+    """IDW families (S/_kernel.pyx:323-369): the chunk contract accumulating
+    in place from non-zero rows, and the driver's per-8192-chunk partials
+    merged in job order -- both bit for bit."""
+    c = case(golden_idw, "idw_" + name)
+    s0, s1 = _idw_sides(c)
+    o0, o1 = c["init0"].copy(), c["init1"].copy()
+    st = oracle.accumulate_chunk(c["gi"], c["gf"], c["comp_side"], c["ksqrt"], c["pole"], 0, 0,
+                                 3000, 7, float(c["eps"]), 10**6, *s0, *s1, o0, o1)
+    assert np.array_equal(o0, c["out0"]) and np.array_equal(o1, c["out1"])
+    assert list(st) == [int(v) for v in c["stats"]]
+    raw0, raw1, ss, _, _, fb, err = oracle.run_accumulate_packed(
+        c["gi"], c["gf"], c["comp_side"], c["ksqrt"], c["poles2"], 11, float(c["eps"]), 10**6,
+        10000, s0, s1, threads=3)
+    assert err is None
+    assert np.array_equal(raw0, c["raw0"]) and np.array_equal(raw1, c["raw1"])
+    assert np.array_equal(ss, c["rsteps"]) and fb == int(c["rfb"])
