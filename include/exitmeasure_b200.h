@@ -180,6 +180,14 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                     const double* init0, const double* init1, double* raw0, double* raw1,
                     int64_t* stats, int64_t* idw_fallbacks, int64_t* err_pole, int64_t* err_rep);
 
+/* Bin arbitrary points (n, d) with the plan's rule: owner component ->
+ * side -> nearest anchor of that side's family (exact lexicographic FP64 on
+ * REF64, the walk kernel's FP32 binner otherwise).  Cell measures of
+ * unstructured families by boundary quadrature use it (S/weights.py:155-181
+ * rejects generic anchors). */
+int em_bin_points(em_plan* p, const double* pts, int64_t n, int64_t* comp, int64_t* side,
+                  int64_t* bin);
+
 /* One-shot convenience: create, run, destroy. */
 int em_run_accumulate(const em_geometry* g, const em_side* s0, const em_side* s1,
                       const double* poles, const int64_t* pole_ids, int64_t n_poles,

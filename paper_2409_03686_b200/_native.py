@@ -103,6 +103,7 @@ def lib():
         "em_run_exits": ([_p, _u64, _i64, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
         "em_plan_run_raw": ([_p, _u64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p],
                             ctypes.c_int),
+        "em_bin_points": ([_p, _p, _i64, _p, _p, _p], ctypes.c_int),
         "em_fp32_peak": ([ctypes.c_int, _p, _p], ctypes.c_int),
         "em_philox4x64_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "em_philox4x32_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),

@@ -387,6 +387,18 @@ class Plan:
             raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
         return x, steps, comp
 
+    def bin_points(self, pts):
+        """(component, side, anchor index) of each point under the plan's
+        binning rule (owner component -> side -> nearest anchor)."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, self.d)
+        n = pts.shape[0]
+        comp = np.empty(n, dtype=np.int64)
+        side = np.empty(n, dtype=np.int64)
+        bins = np.empty(n, dtype=np.int64)
+        N.check(N.lib().em_bin_points(self._h, N.ptr(pts), n, N.ptr(comp), N.ptr(side),
+                                      N.ptr(bins)), "em_bin_points")
+        return comp, side, bins
+
     def last_stats(self):
         ms = ctypes.c_double(0)
         w = ctypes.c_int64(0)

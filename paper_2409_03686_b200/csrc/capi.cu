@@ -30,6 +30,12 @@ cudaError_t launch_idw(const Ref64Params& P, const double* x, const long long* c
                        const double* a1, const double* r1, int n1, int pw1, int wk1, int* kind,
                        long long* idx, double* total, int* side, double* out0, double* out1,
                        const double* init0, const double* init1, cudaStream_t s);
+cudaError_t launch_bin_points_ref64(const Ref64Params& P, const double* pts, long long n,
+                                    long long* comp, long long* side, long long* bin,
+                                    cudaStream_t s);
+cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const double* pts,
+                                  long long n, long long* comp, long long* side, long long* bin,
+                                  cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
@@ -898,6 +904,31 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
   if (err_pole) *err_pole = -1;
   if (err_rep) *err_rep = -1;
   p->last_launches = 3;
+  return EM_OK;
+}
+
+int em_bin_points(em_plan* p, const double* pts, int64_t n, int64_t* comp, int64_t* side,
+                  int64_t* bin) {
+  if (!p || (n > 0 && (!pts || !comp || !side || !bin))) return fail(EM_ERR_INVALID, "null");
+  if (n <= 0) return EM_OK;
+  DeviceGuard dg(p->device);
+  DevBuf dp, dc, ds, db;
+  cudaError_t ce;
+  if ((ce = dp.alloc((size_t)n * p->d * 8)) != cudaSuccess || (ce = dc.alloc((size_t)n * 8)) != cudaSuccess ||
+      (ce = ds.alloc((size_t)n * 8)) != cudaSuccess || (ce = db.alloc((size_t)n * 8)) != cudaSuccess)
+    return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+  EM_CUDA(cudaMemcpyAsync(dp.p, pts, (size_t)n * p->d * 8, cudaMemcpyHostToDevice, p->stream));
+  cudaError_t e = p->precision == EM_PREC_REF64
+                      ? launch_bin_points_ref64(p->p64, dp.as<double>(), n, dc.as<long long>(),
+                                                ds.as<long long>(), db.as<long long>(), p->stream)
+                      : launch_bin_points_f32(p->p32, p->d, p->outer, dp.as<double>(), n,
+                                              dc.as<long long>(), ds.as<long long>(),
+                                              db.as<long long>(), p->stream);
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("bin points: ") + cudaGetErrorString(e));
+  EM_CUDA(cudaMemcpyAsync(comp, dc.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(side, ds.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(bin, db.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaStreamSynchronize(p->stream));
   return EM_OK;
 }
 

@@ -625,6 +625,38 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
 }
 
+// ---- FP32 point binning (same owner/binner as the walk kernel) ----
+template <int D, int OUTER>
+__global__ void bin_points_f32_kernel(const F32Params P, const double* pts, long long n,
+                                      long long* comp_out, long long* side_out,
+                                      long long* bin_out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float xf[3] = {0.0f, 0.0f, 0.0f}, xw[3] = {0.0f, 0.0f, 0.0f};
+  for (int k = 0; k < D; ++k) {
+    xw[k] = (float)pts[j * D + k];
+    xf[k] = (float)(pts[j * D + k] - (double)P.frame[k]);
+  }
+  const int comp = f32::owner<D, OUTER, -1>(P, xf);
+  const int side = P.comp_side[comp];
+  comp_out[j] = comp;
+  side_out[j] = side;
+  bin_out[j] = P.side[side].n_anchors > 0 ? f32::nearest_anchor<D>(side ? P.side[1] : P.side[0], xw) : -1;
+}
+
+cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const double* pts,
+                                  long long n, long long* comp, long long* side, long long* bin,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 127) / 128);
+  if (d == 2 && outer == OUTER_BALL) bin_points_f32_kernel<2, OUTER_BALL><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  else if (d == 2) bin_points_f32_kernel<2, OUTER_BOX><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  else if (outer == OUTER_BALL) bin_points_f32_kernel<3, OUTER_BALL><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  else if (outer == OUTER_BOX) bin_points_f32_kernel<3, OUTER_BOX><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  else bin_points_f32_kernel<3, OUTER_LBOX><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  return cudaGetLastError();
+}
+
 // ---- FP32 issue-rate micro-benchmark (roofline denominator) ----
 __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
   float v[8];

@@ -462,6 +462,32 @@ cudaError_t launch_idw(const Ref64Params& P, const double* x, const long long* c
   return cudaGetLastError();
 }
 
+// Bin arbitrary points with the exact reference rule: owner component ->
+// side -> lexicographic nearest anchor (S/_kernel.pyx:145-156,242-320).  Used
+// for cell measures by boundary quadrature (S/weights.py:155-181).
+__global__ void bin_points_ref64_kernel(const Ref64Params P, const double* pts, long long n,
+                                        long long* comp_out, long long* side_out,
+                                        long long* bin_out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int d = P.d;
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < d; ++k) x[k] = pts[j * d + k];
+  const int comp = r64::owner_component(P, x);
+  const int side = P.comp_side[comp];
+  comp_out[j] = comp;
+  side_out[j] = side;
+  bin_out[j] = P.side[side].n_anchors > 0 ? r64::assign_anchor(x, d, P.side[side]) : -1;
+}
+
+cudaError_t launch_bin_points_ref64(const Ref64Params& P, const double* pts, long long n,
+                                    long long* comp, long long* side, long long* bin,
+                                    cudaStream_t s) {
+  if (n > 0)
+    bin_points_ref64_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, pts, n, comp, side, bin);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s) {
   if (mode == 0)
     r64::walk_ref64_kernel<0><<<grid, block, 0, s>>>(P);
