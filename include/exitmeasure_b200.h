@@ -157,6 +157,12 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
 int em_plan_destroy(em_plan* p);
 /* walks rep in [rep_start, rep_start + n_rep) for every pole; host outputs */
 int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_outputs* out);
+/* same, but the whole output block -- counts (n_poles, n0 + n1) | stats
+ * (3, n_poles) int64 -- is copied once into a plan-owned page-locked buffer
+ * and *block points at it (valid until the next run or destroy): no extra
+ * host copy for callers that convert the rows anyway. */
+int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                     const int64_t** block, int64_t* err_pole, int64_t* err_rep);
 /* same, outputs left in device memory (caller-owned, zeroed by the library)
  * and work ordered on `stream` (cudaStream_t, NULL = the plan's stream) */
 int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,

@@ -91,6 +91,8 @@ def lib():
                             ctypes.POINTER(EmOptions), ctypes.POINTER(_p)], ctypes.c_int),
         "em_plan_destroy": ([_p], ctypes.c_int),
         "em_plan_run": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs)], ctypes.c_int),
+        "em_plan_run_host": ([_p, _u64, _i64, _i64, ctypes.POINTER(ctypes.POINTER(_i64)), _p, _p],
+                             ctypes.c_int),
         "em_plan_run_device": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs), _p],
                                ctypes.c_int),
         "em_plan_last_stats": ([_p, _p, _p, _p], ctypes.c_int),

@@ -242,16 +242,35 @@ def accumulate_chunk(gi, gf, comp_side, ksqrt, pole_xy, pole_index, rep_start, r
 # batched driver
 
 
-@dataclass(eq=False)
 class AccumulateResult:
-    raw0: np.ndarray  # (n_poles, M0) exit weight sums (not yet / N)
-    raw1: np.ndarray
-    steps_sum: np.ndarray  # (n_poles,) int64
-    steps_sq_sum: np.ndarray
-    steps_max: np.ndarray
-    idw_fallbacks: int
-    counts: np.ndarray | None = None  # (n_poles, M0 + M1) int64, exact
-    kernel_ms: float = 0.0
+    """Per-pole exit rows of a run (S/backend.py:137-144's fields).
+
+    ``counts`` holds the exact int64 rows (side-0 columns first); ``raw0`` /
+    ``raw1`` are the reference's float64 views of them, converted on first
+    access (IDW runs set them directly: their rows are fractional)."""
+
+    def __init__(self, raw0=None, raw1=None, steps_sum=None, steps_sq_sum=None, steps_max=None,
+                 idw_fallbacks: int = 0, counts=None, kernel_ms: float = 0.0, n0: int | None = None):
+        self._raw0, self._raw1 = raw0, raw1
+        self.steps_sum = steps_sum
+        self.steps_sq_sum = steps_sq_sum
+        self.steps_max = steps_max
+        self.idw_fallbacks = idw_fallbacks
+        self.counts = counts
+        self.kernel_ms = kernel_ms
+        self._n0 = n0 if n0 is not None else (raw0.shape[1] if raw0 is not None else 0)
+
+    @property
+    def raw0(self) -> np.ndarray:
+        if self._raw0 is None:
+            self._raw0 = self.counts[:, : self._n0].astype(np.float64)
+        return self._raw0
+
+    @property
+    def raw1(self) -> np.ndarray:
+        if self._raw1 is None:
+            self._raw1 = self.counts[:, self._n0:].astype(np.float64)
+        return self._raw1
 
 
 class Plan:
@@ -340,21 +359,21 @@ class Plan:
         if self.idw:
             return self.run_raw(seed, n_rep, rep_start)
         row = self.n0 + self.n1
-        counts = np.zeros((self.n_poles, row), dtype=np.int64)
-        stats = np.zeros((3, self.n_poles), dtype=np.int64)
-        out = N.EmOutputs(N.ptr(counts), N.ptr(stats[0]), N.ptr(stats[1]), N.ptr(stats[2]),
-                          -1, -1)
-        rc = N.check(N.lib().em_plan_run(self._h, int(seed) & (2**64 - 1), int(rep_start),
-                                         int(n_rep), ctypes.byref(out)), "em_plan_run")
+        blk = ctypes.POINTER(ctypes.c_int64)()
+        ep, er = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = N.check(N.lib().em_plan_run_host(self._h, int(seed) & (2**64 - 1), int(rep_start),
+                                              int(n_rep), ctypes.byref(blk), ctypes.byref(ep),
+                                              ctypes.byref(er)), "em_plan_run_host")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(out.err_pole), int(rep_start + out.err_rep),
-                                  self.max_steps)
+            raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
+        nc = self.n_poles * row
+        view = np.ctypeslib.as_array(blk, shape=(nc + 3 * self.n_poles,))
+        counts = view[:nc].reshape(self.n_poles, row)
+        stats = view[nc:].reshape(3, self.n_poles)
         ms = ctypes.c_double(0)
         N.lib().em_plan_last_stats(self._h, ctypes.byref(ms), None, None)
-        return AccumulateResult(counts[:, : self.n0].astype(np.float64),
-                                counts[:, self.n0:].astype(np.float64),
-                                stats[0].copy(), stats[1].copy(), stats[2].copy(), 0,
-                                counts, ms.value)
+        return AccumulateResult(None, None, stats[0].copy(), stats[1].copy(), stats[2].copy(),
+                                0, counts.copy(), ms.value, n0=self.n0)
 
     def run_device(self, seed: int, n_rep: int, counts_ptr: int, stats_ptr: int,
                    stream_ptr: int | None = None, rep_start: int = 0) -> None:

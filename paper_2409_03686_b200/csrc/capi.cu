@@ -80,8 +80,7 @@ struct BufCache {
   std::vector<std::pair<size_t, void*>> free_bufs;  // (capacity, ptr) per device below
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> events;
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
+  std::vector<std::pair<size_t, void*>> free_pinned;
 };
 
 static BufCache& cache_of(int dev) {
@@ -139,6 +138,43 @@ struct DevBuf {
   }
 };
 
+// page-locked host staging, recycled like the device buffers
+struct PinBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int dev = 0;
+  ~PinBuf() { release(); }
+  void release() {
+    if (!p) return;
+    BufCache& c = cache_of(dev);
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.free_pinned.push_back({bytes, p});
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t alloc(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    release();
+    cudaGetDevice(&dev);
+    const size_t cap = round_cap(std::max<size_t>(n, 16));
+    {
+      BufCache& c = cache_of(dev);
+      std::lock_guard<std::mutex> lk(c.mu);
+      for (size_t i = 0; i < c.free_pinned.size(); ++i)
+        if (c.free_pinned[i].first == cap) {
+          p = c.free_pinned[i].second;
+          bytes = cap;
+          c.free_pinned.erase(c.free_pinned.begin() + i);
+          return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocDefault);
+    if (e == cudaSuccess) bytes = cap;
+    else p = nullptr;
+    return e;
+  }
+};
+
 static cudaStream_t take_stream(int dev) {
   BufCache& c = cache_of(dev);
   {
@@ -186,7 +222,12 @@ struct em_plan {
   Ref64Params p64{};
   F32Params p32{};
   DevBuf poles, pole_ids, anchors[2], gcell[2], gcand[2];
-  DevBuf counts, stats, misc;  // stats: 3 * n_poles u64; misc: err, ticket, walks
+  // one output block: counts (n_poles x row) | stats (3 x n_poles) | misc (err, ticket)
+  DevBuf counts, stats, misc;
+  PinBuf pin;  // host staging of the output block
+  bool pin_valid = false;
+  unsigned long long *blk_counts = nullptr, *blk_stats = nullptr, *blk_misc = nullptr;
+  size_t blk_words = 0;
   DevBuf xo, so, co;           // exits
   DevBuf radii[2];             // IDW supports (REF64)
   DevBuf ikind, iidx, itot, iside, iraw0, iraw1, iinit0, iinit1;
@@ -436,9 +477,11 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
 #define EM_ALLOC(buf, bytes)                                                          \
   if ((ce = (buf).alloc(bytes)) != cudaSuccess)                                       \
     return bail(fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce)));
-  EM_ALLOC(p->counts, (size_t)n_poles * row * 8);
-  EM_ALLOC(p->stats, (size_t)n_poles * 3 * 8);
-  EM_ALLOC(p->misc, 8 * 8);
+  p->blk_words = (size_t)n_poles * row + 3 * (size_t)n_poles + 8;
+  EM_ALLOC(p->counts, p->blk_words * 8);
+  p->blk_counts = p->counts.as<unsigned long long>();
+  p->blk_stats = p->blk_counts + (size_t)n_poles * row;
+  p->blk_misc = p->blk_stats + 3 * (size_t)n_poles;
   if (pole_ids) {
     EM_ALLOC(p->pole_ids, (size_t)n_poles * 8);
     if (cudaMemcpy(p->pole_ids.p, pole_ids, n_poles * 8, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -449,12 +492,12 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   w.n_poles = n_poles;
   w.inv_poles = 1.0 / (double)n_poles;
   w.pole_ids = pole_ids ? p->pole_ids.as<long long>() : nullptr;
-  w.ticket = p->misc.as<unsigned long long>() + 1;
-  w.err_key = p->misc.as<unsigned long long>();
-  w.counts = p->counts.as<unsigned long long>();
+  w.ticket = p->blk_misc + 1;
+  w.err_key = p->blk_misc;
+  w.counts = p->blk_counts;
   w.row_len = (int)row;
   w.col_off1 = (int)p->n0;
-  w.ssum = p->stats.as<unsigned long long>();
+  w.ssum = p->blk_stats;
   w.ssq = w.ssum + n_poles;
   w.smax = w.ssq + n_poles;
 
@@ -668,12 +711,15 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   w->smax = stats + 2 * p->n_poles;
   const int64_t row = p->n0 + p->n1;
   int64_t launches = 0;
-  if (mode == 0) {
-    EM_CUDA(cudaMemsetAsync(counts, 0, (size_t)p->n_poles * row * 8, s));
-    EM_CUDA(cudaMemsetAsync(stats, 0, (size_t)p->n_poles * 3 * 8, s));
+  if (mode == 0 && counts == p->blk_counts) {
+    EM_CUDA(cudaMemsetAsync(p->blk_counts, 0, p->blk_words * 8, s));  // counts | stats | misc
+  } else {
+    if (mode == 0) {
+      EM_CUDA(cudaMemsetAsync(counts, 0, (size_t)p->n_poles * row * 8, s));
+      EM_CUDA(cudaMemsetAsync(stats, 0, (size_t)p->n_poles * 3 * 8, s));
+    }
+    EM_CUDA(cudaMemsetAsync(p->blk_misc, 0, 64, s));
   }
-  EM_CUDA(cudaMemsetAsync(p->misc.p, 0, 64, s));
-  EM_CUDA(cudaMemsetAsync(p->misc.p, 0xff, 8, s));  // err_key = ~0
   if (total > 0) {
     const int64_t lanes_needed = (total + 31) / 32 * 32;
     int grid = p->grid;
@@ -702,9 +748,15 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
 
 static int plan_finish(em_plan* p, cudaStream_t s, int64_t n_rep, em_outputs* out,
                        const unsigned long long* host_stats) {
-  unsigned long long err = ~0ULL;
-  EM_CUDA(cudaMemcpyAsync(&err, p->misc.p, 8, cudaMemcpyDeviceToHost, s));
-  EM_CUDA(cudaStreamSynchronize(s));
+  unsigned long long errv = 0;
+  if (p->pin.p && p->pin_valid) {
+    EM_CUDA(cudaStreamSynchronize(s));
+    errv = reinterpret_cast<const unsigned long long*>(p->pin.p)[p->blk_words - 8];
+  } else {
+    EM_CUDA(cudaMemcpyAsync(&errv, p->blk_misc, 8, cudaMemcpyDeviceToHost, s));
+    EM_CUDA(cudaStreamSynchronize(s));
+  }
+  const unsigned long long err = errv ? ~errv : ~0ULL;
   float ms = 0.0f;
   if (p->last_launches) {
     EM_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
@@ -726,23 +778,47 @@ static int plan_finish(em_plan* p, cudaStream_t s, int64_t n_rep, em_outputs* ou
   return EM_OK;
 }
 
+// run + one D2H of the whole output block into the plan's pinned staging
+static int plan_run_staged(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                           em_outputs* out) {
+  DeviceGuard dg(p->device);
+  int rc = plan_launch(p, seed, rep_start, n_rep, 0, p->blk_counts, p->blk_stats, p->stream);
+  if (rc) return rc;
+  cudaError_t ce = p->pin.alloc(p->blk_words * 8);
+  if (ce != cudaSuccess) return fail(EM_ERR_NOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce));
+  EM_CUDA(cudaMemcpyAsync(p->pin.p, p->blk_counts, p->blk_words * 8, cudaMemcpyDeviceToHost, p->stream));
+  p->pin_valid = true;
+  rc = plan_finish(p, p->stream, n_rep, out,
+                   reinterpret_cast<const unsigned long long*>(p->pin.p) +
+                       (size_t)p->n_poles * (p->n0 + p->n1));
+  p->pin_valid = false;
+  return rc;
+}
+
 int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_outputs* out) {
   if (!p || !out || !out->counts || !out->steps_sum || !out->steps_sq || !out->steps_max)
     return fail(EM_ERR_INVALID, "plan/outputs null");
-  DeviceGuard dg(p->device);
-  int rc = plan_launch(p, seed, rep_start, n_rep, 0, p->counts.as<unsigned long long>(),
-                       p->stats.as<unsigned long long>(), p->stream);
-  if (rc) return rc;
-  const int64_t row = p->n0 + p->n1;
-  EM_CUDA(cudaMemcpyAsync(out->counts, p->counts.p, (size_t)p->n_poles * row * 8,
-                          cudaMemcpyDeviceToHost, p->stream));
-  EM_CUDA(cudaMemcpyAsync(out->steps_sum, p->stats.p, p->n_poles * 8, cudaMemcpyDeviceToHost, p->stream));
-  EM_CUDA(cudaMemcpyAsync(out->steps_sq, p->stats.as<char>() + p->n_poles * 8, p->n_poles * 8,
-                          cudaMemcpyDeviceToHost, p->stream));
-  EM_CUDA(cudaMemcpyAsync(out->steps_max, p->stats.as<char>() + 2 * p->n_poles * 8, p->n_poles * 8,
-                          cudaMemcpyDeviceToHost, p->stream));
-  return plan_finish(p, p->stream, n_rep, out,
-                     reinterpret_cast<const unsigned long long*>(out->steps_sum));
+  int rc = plan_run_staged(p, seed, rep_start, n_rep, out);
+  if (rc < 0) return rc;
+  const size_t nc = (size_t)p->n_poles * (p->n0 + p->n1);
+  const int64_t* h = reinterpret_cast<const int64_t*>(p->pin.p);
+  std::memcpy(out->counts, h, nc * 8);
+  std::memcpy(out->steps_sum, h + nc, p->n_poles * 8);
+  std::memcpy(out->steps_sq, h + nc + p->n_poles, p->n_poles * 8);
+  std::memcpy(out->steps_max, h + nc + 2 * p->n_poles, p->n_poles * 8);
+  return rc;
+}
+
+int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                     const int64_t** block, int64_t* err_pole, int64_t* err_rep) {
+  if (!p || !block) return fail(EM_ERR_INVALID, "plan/block null");
+  em_outputs o{};
+  int rc = plan_run_staged(p, seed, rep_start, n_rep, &o);
+  if (rc < 0) return rc;
+  *block = reinterpret_cast<const int64_t*>(p->pin.p);
+  if (err_pole) *err_pole = o.err_pole;
+  if (err_rep) *err_rep = o.err_rep;
+  return rc;
 }
 
 int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
@@ -807,8 +883,7 @@ int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, do
   w->x_out = p->xo.as<double>();
   w->steps_out = p->so.as<long long>();
   w->comp_out = p->co.as<long long>();
-  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->counts.as<unsigned long long>(),
-                       p->stats.as<unsigned long long>(), p->stream);
+  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->blk_counts, p->blk_stats, p->stream);
   if (rc) return rc;
   if (total > 0) {
     EM_CUDA(cudaMemcpyAsync(x_out, p->xo.p, total * p->d * 8, cudaMemcpyDeviceToHost, p->stream));
@@ -844,8 +919,7 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
   w->x_out = p->xo.as<double>();
   w->steps_out = p->so.as<long long>();
   w->comp_out = p->co.as<long long>();
-  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->counts.as<unsigned long long>(),
-                       p->stats.as<unsigned long long>(), p->stream);
+  int rc = plan_launch(p, seed, rep_start, n_rep, 1, p->blk_counts, p->blk_stats, p->stream);
   if (rc) return rc;
   const double* d_init0 = nullptr;
   const double* d_init1 = nullptr;
@@ -860,8 +934,9 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
   }
   // budget check before binning: outputs are meaningless after a failure
   unsigned long long err = ~0ULL;
-  EM_CUDA(cudaMemcpyAsync(&err, p->misc.p, 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(&err, p->blk_misc, 8, cudaMemcpyDeviceToHost, p->stream));
   EM_CUDA(cudaStreamSynchronize(p->stream));
+  err = err ? ~err : ~0ULL;
   if (err != ~0ULL) {
     if (err_pole) *err_pole = n_rep > 0 ? (int64_t)(err / (unsigned long long)n_rep) : 0;
     if (err_rep) *err_rep = n_rep > 0 ? (int64_t)(err % (unsigned long long)n_rep) : 0;

@@ -54,7 +54,10 @@ struct WorkOut {
   unsigned long long* ticket;                  // global chunk counter
   unsigned long long* counts;                  // (n_poles, row_len)
   int row_len, col_off1;                       // side-1 column offset
-  unsigned long long *ssum, *ssq, *smax, *err_key;
+  unsigned long long *ssum, *ssq, *smax;
+  // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
+  // output block means "no failure" and the smallest key wins
+  unsigned long long* err_key;
   // exits mode (em_run_exits / walk_exits_chunk)
   double* x_out;
   long long* steps_out;

@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
       if (failed)
-        atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
+        atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
       if (!walking) {
         failed = 0;
         inflight = 0;

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     }
     if (steps >= P.max_steps) {
       active = false;
-      atomicMin(W.err_key, (unsigned long long)((long long)pole * W.n_rep + rep_off));
+      atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
       if (MODE == 1) {
         const long long o = (long long)pole * W.n_rep + rep_off;
         for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];

@@ -60,17 +60,24 @@ def run_accumulate_sharded(dom, ksqrt, poles, seed: int, eps: float, max_steps: 
     poles = np.ascontiguousarray(poles, dtype=np.float64)
     ids = shard_rows(poles.shape[0], world, rank)
     geom = pack_geometry(dom)
+    nccl = dist.get_backend(group) == "nccl"
     with Plan(geom, ksqrt, poles[ids], eps, max_steps, side0, side1, precision, chain, device,
               pole_ids=ids) as plan:
-        res = plan.run(seed, n_rep)
-    dev = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else torch.device("cpu")
-    counts = torch.as_tensor(res.counts, device=dev)
-    stats = torch.as_tensor(np.stack([res.steps_sum, res.steps_sq_sum, res.steps_max], 1),
-                            device=dev)
+        if nccl:  # rows stay in HBM: walk, all-gather over NVLink, one copy back
+            dev = torch.device("cuda", device)
+            row = plan.n0 + plan.n1
+            counts = torch.zeros((len(ids), row), dtype=torch.int64, device=dev)
+            stats3 = torch.zeros((3, len(ids)), dtype=torch.int64, device=dev)
+            plan.run_device(seed, n_rep, counts.data_ptr(), stats3.data_ptr(),
+                            torch.cuda.current_stream(dev).cuda_stream)
+            stats = stats3.t().contiguous()
+            ms = plan.last_stats()[0]
+        else:
+            res = plan.run(seed, n_rep)
+            counts = torch.as_tensor(res.counts)
+            stats = torch.as_tensor(np.stack([res.steps_sum, res.steps_sq_sum, res.steps_max], 1))
+            ms = res.kernel_ms
     full_counts = gather_rows(counts, poles.shape[0], world, group).cpu().numpy()
     full_stats = gather_rows(stats, poles.shape[0], world, group).cpu().numpy()
-    n0 = side0.size
-    return AccumulateResult(full_counts[:, :n0].astype(np.float64),
-                            full_counts[:, n0:].astype(np.float64), full_stats[:, 0].copy(),
-                            full_stats[:, 1].copy(), full_stats[:, 2].copy(), 0, full_counts,
-                            res.kernel_ms)
+    return AccumulateResult(None, None, full_stats[:, 0].copy(), full_stats[:, 1].copy(),
+                            full_stats[:, 2].copy(), 0, full_counts, ms, n0=side0.size)
