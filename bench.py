@@ -43,7 +43,7 @@ F_STEP = {
     # kernels" derives each entry term by term from walk_f32.cu
     (1, "woe"): (13, 3), (1, "max"): (13, 3),   # K = I: both chains are the sphere step
     (2, "woe"): (18, 2), (2, "max"): (21, 2),
-    (3, "woe"): (24, 4), (3, "max"): (58, 10),
+    (3, "woe"): (24, 4), (3, "max"): (44, 7),    # concentric hole: shared |v|, |Av|, one rcp
     (4, "woe"): (31, 4), (4, "max"): (51, 7),
     (5, "woe"): (43, 4), (5, "max"): (53, 4),
 }

@@ -568,9 +568,13 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       scale = std::max(scale, 2.0 * gf[d]);
     }
     for (int j = 0; j < 3; ++j) P.frame[j] = (float)frame[j];
+    P.concentric = (g->gi[1] == 0 && nh > 0) ? 1 : 0;
     for (int h = 0; h < nh; ++h) {
       const int off = d + 1 + h * (d + 1);
-      for (int j = 0; j < d; ++j) P.hc[h][j] = (float)(gf[off + j] - frame[j]);
+      for (int j = 0; j < d; ++j) {
+        P.hc[h][j] = (float)(gf[off + j] - frame[j]);
+        if (gf[off + j] != gf[j]) P.concentric = 0;
+      }
       P.hr[h] = (float)gf[off + d];
     }
     if (nn) {

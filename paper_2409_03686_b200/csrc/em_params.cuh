@@ -79,6 +79,7 @@ struct Ref64Params {
 
 struct F32Params {
   int n_holes, has_notch;
+  int concentric;  // every hole shares the outer ball's centre (annulus, shell)
   // The kernel works in a frame where the outer ball's centre / the box's low
   // corner is the origin (saves the per-step x - c); world = frame + offset.
   float frame[3];

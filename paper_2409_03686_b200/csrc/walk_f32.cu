@@ -44,6 +44,40 @@ __device__ __forceinline__ int n_holes(const F32Params& P) {
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
+  if (OUTER == OUTER_BALL && NH == 1 && MAXC && P.concentric) {
+    // annulus / spherical shell: one |v| and one |Av| serve both bounds, and
+    //   r = min(q_o / D_o, max(q_h / D_h, e_h)) = min(q_o / D_o, n_h / D_h)
+    // with n_h = max(q_h, e_h D_h) is picked by cross-multiplication, so a
+    // single reciprocal replaces two divisions (XU-bound step: 10 -> 7 MUFU)
+    const float v0 = x[0], v1 = x[1];
+    const float v2 = D == 3 ? x[2] : 0.0f;
+    float s2 = v0 * v0 + v1 * v1;
+    if (D == 3) s2 = fmaf(v2, v2, s2);
+    const float s = sqrtf(s2);
+    const float rho = P.hr[0];
+    const float eo = P.oR - s, eh = s - rho;
+    e = fminf(eo, eh);
+    float a0, a1, a2 = 0.0f;
+    if (D == 2) {
+      a0 = fmaf(P.A[0], v0, P.A[1] * v1);
+      a1 = fmaf(P.A[2], v0, P.A[3] * v1);
+    } else {
+      a0 = fmaf(P.A[0], v0, fmaf(P.A[1], v1, P.A[2] * v2));
+      a1 = fmaf(P.A[3], v0, fmaf(P.A[4], v1, P.A[5] * v2));
+      a2 = fmaf(P.A[6], v0, fmaf(P.A[7], v1, P.A[8] * v2));
+    }
+    float aa = a0 * a0 + a1 * a1;
+    if (D == 3) aa = fmaf(a2, a2, aa);
+    const float a = sqrtf(aa);
+    const float qo = eo * (P.oR + s);
+    const float Do = a + sqrtf(fmaxf(aa + qo, 0.0f));
+    const float qh = eh * (s + rho);
+    const float Dh = a + sqrtf(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
+    const float nh = fmaxf(qh, eh * Dh);
+    const bool outer = qo * Dh <= nh * Do;
+    r = __fdividef(outer ? qo : nh, outer ? Do : Dh);
+    return;
+  }
   if (OUTER == OUTER_BALL) {
     // kernel frame: the outer ball is centred at the origin
     const float v0 = x[0], v1 = x[1];
