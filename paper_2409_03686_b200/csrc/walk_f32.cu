@@ -119,14 +119,11 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
     }
     if (!MAXC) r = e;
     if (OUTER == OUTER_LBOX) {
+      // distance to the notch prism; a point a rounding step inside it gets
+      // 0, which stops the walk exactly as a negative distance would
       const float qx = P.notch[0] - x[0], qy = P.notch[1] - x[1];
-      float en;
-      if (qx <= 0.0f && qy <= 0.0f) {
-        en = fmaxf(qx, qy);
-      } else {
-        const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
-        en = sqrtf(fmaf(ax, ax, ay * ay));
-      }
+      const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
+      const float en = sqrtf(fmaf(ax, ax, ay * ay));
       e = fminf(e, en);
       if (MAXC)
         r = fminf(r, fmaxf(en, fmaxf(qx * P.g[0], qy * P.g[1])));
@@ -376,33 +373,53 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
 #ifndef EM_BATCH_STEPS
 #define EM_BATCH_STEPS 8
 #endif
+// Random bits per azimuth: 16 (two angles per 32-bit word) or 23.  A uniform
+// grid of 2^16 equally spaced angles averages every Fourier mode |k| < 2^16
+// exactly, so the mean-value property the step relies on holds to that order
+// (DESIGN.md §3.1); 3D keeps 23-bit z.
+#ifndef EM_ANGLE_BITS
+#define EM_ANGLE_BITS 16
+#endif
 template <int D>
 struct Batch {
   static constexpr int kSteps = EM_BATCH_STEPS;
-  static constexpr int kBlocks = D == 2 ? EM_BATCH_STEPS / 4 : EM_BATCH_STEPS / 2;
+  static constexpr int kAngleWords = EM_ANGLE_BITS == 16 ? (kSteps + 1) / 2 : kSteps;
+  static constexpr int kZWords = D == 3 ? kSteps : 0;
+  static constexpr int kWords = kZWords + kAngleWords;
+  static constexpr int kBlocks = (kWords + 3) / 4;
 };
+
+// the angle of step k of a batch from the batch's words
+template <int D>
+__device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k) {
+  if (EM_ANGLE_BITS == 16) {
+    const unsigned w = wv[Batch<D>::kZWords + (k >> 1)];
+    const unsigned m = (k & 1) ? ((w >> 9) & 0x7FFF80u) : ((w << 7) & 0x7FFF80u);
+    return 0x3f800000u | m;  // 1 + bits16 / 2^16
+  }
+  return 0x3f800000u | (wv[Batch<D>::kZWords + k] >> 9);
+}
 
 // One walk-on-ellipsoids step from x (r from dist()): direction from the RNG
 // word(s), y = K^{1/2} u, x += rs y with rs = r shrunk by the FP32 safety
 // margin, or rs = 0 for a lane that is not walking (branch-free: the warp
 // issues the same instructions whether or not every lane is live).
-// Uniform angle on the circle from a word's top 23 bits with ONE FFMA:
-// f = 1 + m/2^23 in [1,2) -> theta = 2 pi f - 3 pi in [-pi, pi).  The 2^23
+// Uniform angle on the circle with ONE FFMA from f = 1 + m/2^b in [1,2)
+// (the float built by angle_bits): theta = 2 pi f - 3 pi in [-pi, pi).  The
 // angles are equally spaced around the circle, so the offset is irrelevant.
-__device__ __forceinline__ float angle23(unsigned w) {
-  const float f = __uint_as_float(0x3f800000u | (w >> 9));
-  return fmaf(f, 6.283185307179586f, -9.42477796076938f);
+__device__ __forceinline__ float angle_of(unsigned fbits) {
+  return fmaf(__uint_as_float(fbits), 6.283185307179586f, -9.42477796076938f);
 }
 
 template <int D, bool IDENT>
-__device__ __forceinline__ void step(const F32Params& P, float* x, float rs, unsigned w0,
-                                     unsigned w1) {
+__device__ __forceinline__ void step(const F32Params& P, float* x, float rs, unsigned zw,
+                                     unsigned afbits) {
   float u0, u1, u2 = 0.0f;
   if (D == 2) {
-    __sincosf(angle23(w0), &u1, &u0);
+    __sincosf(angle_of(afbits), &u1, &u0);
   } else {
-    const float z = sym11_23(w0);
-    const float th = angle23(w1);
+    const float z = sym11_23(zw);
+    const float th = angle_of(afbits);
     const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
     float sn, cs;
     __sincosf(th, &sn, &cs);
@@ -554,10 +571,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
         walking &= (e > P.eps);
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
-        if (D == 2)
-          step<D, IDENT>(P, x, rs, wv[k], 0u);
-        else
-          step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
+        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k));
         steps += walking;
       }
     } else {
@@ -570,10 +584,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
         const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
-        if (D == 2)
-          step<D, IDENT>(P, x, rs, wv[k], 0u);
-        else
-          step<D, IDENT>(P, x, rs, wv[2 * k], wv[2 * k + 1]);
+        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k));
         steps += walking;
       }
     }
