@@ -593,6 +593,15 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     const double lam = sym_min_eig(g->ksqrt, d);
     P.m2 = (float)(std::max(0.0, lam) * std::max(0.0, lam) * (1.0 - 1e-4));
     P.eps = (float)eps;
+    {
+      // scale = 2^k with ulp(eps_f) * 2^k >= 1: every representable e > eps
+      // then gives (e - eps) * scale >= 1 (bias = -eps * scale is exact)
+      int ex = 0;
+      std::frexp((double)P.eps, &ex);  // eps_f in [2^(ex-1), 2^ex)
+      const int k = 24 - (ex - 1) + 1;  // ulp(eps_f) = 2^(ex-1-23)
+      P.stop_scale = std::ldexp(1.0f, k);
+      P.stop_bias = -P.eps * P.stop_scale;
+    }
     P.shrink_rel = 4.0e-6f;
     P.shrink_abs = (float)(scale * 1.1920928955078125e-07);
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);

@@ -92,6 +92,7 @@ struct F32Params {
   float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid
   float m2;         // sigma_min(A)^2 (hole bound)
   float eps;
+  float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
   float shrink_rel, shrink_abs;  // step safety margins
   int max_steps;
   unsigned key0, key1;

@@ -394,7 +394,8 @@ template <int D>
 __device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k) {
   if (EM_ANGLE_BITS == 16) {
     const unsigned w = wv[Batch<D>::kZWords + (k >> 1)];
-    const unsigned m = (k & 1) ? ((w >> 9) & 0x7FFF80u) : ((w << 7) & 0x7FFF80u);
+    // shifts as IMAD.HI / IMAD (FMA pipe), one LOP3 for mask | exponent
+    const unsigned m = (k & 1) ? (__umulhi(w, 1u << 23) & 0x7FFF80u) : ((w * 128u) & 0x7FFF80u);
     return 0x3f800000u | m;  // 1 + bits16 / 2^16
   }
   return 0x3f800000u | (wv[Batch<D>::kZWords + k] >> 9);
@@ -564,16 +565,23 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
     }
     ++draw;
     if (__all_sync(kFull, steps + K <= P.max_steps)) {
-      // fast path: no lane can reach the step budget inside this batch
+      // fast path: no lane can reach the step budget inside this batch.
+      // Bookkeeping on the FMA pipes (the ALU pipe is the busy one): the
+      // live mask is a float, cleared by FFMA.SAT((e - eps) * 2^k) -- exactly
+      // 0 when e <= eps and exactly 1 otherwise, since every representable
+      // positive difference scales to >= 1 -- and multiplies the step scale.
+      float wm = walking ? 1.0f : 0.0f, sf = 0.0f;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         float e, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        walking &= (e > P.eps);
-        const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
+        wm *= __saturatef(fmaf(e, P.stop_scale, P.stop_bias));
+        const float rs = fmaf(r, keep, -P.shrink_abs) * wm;
         step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k));
-        steps += walking;
+        sf += wm;
       }
+      walking = wm != 0.0f;
+      steps += (int)sf;
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
