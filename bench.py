@@ -181,6 +181,30 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
 REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
 
 
+def profiled_traffic(cfg_index: int, precision: str, chain: str):
+    """DRAM bytes per launch of the walk kernel from the committed `ncu --set
+    full` capture of this same command (profiles/r01_cfg2_walk_f32_ncu_raw.csv),
+    or None when no capture matches the configuration."""
+    import csv
+
+    f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
+    if cfg_index != 2 or precision != "fp32" or chain != "max" or not f.exists():
+        return None
+    vals = {}
+    for row in csv.reader(open(f)):
+        if len(row) == 3:
+            vals[row[0]] = (row[1], row[2])
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = vals[k]
+            tot += float(v) * scale[u]
+        return tot
+    except (KeyError, ValueError):
+        return None
+
+
 def run_reference(args):
     world, rank, _ = _dist_env()
     if rank != 0:
@@ -348,7 +372,11 @@ def run_ours(args):
                        "counts": "int64 (n_poles, n0+n1) rows + step stats"},
             "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
                          "unit": "Top/s", "frac": achieved / peak_nominal,
-                         "traffic": None,
+                         "traffic": profiled_traffic(cfg.index, plan.precision, plan.chain),
+                         "traffic_note": "DRAM bytes per launch from the committed ncu --set "
+                                         "full capture (profiles/r01_cfg2_walk_f32_ncu_raw.csv); "
+                                         "algorithmic: the int64 count rows",
+                         "algorithmic_bytes": int(cfg.n_poles * (plan.n0 + plan.n1) * 8),
                          "f_step": {"fp32": fp32, "xu": xu},
                          "peak_note": f"{info['sm_count']} SMs x 128 FP32 lanes x median SM "
                                       f"clock under load {clk_mhz:.0f} MHz (MEASURED_PEAKS.json "
