@@ -553,7 +553,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     const double* gf = g->gf;
     P.n_holes = nh;
     P.has_notch = nn;
-    // kernel frame: origin at the ball centre / the box's low corner
+    // kernel frame: origin at the ball's / box's centre
     double frame[3] = {0.0, 0.0, 0.0};
     double scale = 1.0;
     if (g->gi[1] == 0) {
@@ -562,10 +562,10 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       scale = std::max(scale, gf[d]);
     } else {
       for (int j = 0; j < d; ++j) {
-        frame[j] = gf[j] - gf[d];
-        P.bhi[j] = (float)(2.0 * gf[d]);
+        frame[j] = gf[j];
+        P.bhi[j] = (float)gf[d];
       }
-      scale = std::max(scale, 2.0 * gf[d]);
+      scale = std::max(scale, gf[d]);
     }
     for (int j = 0; j < 3; ++j) P.frame[j] = (float)frame[j];
     P.concentric = (g->gi[1] == 0 && nh > 0) ? 1 : 0;

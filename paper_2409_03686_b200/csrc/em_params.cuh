@@ -80,11 +80,11 @@ struct Ref64Params {
 struct F32Params {
   int n_holes, has_notch;
   int concentric;  // every hole shares the outer ball's centre (annulus, shell)
-  // The kernel works in a frame where the outer ball's centre / the box's low
-  // corner is the origin (saves the per-step x - c); world = frame + offset.
+  // The kernel works in a frame where the outer ball's / box's centre is the
+  // origin (saves the per-step x - c); world = frame + offset.
   float frame[3];
   float oR;      // ball outer: radius
-  float bhi[3];  // box / L-box outer: widths (the box is [0, bhi] in the frame)
+  float bhi[3];  // box / L-box outer: half-widths (the box is [-bhi, bhi] in the frame)
   float hc[EM_MAX_HOLES][3], hr[EM_MAX_HOLES];  // hole centres in the frame
   float notch[2];                               // notch corner in the frame
   signed char comp_side[kMaxComp];

@@ -112,8 +112,9 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
     r = kInf;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      // kernel frame: the box is [0, bhi_i] in every axis
-      const float m = fminf(x[i], P.bhi[i] - x[i]);
+      // kernel frame: the box is [-bhi_i, bhi_i] (centred), so the distance
+      // to the nearer face is one FADD with a free |.| operand
+      const float m = P.bhi[i] - fabsf(x[i]);
       e = fminf(e, m);
       if (MAXC) r = fminf(r, m * P.g[i]);
     }
@@ -177,7 +178,7 @@ __device__ __forceinline__ int owner(const F32Params& P, const float* x) {
   } else {
     float m = kInf;
 #pragma unroll
-    for (int i = 0; i < D; ++i) m = fminf(m, fminf(x[i], P.bhi[i] - x[i]));
+    for (int i = 0; i < D; ++i) m = fminf(m, P.bhi[i] - fabsf(x[i]));
     best = fabsf(m);
   }
   int comp = 0;
@@ -389,14 +390,16 @@ struct Batch {
   static constexpr int kBlocks = (kWords + 3) / 4;
 };
 
-// the angle of step k of a batch from the batch's words
+// The angle of step k of a batch, as theta = fmaf(f, kAngScale, kAngBias)
+// of the float f built from the batch's words.  16-bit angles: ONE byte
+// permute (PRMT) drops a half-word into the low mantissa bytes of 1.0f, so
+// f = 1 + k16 / 2^23, and the FFMA maps the 2^16 values onto equally spaced
+// angles spanning exactly 2 pi (the offset is irrelevant on the circle).
 template <int D>
 __device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k) {
   if (EM_ANGLE_BITS == 16) {
     const unsigned w = wv[Batch<D>::kZWords + (k >> 1)];
-    // shifts as IMAD.HI / IMAD (FMA pipe), one LOP3 for mask | exponent
-    const unsigned m = (k & 1) ? (__umulhi(w, 1u << 23) & 0x7FFF80u) : ((w * 128u) & 0x7FFF80u);
-    return 0x3f800000u | m;  // 1 + bits16 / 2^16
+    return __byte_perm(w, 0x3f800000u, (k & 1) ? 0x7632u : 0x7610u);
   }
   return 0x3f800000u | (wv[Batch<D>::kZWords + k] >> 9);
 }
@@ -408,8 +411,17 @@ __device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k) {
 // Uniform angle on the circle with ONE FFMA from f = 1 + m/2^b in [1,2)
 // (the float built by angle_bits): theta = 2 pi f - 3 pi in [-pi, pi).  The
 // angles are equally spaced around the circle, so the offset is irrelevant.
+#if EM_ANGLE_BITS == 16
+// f in [1, 1 + 2^-7): theta = (f - 1) * 2^7 * 2 pi - pi
+constexpr float kAngScale = 6.283185307179586f * 128.0f;
+constexpr float kAngBias = -(6.283185307179586f * 128.0f) - 3.14159265358979323846f;
+#else
+// f in [1, 2): theta = 2 pi f - 3 pi
+constexpr float kAngScale = 6.283185307179586f;
+constexpr float kAngBias = -9.42477796076938f;
+#endif
 __device__ __forceinline__ float angle_of(unsigned fbits) {
-  return fmaf(__uint_as_float(fbits), 6.283185307179586f, -9.42477796076938f);
+  return fmaf(__uint_as_float(fbits), kAngScale, kAngBias);
 }
 
 template <int D, bool IDENT>
