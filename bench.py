@@ -303,6 +303,7 @@ def run_ours(args):
             ev[i][1].record(stream)
             launches += plan.last_launches()
         torch.cuda.synchronize()
+    plan.check()  # budget errors of the (asynchronous) runs
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]

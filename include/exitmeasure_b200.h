@@ -164,9 +164,13 @@ int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_
 int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                      const int64_t** block, int64_t* err_pole, int64_t* err_rep);
 /* same, outputs left in device memory (caller-owned, zeroed by the library)
- * and work ordered on `stream` (cudaStream_t, NULL = the plan's stream) */
+ * and work ordered on `stream` (cudaStream_t, NULL = the plan's stream).
+ * Asynchronous: returns once the work is enqueued; after synchronising,
+ * em_plan_check reports a budget overrun of that run (EM_BUDGET) and makes
+ * em_plan_last_stats' kernel time available. */
 int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                        em_outputs* dev_out, void* stream);
+int em_plan_check(em_plan* p, int64_t* err_pole, int64_t* err_rep);
 /* device time (ms) of the walk kernel of the last run, CUDA events on the
  * launching stream; walks and steps of that run */
 int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int64_t* steps);

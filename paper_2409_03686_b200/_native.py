@@ -96,6 +96,7 @@ def lib():
         "em_plan_run_device": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs), _p],
                                ctypes.c_int),
         "em_plan_last_stats": ([_p, _p, _p, _p], ctypes.c_int),
+        "em_plan_check": ([_p, _p, _p], ctypes.c_int),
         "em_plan_last_launches": ([_p, _p], ctypes.c_int),
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),

@@ -379,17 +379,29 @@ class Plan:
                    stream_ptr: int | None = None, rep_start: int = 0) -> None:
         """Outputs stay in device memory: counts (n_poles, n0+n1) int64 and
         stats (3, n_poles) int64 at the given device pointers; work is
-        ordered on ``stream_ptr`` (e.g. torch's current stream)."""
+        ordered on ``stream_ptr`` (e.g. torch's current stream) and this call
+        returns without waiting -- call ``check()`` after synchronising."""
         out = N.EmOutputs(ctypes.c_void_p(counts_ptr), ctypes.c_void_p(stats_ptr),
                           ctypes.c_void_p(stats_ptr + 8 * self.n_poles),
                           ctypes.c_void_p(stats_ptr + 16 * self.n_poles), -1, -1)
-        rc = N.check(N.lib().em_plan_run_device(self._h, int(seed) & (2**64 - 1),
-                                                int(rep_start), int(n_rep), ctypes.byref(out),
-                                                ctypes.c_void_p(stream_ptr or 0)),
-                     "em_plan_run_device")
+        # torch reports the legacy default stream as handle 0, which this ABI
+        # reads as "the plan's own stream": pass cudaStreamLegacy (0x1) instead
+        # so the work is ordered with the caller's events and kernels
+        sp = stream_ptr if stream_ptr else 1
+        N.check(N.lib().em_plan_run_device(self._h, int(seed) & (2**64 - 1), int(rep_start),
+                                           int(n_rep), ctypes.byref(out), ctypes.c_void_p(sp)),
+                "em_plan_run_device")
+        self._last_rep_start = int(rep_start)
+
+    def check(self) -> None:
+        """Raise WalkBudgetError if the last run_device hit the step budget
+        (waits for the plan's stream)."""
+        ep, er = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = N.check(N.lib().em_plan_check(self._h, ctypes.byref(ep), ctypes.byref(er)),
+                     "em_plan_check")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(out.err_pole), int(rep_start + out.err_rep),
-                                  self.max_steps)
+            raise WalkBudgetError(int(ep.value), int(getattr(self, "_last_rep_start", 0)
+                                                     + er.value), self.max_steps)
 
     def exits(self, seed: int, n_rep: int, rep_start: int = 0):
         """Exit points, steps and components of n_rep walks per pole,

@@ -235,7 +235,8 @@ struct em_plan {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
-  int64_t last_walks = 0, last_steps = 0, last_launches = 0;
+  int64_t last_walks = 0, last_steps = 0, last_launches = 0, last_n_rep = 0;
+  cudaStream_t last_stream = nullptr;  // stream of the last run_device
   ~em_plan() { give_back(device, stream, ev0, ev1); }
 };
 
@@ -848,7 +849,21 @@ int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
                        reinterpret_cast<unsigned long long*>(dev_out->counts),
                        reinterpret_cast<unsigned long long*>(dev_out->steps_sum), s);
   if (rc) return rc;
-  return plan_finish(p, s, n_rep, dev_out, nullptr);
+  // asynchronous: nothing waits for the kernel here; em_plan_check reads the
+  // budget-error word (and the kernel time) once the caller has synchronised
+  p->last_n_rep = n_rep;
+  p->last_stream = s;
+  return EM_OK;
+}
+
+int em_plan_check(em_plan* p, int64_t* err_pole, int64_t* err_rep) {
+  if (!p) return fail(EM_ERR_INVALID, "plan null");
+  DeviceGuard dg(p->device);
+  em_outputs o{};
+  int rc = plan_finish(p, p->last_stream ? p->last_stream : p->stream, p->last_n_rep, &o, nullptr);
+  if (err_pole) *err_pole = o.err_pole;
+  if (err_rep) *err_rep = o.err_rep;
+  return rc;
 }
 
 int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int64_t* steps) {

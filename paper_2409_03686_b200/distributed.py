@@ -70,6 +70,8 @@ def run_accumulate_sharded(dom, ksqrt, poles, seed: int, eps: float, max_steps: 
             stats3 = torch.zeros((3, len(ids)), dtype=torch.int64, device=dev)
             plan.run_device(seed, n_rep, counts.data_ptr(), stats3.data_ptr(),
                             torch.cuda.current_stream(dev).cuda_stream)
+            torch.cuda.current_stream(dev).synchronize()
+            plan.check()
             stats = stats3.t().contiguous()
             ms = plan.last_stats()[0]
         else:
