@@ -265,7 +265,7 @@ def run_ours(args):
     s1 = backend.pack_side(cfg.fam1, cfg.d, cfg.eps)
     plan = backend.Plan(geom, cfg.kt.k_sqrt, cfg.poles[ids], cfg.eps, 10**6, s0, s1,
                         precision=args.precision, chain=args.chain, device=device,
-                        pole_ids=ids)
+                        pole_ids=ids, grid=args.grid)
     row = plan.n0 + plan.n1
     m_local = len(ids)
     m_pad = -(-cfg.n_poles // world)
@@ -413,6 +413,7 @@ def main():
     ap.add_argument("--n-rep", type=int, default=None, help="override walks per pole")
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -501,6 +501,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   w.ssum = p->blk_stats;
   w.ssq = w.ssum + n_poles;
   w.smax = w.ssq + n_poles;
+  w.smem_stats = 0;  // decided per launch (plan_launch)
 
   const em_side* sides[2] = {s0, s1};
   if (p->precision == EM_PREC_REF64) {
@@ -718,6 +719,11 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
     w->rb = rb;
     w->n_chunks = (unsigned long long)p->n_poles * (unsigned long long)((n_rep + rb - 1) / rb);
+    // small chunks mean a pole change (a statistics flush) almost every walk:
+    // collect those flushes in a per-block shared table instead of global
+    // atomics on 3 * n_poles addresses; big jobs flush rarely and keep the
+    // register path (no end-of-kernel burst of per-block flushes)
+    w->smem_stats = (p->n_poles <= 128 && rb < 256) ? 1 : 0;
   }
   w->counts = counts;
   w->ssum = stats;

@@ -54,6 +54,7 @@ struct WorkOut {
   unsigned long long* ticket;                  // global chunk counter
   unsigned long long* counts;                  // (n_poles, row_len)
   int row_len, col_off1;                       // side-1 column offset
+  int smem_stats;                              // per-block shared stats table (n_poles <= 1024)
   unsigned long long *ssum, *ssq, *smax;
   // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
   // output block means "no failure" and the smallest key wins

@@ -100,19 +100,67 @@ __device__ __forceinline__ void acc_init(StepAcc& a) {
   a.sum = a.sq = a.mx = 0;
 }
 
+// Per-WARP shared tables of step statistics, (3, n_poles) u64 each, used
+// when the job is small (W.smem_stats: few poles, small chunks): then a chunk
+// holds ~1 walk per lane, lanes change pole on every walk, and global
+// per-pole atomics would serialise on 3 * n_poles addresses.  Warp-private,
+// so only __syncwarp is needed (a block barrier in this kernel costs ~20% by
+// changing its register allocation); each warp flushes its table at exit.
+extern __shared__ unsigned long long s_stats[];
+
+__device__ __forceinline__ unsigned long long* warp_stats(const WorkOut& W) {
+  return s_stats + (threadIdx.x >> 5) * 3 * W.n_poles;
+}
+
+// SMEM: compile-time choice (the FP32 kernel is instantiated both ways so the
+// big-job variant's code generation is untouched); -1 = decide at run time
+// from W.smem_stats (the REF64 mirror)
+template <int SMEM = -1>
 __device__ __forceinline__ void acc_flush(StepAcc& a, const WorkOut& W) {
   if (a.pole >= 0 && a.sum + a.mx > 0) {
-    atomicAdd(&W.ssum[a.pole], a.sum);
-    atomicAdd(&W.ssq[a.pole], a.sq);
-    atomicMax(&W.smax[a.pole], a.mx);
+    if (SMEM == 1 || (SMEM < 0 && W.smem_stats)) {
+      unsigned long long* t = warp_stats(W);
+      atomicAdd(&t[a.pole], a.sum);
+      atomicAdd(&t[W.n_poles + a.pole], a.sq);
+      atomicMax(&t[2 * W.n_poles + a.pole], a.mx);
+    } else {
+      atomicAdd(&W.ssum[a.pole], a.sum);
+      atomicAdd(&W.ssq[a.pole], a.sq);
+      atomicMax(&W.smax[a.pole], a.mx);
+    }
   }
   a.sum = a.sq = a.mx = 0;
 }
 
+template <int SMEM = -1>
+__device__ __forceinline__ void stats_smem_init(const WorkOut& W) {
+  if (SMEM == 0 || (SMEM < 0 && !W.smem_stats)) return;
+  unsigned long long* t = warp_stats(W);
+  for (int i = threadIdx.x & 31; i < 3 * W.n_poles; i += 32) t[i] = 0;
+  __syncwarp();
+}
+
+template <int SMEM = -1>
+__device__ __forceinline__ void stats_smem_flush(const WorkOut& W) {
+  if (SMEM == 0 || (SMEM < 0 && !W.smem_stats)) return;
+  __syncwarp();
+  const unsigned long long* t = warp_stats(W);
+  const int n = (int)W.n_poles;
+  for (int i = threadIdx.x & 31; i < n; i += 32) {
+    const unsigned long long sm = t[i], mx = t[2 * n + i];
+    if (sm | mx) {
+      atomicAdd(&W.ssum[i], sm);
+      atomicAdd(&W.ssq[i], t[n + i]);
+      atomicMax(&W.smax[i], mx);
+    }
+  }
+}
+
+template <int SMEM = -1>
 __device__ __forceinline__ void acc_add(StepAcc& a, const WorkOut& W, int pole,
                                         unsigned long long steps) {
   if (pole != a.pole) {
-    acc_flush(a, W);
+    acc_flush<SMEM>(a, W);
     a.pole = pole;
   }
   a.sum += steps;

@@ -464,7 +464,7 @@ constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
 
 // Bin one exit (owner component -> side -> nearest anchor), count it, and
 // add its step count to this lane's per-pole accumulator.
-template <int D, int OUTER, int NH, int BINK>
+template <int D, int OUTER, int NH, int BINK, int SMEM>
 __device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
                                        StepAcc& acc) {
   const WorkOut& W = P.w;
@@ -475,7 +475,7 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
   const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
-  acc_add(acc, W, pole, (unsigned long long)steps);
+  acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
 
 // MODE 0: bin exits into the count rows + per-pole step statistics
@@ -483,7 +483,7 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 #ifndef EM_MIN_BLOCKS
 #define EM_MIN_BLOCKS 4
 #endif
-template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK>
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
 __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
   __shared__ float4 q_x[kWarps][kQueue];  // exit point, pole (as int bits in .w)
@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
   pool_init(wp);
   StepAcc acc;
   acc_init(acc);
+  if (MODE == 0) stats_smem_init<SMEM>(W);
   const float keep = 1.0f - P.shrink_rel;
   constexpr int K = Batch<D>::kSteps;
   for (;;) {
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
             const int slot = qn - 32 + lane;
             const float4 e = qx[slot];
             const float ex[3] = {e.x, e.y, e.z};
-            retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), qs[slot], acc);
+            retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), qs[slot], acc);
             qn -= 32;
             __syncwarp();
           }
@@ -614,9 +615,10 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
     if (lane < qn) {  // drain the queue
       const float4 e = q_x[warp][lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK>(P, ex, __float_as_int(e.w), q_s[warp][lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), q_s[warp][lane], acc);
     }
-    acc_flush(acc, W);
+    acc_flush<SMEM>(acc, W);
+    stats_smem_flush<SMEM>(W);
   }
 }
 
@@ -628,64 +630,72 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
 // them; everything else takes BIN_ANY.
 using F32Kernel = void (*)(F32Params);
 
-template <int D, int OUTER, int NH, int BINK>
-static F32Kernel pick_chain(int mode, int chain, bool ident) {
+template <int D, int OUTER, int NH, int BINK, int SM>
+static F32Kernel pick_chain_sm(int mode, int chain, bool ident) {
   using namespace f32;
   if (mode != 0) {
-    if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 1, BIN_ANY>;
-    if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 1, BIN_ANY>;
-    return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 1, BIN_ANY>;
+    if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 1, BIN_ANY, 0>;
+    if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 1, BIN_ANY, 0>;
+    return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 1, BIN_ANY, 0>;
   }
-  if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 0, BINK>;
-  if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 0, BINK>;
-  return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 0, BINK>;
+  if (ident) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, true, 0, BINK, SM>;
+  if (chain == EM_CHAIN_MAX) return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_MAX, false, 0, BINK, SM>;
+  return walk_f32_kernel<D, OUTER, NH, EM_CHAIN_WOE, false, 0, BINK, SM>;
+}
+
+template <int D, int OUTER, int NH, int BINK>
+static F32Kernel pick_chain(int mode, int chain, bool ident, int smem) {
+  return smem ? pick_chain_sm<D, OUTER, NH, BINK, 1>(mode, chain, ident)
+              : pick_chain_sm<D, OUTER, NH, BINK, 0>(mode, chain, ident);
 }
 
 template <int D, int OUTER, int NH, int B1, int B2>
-static F32Kernel pick_bin(int mode, int chain, bool ident, int bink) {
-  if (mode == 0 && bink == B1 && B1 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B1>(mode, chain, ident);
-  if (mode == 0 && bink == B2 && B2 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B2>(mode, chain, ident);
-  return pick_chain<D, OUTER, NH, f32::BIN_ANY>(mode, chain, ident);
+static F32Kernel pick_bin(int mode, int chain, bool ident, int bink, int smem) {
+  if (mode == 0 && bink == B1 && B1 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B1>(mode, chain, ident, smem);
+  if (mode == 0 && bink == B2 && B2 != f32::BIN_ANY) return pick_chain<D, OUTER, NH, B2>(mode, chain, ident, smem);
+  return pick_chain<D, OUTER, NH, f32::BIN_ANY>(mode, chain, ident, smem);
 }
 
-static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bool ident, int bink) {
+static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bool ident, int bink,
+                          int smem) {
   using namespace f32;
   if (d == 2) {
     if (outer == OUTER_BALL) {
-      if (nh_mode == 0) return pick_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
-      if (nh_mode == 1) return pick_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
-      return pick_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink);
+      if (nh_mode == 0) return pick_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
+      if (nh_mode == 1) return pick_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
+      return pick_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
     }
     if (outer == OUTER_BOX) {
-      if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink);
-      return pick_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
+      if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink, smem);
+      return pick_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink, smem);
     }
     return nullptr;
   }
   if (outer == OUTER_BALL) {
-    if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
-    return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
+    if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
+    return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
   }
   if (outer == OUTER_BOX) {
-    if (nh_mode == 0) return pick_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
-    return pick_bin<3, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
+    if (nh_mode == 0) return pick_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
+    return pick_bin<3, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink, smem);
   }
-  if (nh_mode == 0) return pick_bin<3, OUTER_LBOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink);
-  return pick_bin<3, OUTER_LBOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink);
+  if (nh_mode == 0) return pick_bin<3, OUTER_LBOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
+  return pick_bin<3, OUTER_LBOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink, smem);
 }
 
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
                        bool ident, int bink, int grid, int block, cudaStream_t s) {
   if (block != 32 * f32::kWarps) return cudaErrorInvalidConfiguration;
-  F32Kernel k = pick_f32(d, outer, nh_mode, mode, chain, ident, bink);
+  F32Kernel k = pick_f32(d, outer, nh_mode, mode, chain, ident, bink, P.w.smem_stats);
   if (!k) return cudaErrorInvalidValue;
-  k<<<grid, block, 0, s>>>(P);
+  const size_t smem = (mode == 0 && P.w.smem_stats) ? (size_t)f32::kWarps * 3 * P.w.n_poles * 8 : 0;
+  k<<<grid, block, smem, s>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink,
                               int* nb) {
-  F32Kernel k = pick_f32(d, outer, nh_mode, 0, chain, ident, bink);
+  F32Kernel k = pick_f32(d, outer, nh_mode, 0, chain, ident, bink, 0);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
 }

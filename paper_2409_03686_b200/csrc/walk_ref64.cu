@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   pool_init(wp);
   StepAcc acc;
   acc_init(acc);
+  if (MODE == 0) stats_smem_init(W);
   for (;;) {
     const unsigned need = __ballot_sync(kFull, !active);
     if (need) {
@@ -311,7 +312,10 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     }
     steps = steps + 1;
   }
-  if (MODE == 0) acc_flush(acc, W);
+  if (MODE == 0) {
+    acc_flush(acc, W);
+    stats_smem_flush(W);
+  }
 }
 
 }  // namespace r64
@@ -489,10 +493,12 @@ cudaError_t launch_bin_points_ref64(const Ref64Params& P, const double* pts, lon
 }
 
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s) {
-  if (mode == 0)
-    r64::walk_ref64_kernel<0><<<grid, block, 0, s>>>(P);
-  else
+  if (mode == 0) {
+    const size_t smem = P.w.smem_stats ? (size_t)(block / 32) * 3 * P.w.n_poles * 8 : 0;
+    r64::walk_ref64_kernel<0><<<grid, block, smem, s>>>(P);
+  } else {
     r64::walk_ref64_kernel<1><<<grid, block, 0, s>>>(P);
+  }
   return cudaGetLastError();
 }
 
