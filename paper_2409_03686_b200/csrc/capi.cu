@@ -221,7 +221,13 @@ struct em_plan {
   int grid = 0, block = 256;
   Ref64Params p64{};
   F32Params p32{};
-  DevBuf poles, pole_ids, anchors[2], gcell[2], gcand[2];
+  // every plan input (poles, pole ids, anchors, candidate grids, IDW radii)
+  // lives in one device arena filled by ONE asynchronous H2D from pinned
+  // staging on the plan's stream (ev_up marks its completion)
+  DevBuf arena;
+  PinBuf upin;
+  cudaEvent_t ev_up = nullptr;
+  const double* radii_dev[2] = {nullptr, nullptr};
   // one output block: counts (n_poles x row) | stats (3 x n_poles) | misc (err, ticket)
   DevBuf counts, stats, misc;
   PinBuf pin;  // host staging of the output block
@@ -229,7 +235,6 @@ struct em_plan {
   unsigned long long *blk_counts = nullptr, *blk_stats = nullptr, *blk_misc = nullptr;
   size_t blk_words = 0;
   DevBuf xo, so, co;           // exits
-  DevBuf radii[2];             // IDW supports (REF64)
   DevBuf ikind, iidx, itot, iside, iraw0, iraw1, iinit0, iinit1;
   int wkind[2] = {0, 0}, idw_power[2] = {2, 2};
   cudaStream_t stream = nullptr;
@@ -237,7 +242,13 @@ struct em_plan {
   double last_ms = 0.0;
   int64_t last_walks = 0, last_steps = 0, last_launches = 0, last_n_rep = 0;
   cudaStream_t last_stream = nullptr;  // stream of the last run_device
-  ~em_plan() { give_back(device, stream, ev0, ev1); }
+  ~em_plan() {
+    // buffers go back to the shared cache: nothing in flight may still use them
+    if (stream) cudaStreamSynchronize(stream);
+    if (last_launches && ev1) cudaEventSynchronize(ev1);
+    give_back(device, stream, ev0, ev1);
+    give_back(device, nullptr, ev_up, nullptr);
+  }
 };
 
 namespace {
@@ -463,7 +474,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->stream = take_stream(o.device);
   p->ev0 = take_event(o.device);
   p->ev1 = take_event(o.device);
-  if (!p->stream || !p->ev0 || !p->ev1)
+  p->ev_up = take_event(o.device);
+  if (!p->stream || !p->ev0 || !p->ev1 || !p->ev_up)
     return bail(fail(EM_ERR_CUDA, std::string("stream/event: ") + cudaGetErrorString(cudaGetLastError())));
 
   bool ident = true;
@@ -473,6 +485,15 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->ident = ident;
 
   const int64_t row = p->n0 + p->n1;
+  // input staging: (offset, pointer slot) fixed up once the arena exists
+  std::vector<char> stage;
+  std::vector<std::pair<size_t, void**>> fixups;
+  auto put = [&](const void* src, size_t bytes, void** slot) {
+    const size_t off = (stage.size() + 255) & ~(size_t)255;
+    stage.resize(off + bytes);
+    if (bytes) std::memcpy(stage.data() + off, src, bytes);
+    fixups.push_back({off, slot});
+  };
   // outputs
   cudaError_t ce;
 #define EM_ALLOC(buf, bytes)                                                          \
@@ -483,16 +504,11 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->blk_counts = p->counts.as<unsigned long long>();
   p->blk_stats = p->blk_counts + (size_t)n_poles * row;
   p->blk_misc = p->blk_stats + 3 * (size_t)n_poles;
-  if (pole_ids) {
-    EM_ALLOC(p->pole_ids, (size_t)n_poles * 8);
-    if (cudaMemcpy(p->pole_ids.p, pole_ids, n_poles * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(EM_ERR_CUDA, "upload pole ids"));
-  }
 
   WorkOut w{};
   w.n_poles = n_poles;
   w.inv_poles = 1.0 / (double)n_poles;
-  w.pole_ids = pole_ids ? p->pole_ids.as<long long>() : nullptr;
+  w.pole_ids = nullptr;  // set from the arena below
   w.ticket = p->blk_misc + 1;
   w.err_key = p->blk_misc;
   w.counts = p->blk_counts;
@@ -516,10 +532,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     for (int i = 0; i < d * d; ++i) P.ks[i] = g->ksqrt[i];
     P.eps = eps;
     P.max_steps = max_steps;
-    EM_ALLOC(p->poles, (size_t)n_poles * d * 8);
-    if (cudaMemcpy(p->poles.p, poles, n_poles * d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(EM_ERR_CUDA, "upload poles"));
-    P.poles = p->poles.as<double>();
+    put(poles, (size_t)n_poles * d * 8, (void**)&P.poles);
     for (int s = 0; s < 2; ++s) {
       const em_side* S = sides[s];
       Side64& D = P.side[s];
@@ -537,17 +550,9 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       }
       p->wkind[s] = S->wkind;
       p->idw_power[s] = S->idw_power;
-      if (S->n_anchors > 0 && S->wkind == 1) {
-        EM_ALLOC(p->radii[s], (size_t)S->n_anchors * 8);
-        if (cudaMemcpy(p->radii[s].p, S->idw_radii, S->n_anchors * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-          return bail(fail(EM_ERR_CUDA, "upload idw radii"));
-      }
-      if (S->n_anchors > 0) {
-        EM_ALLOC(p->anchors[s], (size_t)S->n_anchors * d * 8);
-        if (cudaMemcpy(p->anchors[s].p, S->anchors, S->n_anchors * d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-          return bail(fail(EM_ERR_CUDA, "upload anchors"));
-        D.anchors = p->anchors[s].as<double>();
-      }
+      if (S->n_anchors > 0 && S->wkind == 1)
+        put(S->idw_radii, (size_t)S->n_anchors * 8, (void**)&p->radii_dev[s]);
+      if (S->n_anchors > 0) put(S->anchors, (size_t)S->n_anchors * d * 8, (void**)&D.anchors);
     }
     P.w = w;
   } else {
@@ -606,14 +611,15 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     }
     P.shrink_rel = 4.0e-6f;
     P.shrink_abs = (float)(scale * 1.1920928955078125e-07);
+    P.keep = 1.0f - P.shrink_rel;
+    for (int i = 0; i < 3; ++i)  // rounded down: the folded margin is never smaller
+      P.gk[i] = std::nextafter((float)((double)P.g[i] * (double)P.keep), 0.0f);
+    P.one_bits = 0x3f800000u;
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);
     std::vector<float> pf(n_poles * 4, 0.0f);
     for (int64_t i = 0; i < n_poles; ++i)
       for (int j = 0; j < d; ++j) pf[i * 4 + j] = (float)(poles[i * d + j] - frame[j]);
-    EM_ALLOC(p->poles, (size_t)n_poles * 16);
-    if (cudaMemcpy(p->poles.p, pf.data(), n_poles * 16, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(EM_ERR_CUDA, "upload poles"));
-    P.poles = p->poles.as<float4>();
+    put(pf.data(), (size_t)n_poles * 16, (void**)&P.poles);
     for (int s = 0; s < 2; ++s) {
       const em_side* S = sides[s];
       Side32& D = P.side[s];
@@ -638,27 +644,19 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       std::vector<float> af(S->n_anchors * 4, 0.0f);
       for (int64_t i = 0; i < S->n_anchors; ++i)
         for (int j = 0; j < d; ++j) af[i * 4 + j] = (float)S->anchors[i * d + j];
-      EM_ALLOC(p->anchors[s], (size_t)S->n_anchors * 16);
-      if (cudaMemcpy(p->anchors[s].p, af.data(), S->n_anchors * 16, cudaMemcpyHostToDevice) != cudaSuccess)
-        return bail(fail(EM_ERR_CUDA, "upload anchors"));
-      D.anchors = p->anchors[s].as<float4>();
+      put(af.data(), (size_t)S->n_anchors * 16, (void**)&D.anchors);
       // one generic block covering the family: accelerate with the grid
       if (D.n_blk == 1 && D.kind[0] == BLK_GENERIC && S->n_anchors > 8) {
         GridHost G;
         if (cached_grid(S->anchors, S->n_anchors, d, eps, G)) {
-          EM_ALLOC(p->gcell[s], G.cell.size() * 4);
-          EM_ALLOC(p->gcand[s], G.cand.size() * 4);
-          if (cudaMemcpy(p->gcell[s].p, G.cell.data(), G.cell.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-              cudaMemcpy(p->gcand[s].p, G.cand.data(), G.cand.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-            return bail(fail(EM_ERR_CUDA, "upload grid"));
+          put(G.cell.data(), G.cell.size() * 4, (void**)&D.grid.cell);
+          put(G.cand.data(), G.cand.size() * 4, (void**)&D.grid.cand);
           D.has_grid = 1;
           for (int j = 0; j < 3; ++j) {
             D.grid.lo[j] = (float)G.lo[j];
             D.grid.n[j] = G.n[j];
           }
           D.grid.inv_h = (float)(1.0 / G.h);
-          D.grid.cell = p->gcell[s].as<unsigned>();
-          D.grid.cand = p->gcand[s].as<unsigned>();
         }
       }
     }
@@ -687,6 +685,22 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       p->bink = (uniform && k > 0) ? k : 0;
     }
   }
+  // pole ids last: the WorkOut copy inside the params is the live one
+  if (pole_ids)
+    put(pole_ids, (size_t)n_poles * 8,
+        p->precision == EM_PREC_REF64 ? (void**)&p->p64.w.pole_ids : (void**)&p->p32.w.pole_ids);
+  if (!stage.empty()) {
+    EM_ALLOC(p->arena, stage.size());
+    if ((ce = p->upin.alloc(stage.size())) != cudaSuccess)
+      return bail(fail(EM_ERR_NOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce)));
+    std::memcpy(p->upin.p, stage.data(), stage.size());
+    if ((ce = cudaMemcpyAsync(p->arena.p, p->upin.p, stage.size(), cudaMemcpyHostToDevice, p->stream)) !=
+        cudaSuccess)
+      return bail(fail(EM_ERR_CUDA, std::string("upload plan inputs: ") + cudaGetErrorString(ce)));
+    for (auto& f : fixups) *f.second = static_cast<char*>(p->arena.p) + f.first;
+  }
+  if ((ce = cudaEventRecord(p->ev_up, p->stream)) != cudaSuccess)
+    return bail(fail(EM_ERR_CUDA, std::string("upload event: ") + cudaGetErrorString(ce)));
 #undef EM_ALLOC
   // persistent grid: SMs x resident blocks
   int per_sm = 4;
@@ -747,6 +761,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     if (blocks_needed < grid) grid = (int)std::max<int64_t>(1, blocks_needed);
     EM_CUDA(cudaEventRecord(p->ev0, s));
     cudaError_t e;
+    if (s != p->stream) EM_CUDA(cudaStreamWaitEvent(s, p->ev_up, 0));
     if (p->precision == EM_PREC_REF64) {
       p->p64.seed = seed;
       e = launch_ref64(p->p64, mode, grid, p->block, s);
@@ -980,8 +995,8 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
   const Side64& S1 = p->p64.side[1];
   cudaError_t e = launch_idw(p->p64, p->xo.as<double>(), p->co.as<long long>(), p->n_poles, n_rep,
                              chunk > 0 ? chunk : std::max<int64_t>(n_rep, 1),
-                             S0.anchors, p->radii[0].as<double>(), (int)p->n0, p->idw_power[0], p->wkind[0],
-                             S1.anchors, p->radii[1].as<double>(), (int)p->n1, p->idw_power[1], p->wkind[1],
+                             S0.anchors, p->radii_dev[0], (int)p->n0, p->idw_power[0], p->wkind[0],
+                             S1.anchors, p->radii_dev[1], (int)p->n1, p->idw_power[1], p->wkind[1],
                              p->ikind.as<int>(), p->iidx.as<long long>(), p->itot.as<double>(),
                              p->iside.as<int>(), p->iraw0.as<double>(), p->iraw1.as<double>(),
                              d_init0, d_init1, p->stream);

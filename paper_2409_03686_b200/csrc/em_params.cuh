@@ -91,10 +91,13 @@ struct F32Params {
   signed char comp_side[kMaxComp];
   float A[9];       // K^{1/2}, row-major
   float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid
+  float gk[3];      // g * keep (rounded down): face gain with the relative margin folded in
   float m2;         // sigma_min(A)^2 (hole bound)
   float eps;
   float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
   float shrink_rel, shrink_abs;  // step safety margins
+  float keep;                    // 1 - shrink_rel
+  unsigned one_bits;             // 0x3f800000 (1.0f), opaque to the compiler: PRMT operand
   int max_steps;
   unsigned key0, key1;
   PhiloxKey32 rk;   // round keys of (key0, key1), set per run on the host

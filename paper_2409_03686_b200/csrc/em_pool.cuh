@@ -37,12 +37,13 @@ __device__ __forceinline__ void pool_init(WarpPool& wp) {
 
 // Called by all 32 lanes (converged).  Lanes set in need_mask receive
 // (pole, replicate offset) and return true, or return false (no work now).
+// lane / lt (lanes below this one) may be passed in when the caller keeps
+// them in registers.
 template <class RepT>
 __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, const WorkOut& W,
-                                          int& pole, RepT& rep_off) {
-  const int lane = threadIdx.x & 31;
+                                          int& pole, RepT& rep_off, int lane, unsigned lt) {
   const int n_need = __popc(need_mask);
-  const int rank = __popc(need_mask & ((1u << lane) - 1u));
+  const int rank = __popc(need_mask & lt);
   const bool me = (need_mask >> lane) & 1u;
   const int avail = wp.end - wp.next;
   bool got = false;
@@ -87,6 +88,13 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
   wp.next = rem < valid ? rem : valid;
   wp.end = valid;
   return got;
+}
+
+template <class RepT>
+__device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, const WorkOut& W,
+                                          int& pole, RepT& rep_off) {
+  const int lane = threadIdx.x & 31;
+  return pool_take(wp, need_mask, W, pole, rep_off, lane, (1u << lane) - 1u);
 }
 
 // Per-lane step statistics of the pole the lane is currently walking.

@@ -40,10 +40,12 @@ __device__ __forceinline__ int n_holes(const F32Params& P) {
   return NH >= 0 ? NH : P.n_holes;
 }
 
-// Euclidean signed distance e and step scale r at x.
+// Euclidean signed distance e and the unshrunk step scale r at x (shrunk
+// already when FOLD, see dist below).
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
-__device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
+__device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, float& e, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
+  constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
   if (OUTER == OUTER_BALL && NH == 1 && MAXC && P.concentric) {
     // annulus / spherical shell: one |v| and one |Av| serve both bounds, and
     //   r = min(q_o / D_o, max(q_h / D_h, e_h)) = min(q_o / D_o, n_h / D_h)
@@ -116,7 +118,8 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
       // to the nearer face is one FADD with a free |.| operand
       const float m = P.bhi[i] - fabsf(x[i]);
       e = fminf(e, m);
-      if (MAXC) r = fminf(r, m * P.g[i]);
+      if (FOLD) r = fminf(r, fmaf(m, P.gk[i], -P.shrink_abs));
+      else if (MAXC) r = fminf(r, m * P.g[i]);
     }
     if (!MAXC) r = e;
     if (OUTER == OUTER_LBOX) {
@@ -126,7 +129,10 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
       const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
       const float en = sqrtf(fmaf(ax, ax, ay * ay));
       e = fminf(e, en);
-      if (MAXC)
+      if (FOLD)  // every term through the same monotone t -> t keep - abs
+        r = fminf(r, fmaxf(fmaf(en, P.keep, -P.shrink_abs),
+                           fmaxf(fmaf(qx, P.gk[0], -P.shrink_abs), fmaf(qy, P.gk[1], -P.shrink_abs))));
+      else if (MAXC)
         r = fminf(r, fmaxf(en, fmaxf(qx * P.g[0], qy * P.g[1])));
       else
         r = e;
@@ -164,6 +170,18 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
       r = e;
     }
   }
+}
+
+// Euclidean signed distance e and step scale r at x, r already shrunk by the
+// FP32 safety margin: r = r_exact * keep - shrink_abs.  Box faces fold the
+// margin into their gain (one FFMA per face instead of an FMUL per face plus
+// a final FFMA); every other shape applies it once at the end.
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+__device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
+  constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
+  constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
+  dist_raw<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+  if (!FOLD) r = fmaf(r, P.keep, -P.shrink_abs);
 }
 
 // Owner component: argmin of |component distance|, ties to the lowest id
@@ -395,13 +413,16 @@ struct Batch {
 // permute (PRMT) drops a half-word into the low mantissa bytes of 1.0f, so
 // f = 1 + k16 / 2^23, and the FFMA maps the 2^16 values onto equally spaced
 // angles spanning exactly 2 pi (the offset is irrelevant on the circle).
+// (one_bits = 0x3f800000 comes from the params so the compiler keeps it as
+// the register/constant operand and the selector as the immediate: with a
+// literal it materialises the selector in a register on every step)
 template <int D>
-__device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k) {
+__device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k, unsigned one_bits) {
   if (EM_ANGLE_BITS == 16) {
     const unsigned w = wv[Batch<D>::kZWords + (k >> 1)];
-    return __byte_perm(w, 0x3f800000u, (k & 1) ? 0x7632u : 0x7610u);
+    return __byte_perm(w, one_bits, (k & 1) ? 0x7632u : 0x7610u);
   }
-  return 0x3f800000u | (wv[Batch<D>::kZWords + k] >> 9);
+  return one_bits | (wv[Batch<D>::kZWords + k] >> 9);
 }
 
 // One walk-on-ellipsoids step from x (r from dist()): direction from the RNG
@@ -483,51 +504,73 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 #ifndef EM_MIN_BLOCKS
 #define EM_MIN_BLOCKS 4
 #endif
+// Per-warp exit queue in shared memory: exit point + pole (as int bits in
+// .w) and step count, binned 32 at a time.
+struct ExitQueue {
+  float4 x[kQueue];
+  int s[kQueue];
+};
+
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
 __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
-  __shared__ float4 q_x[kWarps][kQueue];  // exit point, pole (as int bits in .w)
-  __shared__ int q_s[kWarps][kQueue];     // steps
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  float4* const qx = q_x[warp];
-  int* const qs = q_s[warp];
+  __shared__ ExitQueue q_all[kWarps];
+  // lane id, lane mask and the queue's shared-window address are made opaque
+  // (empty asm) so the compiler keeps them in registers instead of
+  // re-deriving them from special registers on every service pass
+  int lane = threadIdx.x & 31;
+  unsigned lt = (1u << lane) - 1u;
+  unsigned qb = (unsigned)__cvta_generic_to_shared(&q_all[threadIdx.x >> 5]);
+  asm volatile("" : "+r"(lane), "+r"(lt), "+r"(qb));
   int qn = 0;  // queued exits of this warp (warp-uniform)
-  float x[3] = {0.0f, 0.0f, 0.0f};
+  // idle lanes sit far outside the domain: their distance is negative, so the
+  // fast path's stop mask keeps them still without a separate lane flag
+  constexpr float kFar = 1.0e4f;
+  float x[3] = {kFar, kFar, kFar};
   float px = 0.0f, py = 0.0f, pz = 0.0f;  // this lane's cached pole (start point)
   int cpole = -1;
   unsigned cpid = 0;
+  // steps doubles as the RNG draw counter: a walking lane has taken exactly
+  // K steps per batch, so its batch index is steps / K
   int steps = 0, pole = 0, rep_off = 0;
-  unsigned draw = 0, rep_lo = 0, rep_hi = 0;
-  // lane flags as ints (bools become byte-packed PRMT traffic in SASS)
-  int walking = 0, inflight = 0, failed = 0;
+  unsigned rep_lo = 0, rep_hi = 0;
+  int walking = 0;     // lane flag as an int (bools become PRMT traffic in SASS)
+  unsigned live = 0;   // warp mask of lanes holding a walk not yet retired
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
   acc_init(acc);
   if (MODE == 0) stats_smem_init<SMEM>(W);
-  const float keep = 1.0f - P.shrink_rel;
   constexpr int K = Batch<D>::kSteps;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
     if (need) {
-      const int done = inflight & (walking ^ 1) & (failed ^ 1);
+      const unsigned dm = need & live;  // walks that stopped in the last batch
+      const int done = (dm >> lane) & 1u;
       if (MODE == 0) {
-        const unsigned dm = __ballot_sync(kFull, done);
         if (dm) {
           if (done) {
-            const int slot = qn + __popc(dm & lt);
-            qx[slot] = make_float4(x[0], x[1], x[2], __int_as_float(pole));
-            qs[slot] = steps;
+            const unsigned slot = qn + __popc(dm & lt);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(qb + slot * 16u),
+                         "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(__int_as_float(pole))
+                         : "memory");
+            asm volatile("st.shared.s32 [%0], %1;" ::"r"(qb + kQueue * 16u + slot * 4u), "r"(steps)
+                         : "memory");
           }
           qn += __popc(dm);
           if (qn >= 32) {  // bin 32 queued exits with every lane active
             __syncwarp();
-            const int slot = qn - 32 + lane;
-            const float4 e = qx[slot];
-            const float ex[3] = {e.x, e.y, e.z};
-            retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), qs[slot], acc);
+            const unsigned slot = qn - 32 + lane;
+            float ex[3], pw;
+            int es;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(ex[0]), "=f"(ex[1]), "=f"(ex[2]), "=f"(pw)
+                         : "r"(qb + slot * 16u)
+                         : "memory");
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qb + kQueue * 16u + slot * 4u)
+                         : "memory");
+            retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(pw), es, acc);
             qn -= 32;
             __syncwarp();
           }
@@ -538,13 +581,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
-      if (failed)
-        atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
-      if (!walking) {
-        failed = 0;
-        inflight = 0;
-      }
-      if (pool_take(wp, need, W, pole, rep_off)) {
+      if (pool_take(wp, need, W, pole, rep_off, lane, lt)) {
         if (pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
           px = p.x;
@@ -556,18 +593,18 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         x[0] = px;
         x[1] = py;
         x[2] = pz;
-        const unsigned long long rep = (unsigned long long)(W.rep_start + rep_off);
+        const unsigned long long rep = (unsigned long long)W.rep_start + (unsigned)rep_off;
         rep_lo = (unsigned)rep;
         rep_hi = (unsigned)(rep >> 32);
         steps = 0;
-        draw = 0;
         walking = 1;
-        inflight = 1;
       }
-      if (wp.exhausted && __ballot_sync(kFull, walking) == 0) break;
+      live = __ballot_sync(kFull, walking);
+      if (wp.exhausted && live == 0) break;
     }
     // ---- a batch of K steps on one or two Philox blocks, branch-free ----
     unsigned wv[4 * Batch<D>::kBlocks];
+    const unsigned draw = (unsigned)steps / (unsigned)K;
 #pragma unroll
     for (int b = 0; b < Batch<D>::kBlocks; ++b) {
       const uint4 w = philox4x32_10(P.rk, draw * Batch<D>::kBlocks + b, rep_lo, cpid, rep_hi);
@@ -576,26 +613,28 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
       wv[4 * b + 2] = w.z;
       wv[4 * b + 3] = w.w;
     }
-    ++draw;
     if (__all_sync(kFull, steps + K <= P.max_steps)) {
       // fast path: no lane can reach the step budget inside this batch.
       // Bookkeeping on the FMA pipes (the ALU pipe is the busy one): the
-      // live mask is a float, cleared by FFMA.SAT((e - eps) * 2^k) -- exactly
-      // 0 when e <= eps and exactly 1 otherwise, since every representable
-      // positive difference scales to >= 1 -- and multiplies the step scale.
-      float wm = walking ? 1.0f : 0.0f, sf = 0.0f;
+      // live mask is a float, FFMA.SAT((e - eps) * 2^k) -- exactly 0 when
+      // e <= eps and exactly 1 otherwise, since every representable positive
+      // difference scales to >= 1 -- and multiplies the step scale.  No
+      // running product is needed: a stopped lane does not move, so every
+      // later step of the batch recomputes the same e <= eps (and idle lanes
+      // are parked outside the domain, e < 0).
+      float wm = 0.0f, sf = 0.0f;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         float e, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        wm *= __saturatef(fmaf(e, P.stop_scale, P.stop_bias));
-        const float rs = fmaf(r, keep, -P.shrink_abs) * wm;
-        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k));
+        wm = __saturatef(fmaf(e, P.stop_scale, P.stop_bias));
+        step<D, IDENT>(P, x, r * wm, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k, P.one_bits));
         sf += wm;
       }
       walking = wm != 0.0f;
       steps += (int)sf;
     } else {
+      int failed = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         float e, r;
@@ -604,18 +643,29 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
-        const float rs = walking ? fmaf(r, keep, -P.shrink_abs) : 0.0f;
-        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k));
+        const float rs = walking ? r : 0.0f;
+        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k, P.one_bits));
         steps += walking;
+      }
+      // budget overruns: report (smallest key wins), drop from the live set
+      // (never binned) and park the lane
+      const unsigned fm = __ballot_sync(kFull, failed);
+      if (fm) {
+        if (failed) {
+          atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
+          x[0] = x[1] = x[2] = kFar;
+        }
+        live &= ~fm;
       }
     }
   }
   if (MODE == 0) {
     __syncwarp();
     if (lane < qn) {  // drain the queue
-      const float4 e = q_x[warp][lane];
+      const ExitQueue& q = q_all[threadIdx.x >> 5];
+      const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), q_s[warp][lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
     acc_flush<SMEM>(acc, W);
     stats_smem_flush<SMEM>(W);

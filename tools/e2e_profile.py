@@ -1,15 +1,36 @@
-"""Where does the one-shot API call spend its time? (GPU box)"""
+"""Where does the one-shot API call spend its time? (GPU box)
+python tools/e2e_profile.py [cfg]"""
 import sys
 import time
 from pathlib import Path
 
-import numpy as np
-
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from paper_2409_03686_b200 import backend as B, configs  # noqa: E402
+from paper_2409_03686_b200 import _native as N, backend as B, configs  # noqa: E402
 
 cfg = configs.get(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
-for it in range(4):
+lib = N.lib()
+tim = {}
+
+
+def wrap(name):
+    f = getattr(lib, name)
+
+    class W:
+        def __call__(self, *a):
+            t = time.perf_counter()
+            r = f(*a)
+            tim[name] = tim.get(name, 0.0) + time.perf_counter() - t
+            return r
+
+        def __getattr__(self, k):
+            return getattr(f, k)
+    setattr(lib, name, W())
+
+
+for n in ("em_plan_create", "em_plan_run_host", "em_plan_destroy", "em_plan_last_stats"):
+    wrap(n)
+for it in range(6):
+    tim.clear()
     t0 = time.perf_counter()
     geom = B.pack_geometry(cfg.dom)
     s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
@@ -21,5 +42,14 @@ for it in range(4):
     t3 = time.perf_counter()
     plan.close()
     t4 = time.perf_counter()
-    print(f"iter {it}: pack {1e3*(t1-t0):.2f} ms, plan {1e3*(t2-t1):.2f} ms, run {1e3*(t3-t2):.2f} ms "
-          f"(kernel {r.kernel_ms:.2f} ms), close {1e3*(t4-t3):.2f} ms, total {1e3*(t4-t0):.2f} ms")
+    c = {k: 1e3 * v for k, v in tim.items()}
+    print(f"iter {it}: pack {1e3*(t1-t0):.3f} ms, plan {1e3*(t2-t1):.3f} ms "
+          f"(C {c.get('em_plan_create', 0):.3f}), run {1e3*(t3-t2):.3f} ms "
+          f"(C {c.get('em_plan_run_host', 0):.3f}, kernel {r.kernel_ms:.3f}), "
+          f"close {1e3*(t4-t3):.3f} ms, total {1e3*(t4-t0):.3f} ms")
+t0 = time.perf_counter()
+for _ in range(5):
+    r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, cfg.n_rep,
+                         B.pack_side(cfg.fam0, cfg.d, cfg.eps), B.pack_side(cfg.fam1, cfg.d, cfg.eps),
+                         precision="fp32")
+print(f"run_accumulate: {1e3*(time.perf_counter()-t0)/5:.3f} ms per call (kernel {r.kernel_ms:.3f})")
