@@ -163,6 +163,12 @@ int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_
  * host copy for callers that convert the rows anyway. */
 int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                      const int64_t** block, int64_t* err_pole, int64_t* err_rep);
+/* hand the page-locked block of the last em_plan_run_host to the caller
+ * (zero-copy results): *block stays valid until em_host_block_free(*block);
+ * the plan stages its next run in another block.  (Host-side adapters only:
+ * the reference's AccumulateResult owns its arrays, S/backend.py:193-199.) */
+int em_plan_detach_block(em_plan* p, int64_t** block);
+int em_host_block_free(void* block);
 /* same, outputs left in device memory (caller-owned, zeroed by the library)
  * and work ordered on `stream` (cudaStream_t, NULL = the plan's stream).
  * Asynchronous: returns once the work is enqueued; after synchronising,

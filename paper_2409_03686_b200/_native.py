@@ -93,6 +93,8 @@ def lib():
         "em_plan_run": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs)], ctypes.c_int),
         "em_plan_run_host": ([_p, _u64, _i64, _i64, ctypes.POINTER(ctypes.POINTER(_i64)), _p, _p],
                              ctypes.c_int),
+        "em_plan_detach_block": ([_p, ctypes.POINTER(ctypes.POINTER(_i64))], ctypes.c_int),
+        "em_host_block_free": ([_p], ctypes.c_int),
         "em_plan_run_device": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs), _p],
                                ctypes.c_int),
         "em_plan_last_stats": ([_p, _p, _p, _p], ctypes.c_int),
@@ -165,7 +167,9 @@ def device_info(device: int = 0) -> dict:
 
 
 def ptr(a: np.ndarray):
-    return a.ctypes.data_as(_p)
+    # the raw address as a Python int (c_void_p arguments and struct fields
+    # accept it); a.ctypes.data_as costs ~5 us per call on the API path
+    return a.__array_interface__["data"][0]
 
 
 def fp32_peak(device: int = 0):

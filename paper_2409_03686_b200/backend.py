@@ -26,6 +26,7 @@ There is no CPU fallback: a missing library or device raises NativeError.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 from dataclasses import dataclass
 
@@ -273,6 +274,10 @@ class AccumulateResult:
         return self._raw1
 
 
+def _free_block(addr: int) -> None:
+    N.lib().em_host_block_free(ctypes.c_void_p(addr))
+
+
 class Plan:
     """One problem resident on one GPU: geometry, K^{1/2}, poles, both weight
     families (and their binning accelerators) uploaded once; ``run`` walks
@@ -367,13 +372,19 @@ class Plan:
         if rc == N.EM_BUDGET:
             raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
         nc = self.n_poles * row
-        view = np.ctypeslib.as_array(blk, shape=(nc + 3 * self.n_poles,))
+        # zero-copy: the result owns the page-locked block the counts were
+        # copied into (returned to the library's cache when the arrays die)
+        N.check(N.lib().em_plan_detach_block(self._h, ctypes.byref(blk)), "em_plan_detach_block")
+        addr = ctypes.cast(blk, ctypes.c_void_p).value
+        cbuf = (ctypes.c_int64 * (nc + 3 * self.n_poles)).from_address(addr)
+        weakref.finalize(cbuf, _free_block, addr)  # every numpy view keeps cbuf alive
+        view = np.frombuffer(cbuf, dtype=np.int64)
         counts = view[:nc].reshape(self.n_poles, row)
         stats = view[nc:].reshape(3, self.n_poles)
         ms = ctypes.c_double(0)
         N.lib().em_plan_last_stats(self._h, ctypes.byref(ms), None, None)
-        return AccumulateResult(None, None, stats[0].copy(), stats[1].copy(), stats[2].copy(),
-                                0, counts.copy(), ms.value, n0=self.n0)
+        return AccumulateResult(None, None, stats[0], stats[1], stats[2], 0, counts, ms.value,
+                                n0=self.n0)
 
     def run_device(self, seed: int, n_rep: int, counts_ptr: int, stats_ptr: int,
                    stream_ptr: int | None = None, rep_start: int = 0) -> None:

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -854,6 +855,44 @@ int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep
   if (err_pole) *err_pole = o.err_pole;
   if (err_rep) *err_rep = o.err_rep;
   return rc;
+}
+
+namespace {
+struct Detached {
+  int dev;
+  size_t bytes;
+};
+std::mutex g_detached_mu;
+std::unordered_map<void*, Detached> g_detached;
+}  // namespace
+
+int em_plan_detach_block(em_plan* p, int64_t** block) {
+  if (!p || !block) return fail(EM_ERR_INVALID, "plan/block null");
+  if (!p->pin.p) return fail(EM_ERR_INVALID, "no staged block to detach");
+  {
+    std::lock_guard<std::mutex> lk(g_detached_mu);
+    g_detached[p->pin.p] = {p->pin.dev, p->pin.bytes};
+  }
+  *block = static_cast<int64_t*>(p->pin.p);
+  p->pin.p = nullptr;
+  p->pin.bytes = 0;
+  return EM_OK;
+}
+
+int em_host_block_free(void* block) {
+  if (!block) return EM_OK;
+  Detached d;
+  {
+    std::lock_guard<std::mutex> lk(g_detached_mu);
+    auto it = g_detached.find(block);
+    if (it == g_detached.end()) return fail(EM_ERR_INVALID, "not a detached block");
+    d = it->second;
+    g_detached.erase(it);
+  }
+  BufCache& c = cache_of(d.dev);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.free_pinned.push_back({d.bytes, block});
+  return EM_OK;
 }
 
 int em_plan_run_device(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,

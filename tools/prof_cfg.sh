@@ -11,5 +11,6 @@ echo "$TAG ncu rc=$?"
 python tools/sass_mix.py /tmp/prof_$TAG.ncu-rep > gpurun_out/mix_$TAG.txt 2>&1
 ncu -i /tmp/prof_$TAG.ncu-rep --page raw --csv > gpurun_out/raw_$TAG.csv 2>/dev/null
 ncu -i /tmp/prof_$TAG.ncu-rep --page source --csv --print-source=sass > gpurun_out/sass_$TAG.csv 2>/dev/null
+python tools/line_mix.py /tmp/prof_$TAG.ncu-rep 80 > gpurun_out/lines_$TAG.txt 2>&1
 [ "$KEEP" = "1" ] && cp /tmp/prof_$TAG.ncu-rep gpurun_out/
 true
