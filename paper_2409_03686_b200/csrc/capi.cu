@@ -584,6 +584,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         if (gf[off + j] != gf[j]) P.concentric = 0;
       }
       P.hr[h] = (float)gf[off + d];
+      P.hr2[h] = (float)(gf[off + d] * gf[off + d]);
     }
     if (nn) {
       const int off = (d + 1) * (1 + nh);
@@ -609,6 +610,21 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       const int k = 24 - (ex - 1) + 1;  // ulp(eps_f) = 2^(ex-1-23)
       P.stop_scale = std::ldexp(1.0f, k);
       P.stop_bias = -P.eps * P.stop_scale;
+    }
+    if (g->gi[1] == 0) P.oR2 = (float)(gf[d] * gf[d]);
+    if (g->gi[1] == 0) {
+      // ball stop on |x|^2: c = fl32((R - eps)^2); for |x|^2 < c the exact
+      // difference c - |x|^2 is >= ulp(c) / 2 (Sterbenz near c, larger
+      // below), so a power-of-two scale 2^k >= 2 / ulp(c) maps it to >= 1
+      // and the FFMA (exact product, one rounding) keeps its sign
+      const double R = gf[d];
+      P.oR2 = (float)(R * R);
+      const float c = (float)((R - eps) * (R - eps));
+      int ex = 0;
+      std::frexp((double)c, &ex);  // c in [2^(ex-1), 2^ex)
+      const int k = 24 - (ex - 1) + 2;
+      P.s2_scale = std::ldexp(1.0f, k);
+      P.s2_bias = c * P.s2_scale;
     }
     P.shrink_rel = 4.0e-6f;
     P.shrink_abs = (float)(scale * 1.1920928955078125e-07);

@@ -87,6 +87,7 @@ struct F32Params {
   float oR;      // ball outer: radius
   float bhi[3];  // box / L-box outer: half-widths (the box is [-bhi, bhi] in the frame)
   float hc[EM_MAX_HOLES][3], hr[EM_MAX_HOLES];  // hole centres in the frame
+  float hr2[EM_MAX_HOLES];                      // hole radii squared
   float notch[2];                               // notch corner in the frame
   signed char comp_side[kMaxComp];
   float A[9];       // K^{1/2}, row-major
@@ -95,6 +96,7 @@ struct F32Params {
   float m2;         // sigma_min(A)^2 (hole bound)
   float eps;
   float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
+  float oR2, s2_scale, s2_bias;  // ball: R^2 and sat(-|x|^2 s + b) = [|x|^2 < (R - eps)^2]
   float shrink_rel, shrink_abs;  // step safety margins
   float keep;                    // 1 - shrink_rel
   unsigned one_bits;             // 0x3f800000 (1.0f), opaque to the compiler: PRMT operand

@@ -35,6 +35,21 @@ namespace f32 {
 constexpr float kPi = 3.14159265358979323846f;
 constexpr float kInf = __builtin_huge_valf();
 
+// MUFU.SQRT / MUFU.RCP without the denormal-range fix-ups the non-ftz
+// approximations carry (an FSETP and two FMULs each); every operand on the
+// walk path is a normal number (distances >= ~1e-7, squares >= ~1e-14), so
+// flushing subnormals changes nothing.  Non-volatile asm: freely scheduled.
+__device__ __forceinline__ float fsqrt(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float fdiv(float a, float b) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+  return a * r;
+}
+
 template <int NH>
 __device__ __forceinline__ int n_holes(const F32Params& P) {
   return NH >= 0 ? NH : P.n_holes;
@@ -55,7 +70,7 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     const float v2 = D == 3 ? x[2] : 0.0f;
     float s2 = v0 * v0 + v1 * v1;
     if (D == 3) s2 = fmaf(v2, v2, s2);
-    const float s = sqrtf(s2);
+    const float s = fsqrt(s2);
     const float rho = P.hr[0];
     const float eo = P.oR - s, eh = s - rho;
     e = fminf(eo, eh);
@@ -70,14 +85,14 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     }
     float aa = a0 * a0 + a1 * a1;
     if (D == 3) aa = fmaf(a2, a2, aa);
-    const float a = sqrtf(aa);
-    const float qo = eo * (P.oR + s);
-    const float Do = a + sqrtf(fmaxf(aa + qo, 0.0f));
-    const float qh = eh * (s + rho);
-    const float Dh = a + sqrtf(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
+    const float a = fsqrt(aa);
+    const float qo = P.oR2 - s2;  // R^2 - |v|^2
+    const float Do = a + fsqrt(fmaxf(aa + qo, 0.0f));
+    const float qh = s2 - P.hr2[0];  // |v|^2 - rho^2
+    const float Dh = a + fsqrt(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
     const float nh = fmaxf(qh, eh * Dh);
     const bool outer = qo * Dh <= nh * Do;
-    r = __fdividef(outer ? qo : nh, outer ? Do : Dh);
+    r = fdiv(outer ? qo : nh, outer ? Do : Dh);
     return;
   }
   if (OUTER == OUTER_BALL) {
@@ -86,8 +101,13 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     const float v2 = D == 3 ? x[2] : 0.0f;
     float s2 = v0 * v0 + v1 * v1;
     if (D == 3) s2 = fmaf(v2, v2, s2);
-    const float s = sqrtf(s2);
-    e = P.oR - s;
+    if (MAXC && NH == 0) {
+      // stop test on |x|^2 itself (no |x| needed): e > eps <=> |x|^2 <
+      // (R - eps)^2, returned already as the FFMA.SAT stop margin (see dist)
+      e = fmaf(s2, -P.s2_scale, P.s2_bias);
+    } else {
+      e = P.oR - fsqrt(s2);
+    }
     if (MAXC) {
       // |x + rAu|^2 <= s^2 + 2 r |Av| + r^2 <= R^2  =>  r <= q / (a + sqrt(a^2 + q))
       const float* A = P.A;
@@ -102,8 +122,8 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
       }
       float aa = a0 * a0 + a1 * a1;
       if (D == 3) aa = fmaf(a2, a2, aa);
-      const float q = e * (P.oR + s);
-      r = __fdividef(q, sqrtf(aa) + sqrtf(fmaxf(aa + q, 0.0f)));
+      const float q = P.oR2 - s2;  // R^2 - |x|^2
+      r = fdiv(q, fsqrt(aa) + fsqrt(fmaxf(aa + q, 0.0f)));
     } else {
       r = e;
     }
@@ -127,7 +147,7 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
       // 0, which stops the walk exactly as a negative distance would
       const float qx = P.notch[0] - x[0], qy = P.notch[1] - x[1];
       const float ax = fmaxf(qx, 0.0f), ay = fmaxf(qy, 0.0f);
-      const float en = sqrtf(fmaf(ax, ax, ay * ay));
+      const float en = fsqrt(fmaf(ax, ax, ay * ay));
       e = fminf(e, en);
       if (FOLD)  // every term through the same monotone t -> t keep - abs
         r = fminf(r, fmaxf(fmaf(en, P.keep, -P.shrink_abs),
@@ -145,7 +165,7 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     const float v2 = D == 3 ? x[2] - P.hc[h][2] : 0.0f;
     float s2 = v0 * v0 + v1 * v1;
     if (D == 3) s2 = fmaf(v2, v2, s2);
-    const float s = sqrtf(s2);
+    const float s = fsqrt(s2);
     const float rho = P.hr[h];
     const float eh = s - rho;
     e = fminf(e, eh);
@@ -163,8 +183,8 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
       }
       float aa = a0 * a0 + a1 * a1;
       if (D == 3) aa = fmaf(a2, a2, aa);
-      const float q = eh * (s + rho);
-      const float rh = __fdividef(q, sqrtf(aa) + sqrtf(fmaxf(fmaf(-P.m2, q, aa), 0.0f)));
+      const float q = s2 - P.hr2[h];  // |v|^2 - rho^2
+      const float rh = fdiv(q, fsqrt(aa) + fsqrt(fmaxf(fmaf(-P.m2, q, aa), 0.0f)));
       r = fminf(r, fmaxf(rh, eh));
     } else {
       r = e;
@@ -176,11 +196,17 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
 // FP32 safety margin: r = r_exact * keep - shrink_abs.  Box faces fold the
 // margin into their gain (one FFMA per face instead of an FMUL per face plus
 // a final FFMA); every other shape applies it once at the end.
+// The first output is the stop margin t: t <= 0 exactly when e <= eps, and
+// t >= 1 otherwise (t = (e - eps) 2^k by one FFMA, or the ball's |x|^2 form),
+// so __saturatef(t) is the lane's 0/1 walking mask.
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
-__device__ __forceinline__ void dist(const F32Params& P, const float* x, float& e, float& r) {
+__device__ __forceinline__ void dist(const F32Params& P, const float* x, float& t, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
+  constexpr bool S2STOP = MAXC && OUTER == OUTER_BALL && NH == 0;
+  float e;
   dist_raw<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
+  t = S2STOP ? e : fmaf(e, P.stop_scale, P.stop_bias);
   if (!FOLD) r = fmaf(r, P.keep, -P.shrink_abs);
 }
 
@@ -454,7 +480,7 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, uns
   } else {
     const float z = sym11_23(zw);
     const float th = angle_of(afbits);
-    const float rho = sqrtf(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+    const float rho = fsqrt(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
     float sn, cs;
     __sincosf(th, &sn, &cs);
     u0 = rho * cs;
@@ -625,9 +651,9 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
       float wm = 0.0f, sf = 0.0f;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float e, r;
-        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        wm = __saturatef(fmaf(e, P.stop_scale, P.stop_bias));
+        float t, r;
+        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
+        wm = __saturatef(t);
         step<D, IDENT>(P, x, r * wm, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k, P.one_bits));
         sf += wm;
       }
@@ -637,9 +663,9 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
       int failed = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float e, r;
-        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-        const int stop = walking & (e <= P.eps);
+        float t, r;
+        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
+        const int stop = walking & (t <= 0.0f);
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
