@@ -41,11 +41,11 @@ sys.path.insert(0, str(ROOT))
 F_STEP = {
     # (cfg, chain): (fp32 ops, xu ops) -- DESIGN.md "F_step of the implemented
     # kernels" derives each entry term by term from walk_f32.cu
-    (1, "woe"): (13, 3), (1, "max"): (13, 3),   # K = I: both chains are the sphere step
-    (2, "woe"): (18, 2), (2, "max"): (21, 2),
-    (3, "woe"): (24, 4), (3, "max"): (44, 7),    # concentric hole: shared |v|, |Av|, one rcp
-    (4, "woe"): (31, 4), (4, "max"): (51, 7),
-    (5, "woe"): (43, 4), (5, "max"): (53, 4),
+    (1, "woe"): (11, 3), (1, "max"): (11, 3),   # K = I: both chains are the sphere step
+    (2, "woe"): (15, 2), (2, "max"): (17, 2),
+    (3, "woe"): (21, 4), (3, "max"): (39, 7),    # concentric hole: shared |v|, |Av|, one rcp
+    (4, "woe"): (28, 4), (4, "max"): (44, 6),
+    (5, "woe"): (36, 4), (5, "max"): (46, 4),
 }
 
 
