@@ -9,6 +9,12 @@ attributes at call time: ``mc_rem`` calls ``backend.run_accumulate``
 ``backend.BACKEND`` (S/cli.py:479).  ``install()`` swaps those attributes, so
 the reference's CLI, ``mc_rem`` and tests run unchanged on the GPU.
 
+``linalg="device"`` also moves the large dense algebra to the GPU (SURVEY
+§8f item 3): ``estimator._gram`` (S/estimator.py:112-118), the SVD of the
+scaled operator (``tsvd.svd``, ``linalg.svd``: S/tsvd.py:104,143,
+S/cli.py:368) and the Gram eigendecomposition (``tsvd.sym_eig``,
+S/tsvd.py:55,158).  The 3x3 ``sym_eig`` behind K^{1/2} stays on the host.
+
 Precision: the default ``"ref64"`` keeps the reference's results bit for bit
 (same counts, exits, step statistics and CSVs); ``precision="fp32"`` selects
 the production kernel (statistically identical A, much faster).  Subprocess
@@ -19,6 +25,8 @@ from __future__ import annotations
 
 import sys
 import types
+
+import numpy as np
 
 from . import backend as B
 from .errors import WalkBudgetError
@@ -33,10 +41,46 @@ def _reference_errors():
         return WalkBudgetError
 
 
+def install_linalg(device: int | None = None):
+    """Route the reference's Gram / SVD / Gram-eigendecomposition through
+    spectral.py on the GPU (float64; agrees with the host to rounding)."""
+    from exitmeasure import estimator, linalg, tsvd
+
+    from . import spectral
+
+    def _gram(a1, sigma1, nu):
+        return spectral.gram(a1, sigma1, nu, device)
+
+    def svd(b):
+        linalg._require_matrix(b, "B")  # the reference's own checks and errors
+        return spectral.svd(b, device)
+
+    def sym_eig(a):
+        a = linalg._require_matrix(a, "A")
+        n, m = a.shape
+        if n != m:
+            raise linalg.ValidationError(f"A must be square, got {n}x{m}")
+        scale = np.max(np.abs(a)) or 1.0
+        if np.max(np.abs(a - a.T)) > 1e-12 * scale:
+            raise linalg.ValidationError("A is not symmetric to 1e-12 relative")
+        w, v = spectral.sym_eig(a, device)
+        return linalg.SymEig(w, v)
+
+    estimator._gram = _gram
+    tsvd.svd = svd
+    tsvd.sym_eig = sym_eig
+    linalg.svd = svd
+
+
 def install(precision: str | None = None, chain: str | None = None, device: int | None = None,
-            module=None):
-    """Patch ``exitmeasure.backend`` (or ``module``) to run on this library.
+            module=None, linalg: str | None = None):
+    """Patch ``exitmeasure.backend`` (or ``module``) to run on this library
+    (and, with ``linalg="device"``, the dense algebra: install_linalg).
     Returns the patched backend module."""
+    if linalg not in (None, "host", "device"):
+        raise ValueError(f"linalg must be 'host' or 'device', got {linalg!r}")
+    if linalg == "device":
+        install_linalg(device)
     if module is None:
         import exitmeasure.backend as module
     ref_budget = _reference_errors()

@@ -200,3 +200,20 @@ def test_row_sharded_gather_gloo_two_ranks(tmp_path):
     res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
     assert res.stdout.count("ok") == 2
+
+
+def test_spectral_requires_a_device():
+    """Device Gram/SVD have no CPU fallback: without CUDA they raise."""
+    import torch
+
+    from paper_2409_03686_b200 import spectral
+    from paper_2409_03686_b200.errors import NativeError, ValidationError
+
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is visible")
+    with pytest.raises(NativeError):
+        spectral.gram(np.ones((3, 2)), np.ones(2), np.ones(3))
+    with pytest.raises(ValidationError):
+        spectral.svd(np.ones(3))
+    with pytest.raises(ValidationError):
+        spectral.sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]))
