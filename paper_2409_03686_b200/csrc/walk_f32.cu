@@ -421,15 +421,25 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
 // Random bits per azimuth: 16 (two angles per 32-bit word) or 23.  A uniform
 // grid of 2^16 equally spaced angles averages every Fourier mode |k| < 2^16
 // exactly, so the mean-value property the step relies on holds to that order
-// (DESIGN.md §3.1); 3D keeps 23-bit z.
+// (DESIGN.md §3.1).
 #ifndef EM_ANGLE_BITS
 #define EM_ANGLE_BITS 16
+#endif
+// 3D z = cos(polar angle): 16 bits (two per word: a 3D batch needs two
+// Philox blocks instead of three, +7-10% on cfg4/cfg5) or 23.  With 16-bit z
+// and 16-bit azimuths a step draws uniformly from 2^32 directions that are
+// the centres of 2^32 equal-area cells of the sphere (Archimedes: equal z
+// bands have equal area), a midpoint rule whose error for the smooth
+// (harmonic) integrands of the mean-value property is O(cell size^2) ~ 1e-9
+// -- far below the Monte Carlo error of any run.
+#ifndef EM_Z_BITS
+#define EM_Z_BITS 16
 #endif
 template <int D>
 struct Batch {
   static constexpr int kSteps = EM_BATCH_STEPS;
   static constexpr int kAngleWords = EM_ANGLE_BITS == 16 ? (kSteps + 1) / 2 : kSteps;
-  static constexpr int kZWords = D == 3 ? kSteps : 0;
+  static constexpr int kZWords = D == 3 ? (EM_Z_BITS == 16 ? (kSteps + 1) / 2 : kSteps) : 0;
   static constexpr int kWords = kZWords + kAngleWords;
   static constexpr int kBlocks = (kWords + 3) / 4;
 };
@@ -449,6 +459,19 @@ __device__ __forceinline__ unsigned angle_bits(const unsigned* wv, int k, unsign
     return __byte_perm(w, one_bits, (k & 1) ? 0x7632u : 0x7610u);
   }
   return one_bits | (wv[Batch<D>::kZWords + k] >> 9);
+}
+
+// z of step k in (-1, 1), never +-1, equally spaced: 23 bits from the top of
+// word k (-1 + (2m + 1)/2^23), or 16 bits from half a word by the same
+// PRMT trick as the angles (f = 1 + m/2^23, m < 2^16: -1 + (2m + 1)/2^16);
+// every operation is exact in FP32
+template <int D>
+__device__ __forceinline__ float z_of(const unsigned* wv, int k, unsigned one_bits) {
+  if (EM_Z_BITS == 16) {
+    const float f = __uint_as_float(__byte_perm(wv[k >> 1], one_bits, (k & 1) ? 0x7632u : 0x7610u));
+    return fmaf(f, 256.0f, -257.0f) + 1.52587890625e-05f;  // + 2^-16
+  }
+  return sym11_23(wv[k]);
 }
 
 // One walk-on-ellipsoids step from x (r from dist()): direction from the RNG
@@ -472,13 +495,12 @@ __device__ __forceinline__ float angle_of(unsigned fbits) {
 }
 
 template <int D, bool IDENT>
-__device__ __forceinline__ void step(const F32Params& P, float* x, float rs, unsigned zw,
+__device__ __forceinline__ void step(const F32Params& P, float* x, float rs, float z,
                                      unsigned afbits) {
   float u0, u1, u2 = 0.0f;
   if (D == 2) {
     __sincosf(angle_of(afbits), &u1, &u0);
   } else {
-    const float z = sym11_23(zw);
     const float th = angle_of(afbits);
     const float rho = fsqrt(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
     float sn, cs;
@@ -654,7 +676,8 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         float t, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         wm = __saturatef(t);
-        step<D, IDENT>(P, x, r * wm, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k, P.one_bits));
+        step<D, IDENT>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                       angle_bits<D>(wv, k, P.one_bits));
         sf += wm;
       }
       walking = wm != 0.0f;
@@ -670,7 +693,8 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
         const float rs = walking ? r : 0.0f;
-        step<D, IDENT>(P, x, rs, D == 3 ? wv[k] : 0u, angle_bits<D>(wv, k, P.one_bits));
+        step<D, IDENT>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                       angle_bits<D>(wv, k, P.one_bits));
         steps += walking;
       }
       // budget overruns: report (smallest key wins), drop from the live set
