@@ -24,7 +24,7 @@ struct WarpPool {
   long long rep0;    // first replicate offset of the current chunk
   int pole;          // pole row of the current chunk
   int next, end;     // next / one-past-last replicate index inside the chunk
-  bool exhausted;
+  int exhausted;     // int, not bool: bools become byte-packed PRMT traffic
 };
 
 __device__ __forceinline__ void pool_init(WarpPool& wp) {
@@ -32,7 +32,7 @@ __device__ __forceinline__ void pool_init(WarpPool& wp) {
   wp.pole = 0;
   wp.next = 0;
   wp.end = 0;
-  wp.exhausted = false;
+  wp.exhausted = 0;
 }
 
 // Called by all 32 lanes (converged).  Lanes set in need_mask receive
@@ -62,7 +62,7 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
   if (lane == 0) c = atomicAdd(W.ticket, 1ULL);
   c = __shfl_sync(kFull, c, 0);
   if (c >= W.n_chunks) {
-    wp.exhausted = true;
+    wp.exhausted = 1;
     return got;
   }
   // chunk c -> (replicate block b, pole p); exact for c < 2^53
@@ -95,6 +95,62 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
                                           int& pole, RepT& rep_off) {
   const int lane = threadIdx.x & 31;
   return pool_take(wp, need_mask, W, pole, rep_off, lane, (1u << lane) - 1u);
+}
+
+// Same contract, shaped for the FP32 kernel's service pass: the common case
+// (the current chunk covers every idle lane) is straight-line predicated
+// code; only a chunk claim branches.  eq / lt are this lane's bit and the
+// bits below it, kept in registers by the caller.
+template <class RepT>
+__device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask, const WorkOut& W,
+                                               int& pole, RepT& rep_off, unsigned eq, unsigned lt) {
+  const int n_need = __popc(need_mask);
+  const int rank = __popc(need_mask & lt);
+  const int me = (need_mask & eq) != 0u;
+  const int avail = wp.end - wp.next;
+  int got = me & (rank < avail);
+  int np = wp.pole;
+  long long r = wp.rep0 + wp.next + rank;
+  if (avail < n_need) {  // rare: claim the next chunk for the lanes beyond avail
+    wp.next = wp.end;
+    if (!wp.exhausted) {
+      unsigned long long c = 0;
+      if (eq == 1u) c = atomicAdd(W.ticket, 1ULL);
+      c = __shfl_sync(kFull, c, 0);
+      if (c >= W.n_chunks) {
+        wp.exhausted = 1;
+      } else {
+        long long b = (long long)((double)c * W.inv_poles);
+        long long p = (long long)c - b * W.n_poles;
+        if (p < 0) {
+          b -= 1;
+          p += W.n_poles;
+        } else if (p >= W.n_poles) {
+          b += 1;
+          p -= W.n_poles;
+        }
+        const long long r0 = b * W.rb;
+        const int valid = (int)(W.n_rep - r0 < W.rb ? W.n_rep - r0 : W.rb);
+        const int rem = n_need - avail;
+        if (me && rank >= avail && rank - avail < valid) {
+          np = (int)p;
+          r = r0 + (rank - avail);
+          got = 1;
+        }
+        wp.pole = (int)p;
+        wp.rep0 = r0;
+        wp.next = rem < valid ? rem : valid;
+        wp.end = valid;
+      }
+    }
+  } else {
+    wp.next += n_need;
+  }
+  if (got) {
+    pole = np;
+    rep_off = (RepT)r;
+  }
+  return got != 0;
 }
 
 // Per-lane step statistics of the pole the lane is currently walking.

@@ -567,9 +567,9 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
   // (empty asm) so the compiler keeps them in registers instead of
   // re-deriving them from special registers on every service pass
   int lane = threadIdx.x & 31;
-  unsigned lt = (1u << lane) - 1u;
+  unsigned eq = 1u << lane, lt = eq - 1u;
   unsigned qb = (unsigned)__cvta_generic_to_shared(&q_all[threadIdx.x >> 5]);
-  asm volatile("" : "+r"(lane), "+r"(lt), "+r"(qb));
+  asm volatile("" : "+r"(lane), "+r"(eq), "+r"(lt), "+r"(qb));
   int qn = 0;  // queued exits of this warp (warp-uniform)
   // idle lanes sit far outside the domain: their distance is negative, so the
   // fast path's stop mask keeps them still without a separate lane flag
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
     const unsigned need = __ballot_sync(kFull, !walking);
     if (need) {
       const unsigned dm = need & live;  // walks that stopped in the last batch
-      const int done = (dm >> lane) & 1u;
+      const bool done = (dm & eq) != 0u;
       if (MODE == 0) {
         if (dm) {
           if (done) {
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
-      if (pool_take(wp, need, W, pole, rep_off, lane, lt)) {
+      if (pool_take_fast(wp, need, W, pole, rep_off, eq, lt)) {
         if (pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
           px = p.x;
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32P
         }
         x[0] = px;
         x[1] = py;
-        x[2] = pz;
+        if (D == 3) x[2] = pz;
         const unsigned long long rep = (unsigned long long)W.rep_start + (unsigned)rep_off;
         rep_lo = (unsigned)rep;
         rep_hi = (unsigned)(rep >> 32);
