@@ -178,7 +178,13 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
     return walks / dt, float(ss.sum()) / dt, "port", dt, float(ss.sum()) / walks
 
 
+# walks per pole per step of the `--impl reference` arm (~0.2-1 s of CPU work
+# per step on 16 host threads, so a K-step run ends in minutes) ...
 REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
+# ... and of the in-bench `cpu_baseline` leg: about 10 s of CPU work on the
+# GPU box's 16 host threads (cfg1: the whole 3.2e5-walk workload), see
+# profiles/r01_cpu_baseline.json for threads=1 / all and linearity in N
+CPU_SAMPLE = {1: 10_000, 2: 163_840, 3: 32_768, 4: 16_384, 5: 1024}
 
 
 def profiled_traffic(cfg_index: int, precision: str, chain: str):
@@ -352,7 +358,7 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            n_sample = REF_SAMPLE[cfg.index]
+            n_sample = CPU_SAMPLE[cfg.index]
             c = cpu_reference_walks_per_s(cfg, n_sample, os.cpu_count() or 1)
             cpu = {"value": c[0], "unit": "walks/s", "cores": os.cpu_count() or 1,
                    "kind": c[2],
