@@ -468,6 +468,12 @@ def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_r
     poles = np.ascontiguousarray(poles, dtype=np.float64)
     if poles.ndim == 1:
         poles = poles.reshape(1, -1)
+    if poles.shape[0] == 0:  # no jobs: the reference returns empty rows (S/backend.py:150-199)
+        z = np.zeros(0, dtype=np.int64)
+        return AccumulateResult(np.zeros((0, int(side0.size))), np.zeros((0, int(side1.size))),
+                                z, z.copy(), z.copy(), 0, np.zeros((0, int(side0.size + side1.size)),
+                                                                   dtype=np.int64),
+                                n0=int(side0.size))
     with Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
               pole_ids) as plan:
         return plan.run(seed, n_rep)

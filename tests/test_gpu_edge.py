@@ -1,0 +1,142 @@
+"""Edge cases of the drop-in boundary on the GPU: empty ranges, tiny jobs,
+empty families, budget overruns on the FP32 path, replicate offsets across
+the 2^32 boundary of the RNG counter, and the size limits.  Conventions
+follow the reference driver/kernel (S/backend.py:137-227,
+S/_kernel.pyx:376-464; S/ = the reference's src/exitmeasure)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2409_03686_b200 import _native, backend
+
+    _native.require_device(0)
+    return backend
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    from paper_2409_03686_b200 import configs
+
+    return configs.get(2)
+
+
+def _sides(B, cfg):
+    return B.pack_side(cfg.fam0, cfg.d, cfg.eps), B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+
+
+@pytest.mark.parametrize("precision", ["ref64", "fp32"])
+def test_zero_replicates(B, cfg2, precision):
+    s0, s1 = _sides(B, cfg2)
+    r = B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, cfg2.poles[:5], cfg2.seed, cfg2.eps, 10**6, 0,
+                         s0, s1, precision=precision)
+    assert r.raw0.shape == (5, s0.size) and r.raw1.shape == (5, s1.size)
+    assert not r.raw0.any() and not r.raw1.any()
+    assert not r.steps_sum.any() and not r.steps_max.any()
+
+
+def test_zero_poles(B, cfg2):
+    s0, s1 = _sides(B, cfg2)
+    r = B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, np.zeros((0, 2)), cfg2.seed, cfg2.eps, 10**6,
+                         100, s0, s1, precision="fp32")
+    assert r.raw0.shape == (0, s0.size) and r.raw1.shape == (0, s1.size)
+    assert r.steps_sum.shape == (0,)
+
+
+def test_empty_chunk_range(B, cfg2):
+    """accumulate_chunk / walk_exits_chunk with rep_start == rep_end leave the
+    outputs untouched and report no error (the reference's empty loop)."""
+    s0, s1 = _sides(B, cfg2)
+    geom = B.pack_geometry(cfg2.dom)
+    out0 = np.full(s0.size, 7.0)
+    out1 = np.full(s1.size, 3.0)
+    res = B.accumulate_chunk(geom.gi, geom.gf, geom.comp_side, cfg2.kt.k_sqrt, cfg2.poles[0], 0,
+                             5, 5, cfg2.seed, cfg2.eps, 10**6, s0.anchors, s0.blk, s0.blkf, 0,
+                             np.zeros(0), 2, s1.anchors, s1.blk, s1.blkf, 0, np.zeros(0), 2,
+                             out0, out1)
+    assert tuple(res) == (0, 0, 0, 0, -1)
+    assert np.all(out0 == 7.0) and np.all(out1 == 3.0)
+    x, steps, comp, err = B.walk_exits_chunk(geom.gi, geom.gf, geom.comp_side, cfg2.kt.k_sqrt,
+                                             cfg2.poles[0], 0, 9, 9, cfg2.seed, cfg2.eps, 10**6)
+    assert x.shape == (0, 2) and steps.shape == (0,) and comp.shape == (0,) and err == -1
+
+
+@pytest.mark.parametrize("n_rep", [1, 5, 31, 33])
+def test_fp32_tiny_jobs_count_every_walk(B, cfg2, n_rep):
+    """Fewer walks than one warp / one block: every walk is counted once."""
+    s0, s1 = _sides(B, cfg2)
+    r = B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, cfg2.poles[:3], cfg2.seed, cfg2.eps, 10**6,
+                         n_rep, s0, s1, precision="fp32")
+    assert np.all(r.counts.sum(axis=1) == n_rep)
+    assert np.all(r.steps_max >= 1) and np.all(r.steps_sum >= n_rep)
+
+
+def test_empty_family_on_a_used_side_is_rejected(B, cfg2):
+    """An exit side with no anchors is a configuration error at the boundary
+    (the reference's kernel would write out of bounds)."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.errors import NativeError
+
+    cfg3 = configs.get(3)  # annulus: outer circle -> Gamma0, hole -> Gamma1
+    s0 = B.pack_side(None, 2, cfg3.eps)
+    _, s1 = _sides(B, cfg3)
+    for precision in ("ref64", "fp32"):
+        with pytest.raises(NativeError, match="side0"):
+            B.run_accumulate(cfg3.dom, cfg3.kt.k_sqrt, cfg3.poles[:2], cfg3.seed, cfg3.eps, 10**6,
+                             10, s0, s1, precision=precision)
+
+
+def test_fp32_budget_error_is_the_smallest_failing_walk(B, cfg2):
+    """With a tiny step budget the FP32 run reports the lexicographically
+    smallest (pole, replicate) whose walk needs more steps, exactly as the
+    reference's job-order scan (S/backend.py:189-192); the step counts come
+    from the same walks run through the exits kernel with a large budget."""
+    from paper_2409_03686_b200.errors import WalkBudgetError
+
+    s0, s1 = _sides(B, cfg2)
+    budget = 6
+    poles = cfg2.poles[:4]
+    expect = None
+    for p in range(len(poles)):
+        _, steps, _ = B.run_exits(cfg2.dom, cfg2.kt.k_sqrt, poles[p], p, cfg2.seed, cfg2.eps,
+                                  10**6, 64, precision="fp32")
+        over = np.nonzero(steps > budget)[0]
+        if over.size:
+            expect = (p, int(over[0]))
+            break
+    assert expect is not None
+    with pytest.raises(WalkBudgetError) as ei:
+        B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, poles, cfg2.seed, cfg2.eps, budget, 64, s0, s1,
+                         precision="fp32")
+    assert (ei.value.pole, ei.value.replicate, ei.value.max_steps) == (*expect, budget)
+
+
+@pytest.mark.parametrize("rep_start", [0, 1000, 2**32 - 3])
+def test_fp32_replicate_ranges_compose(B, cfg2, rep_start):
+    """Replicates [a, c) = [a, b) + [b, c) row for row (every walk keyed by
+    its own replicate index), including a range across the 2^32 boundary of
+    the RNG counter's low word."""
+    s0, s1 = _sides(B, cfg2)
+    geom = B.pack_geometry(cfg2.dom)
+    with B.Plan(geom, cfg2.kt.k_sqrt, cfg2.poles[:4], cfg2.eps, 10**6, s0, s1, "fp32") as plan:
+        full = plan.run(cfg2.seed, 40, rep_start).counts.copy()
+        a = plan.run(cfg2.seed, 7, rep_start).counts.copy()
+        b = plan.run(cfg2.seed, 33, rep_start + 7).counts.copy()
+    assert np.array_equal(full, a + b)
+    assert np.all(full.sum(axis=1) == 40)
+
+
+def test_fp32_replicate_limit(B, cfg2):
+    """More than 2^31 - 1 replicates per pole in one FP32 run is refused
+    before anything is launched (int32 replicate offsets in the kernel)."""
+    from paper_2409_03686_b200.errors import NativeError
+
+    s0, s1 = _sides(B, cfg2)
+    geom = B.pack_geometry(cfg2.dom)
+    with B.Plan(geom, cfg2.kt.k_sqrt, cfg2.poles[:1], cfg2.eps, 10**6, s0, s1, "fp32") as plan:
+        with pytest.raises(NativeError, match="2\\^31"):
+            plan.run(cfg2.seed, 2**31)
