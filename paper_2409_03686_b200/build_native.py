@@ -34,7 +34,7 @@ UNITS = [
     ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]),
     ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false",
                      f"-DEM_BATCH_STEPS={os.environ.get('EM_BATCH_STEPS', '8')}",
-                     f"-DEM_MIN_BLOCKS={os.environ.get('EM_MIN_BLOCKS', '4')}",
+                     f"-DEM_MIN_BLOCKS={os.environ.get('EM_MIN_BLOCKS', '0')}",
                      f"-DEM_ANGLE_BITS={os.environ.get('EM_ANGLE_BITS', '16')}",
                      f"-DEM_Z_BITS={os.environ.get('EM_Z_BITS', '16')}"]),
     ("capi.cu", []),

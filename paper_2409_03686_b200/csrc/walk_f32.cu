@@ -549,9 +549,13 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 
 // MODE 0: bin exits into the count rows + per-pole step statistics
 // MODE 1: write exit points / steps / components (em_run_exits)
+// resident 256-thread blocks per SM the register allocation must allow:
+// 5 in 2D (<= 51 registers; cfg3 +3%), 4 in 3D (<= 64; 5 costs cfg4 4%),
+// measured with tools/ab_bench.sh EM_MIN_BLOCKS
 #ifndef EM_MIN_BLOCKS
-#define EM_MIN_BLOCKS 4
+#define EM_MIN_BLOCKS 0
 #endif
+#define EM_MINB(D) (EM_MIN_BLOCKS > 0 ? EM_MIN_BLOCKS : ((D) == 2 ? 5 : 4))
 // Per-warp exit queue in shared memory: exit point + pole (as int bits in
 // .w) and step count, binned 32 at a time.
 struct ExitQueue {
@@ -560,7 +564,7 @@ struct ExitQueue {
 };
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
-__global__ void __launch_bounds__(256, EM_MIN_BLOCKS) walk_f32_kernel(const F32Params P) {
+__global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
   __shared__ ExitQueue q_all[kWarps];
   // lane id, lane mask and the queue's shared-window address are made opaque

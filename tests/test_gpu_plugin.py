@@ -86,3 +86,37 @@ def test_cli_outputs_byte_identical(ref, tmp_path):
         outs.append(out)
     for name in ("eigenvalues.csv", "density.csv", "eigvecs.csv", "tsvd.csv", "residuals.csv"):
         assert (outs[0] / name).read_bytes() == (outs[1] / name).read_bytes(), name
+
+
+def test_reference_driver_threads_over_the_chunk_dropin(ref):
+    """Only ``_impl`` swapped: the reference's OWN driver (S/backend.py:147-199,
+    a ThreadPoolExecutor over 8192-walk chunks, 8 threads) calls our
+    accumulate_chunk / walk_exits_chunk concurrently; results equal the
+    reference kernel's bit for bit (reentrancy, released GIL, in-place +=)."""
+    from exitmeasure.conductivity import identity_tensor
+    from exitmeasure.geometry import catalog, side_points
+
+    from paper_2409_03686_b200 import plugin
+
+    dom = catalog("annulus")
+    s0 = ref.pack_side(side_points(dom, "gamma0", [64]), 2, 1e-6)
+    s1 = ref.pack_side(side_points(dom, "gamma1", [32]), 2, 1e-6)
+    poles = np.array([[0.0, 0.75], [0.8, 0.1], [-0.6, -0.5]])
+    args = (dom, identity_tensor(2).k_sqrt, poles, 23, 1e-6, 10**6, 20000, s0, s1)
+    cpu = ref.run_accumulate(*args, threads=8)
+    x_cpu = ref.run_exits(dom, identity_tensor(2).k_sqrt, poles[1], 1, 23, 1e-6, 10**6, 20000,
+                          threads=8)
+    saved = (ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND)
+    try:
+        plugin.install(precision="ref64", module=ref)
+        ref.run_accumulate, ref.run_exits = saved[0], saved[1]  # keep the reference driver
+        assert ref._impl.accumulate_chunk.__module__.startswith("paper_2409_03686_b200")
+        gpu = ref.run_accumulate(*args, threads=8)
+        x_gpu = ref.run_exits(dom, identity_tensor(2).k_sqrt, poles[1], 1, 23, 1e-6, 10**6, 20000,
+                              threads=8)
+    finally:
+        ref.run_accumulate, ref.run_exits, ref._impl, ref.BACKEND = saved
+    for name in ("raw0", "raw1", "steps_sum", "steps_sq_sum", "steps_max"):
+        assert np.array_equal(getattr(cpu, name), getattr(gpu, name)), name
+    for a, b in zip(x_cpu, x_gpu):
+        assert np.array_equal(a, b)

@@ -9,7 +9,7 @@ mkdir -p $OUT
 /usr/local/cuda/bin/nvcc -cubin -o $OUT/walk_f32.cubin $ROOT/paper_2409_03686_b200/csrc/walk_f32.cu \
   -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -I $ROOT/include \
   -fmad=true -prec-sqrt=false -prec-div=false -DEM_BATCH_STEPS=${EM_BATCH_STEPS:-8} \
-  -DEM_MIN_BLOCKS=${EM_MIN_BLOCKS:-4} -DEM_ANGLE_BITS=${EM_ANGLE_BITS:-16} -Xptxas -v 2> $OUT/ptxas.log
+  -DEM_MIN_BLOCKS=${EM_MIN_BLOCKS:-0} -DEM_ANGLE_BITS=${EM_ANGLE_BITS:-16} -Xptxas -v 2> $OUT/ptxas.log
 /usr/local/cuda/bin/cuobjdump -sass $OUT/walk_f32.cubin > $OUT/all.sass
 python3 - "$OUT" "$K" <<'PY'
 import re, sys
