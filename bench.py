@@ -4,8 +4,7 @@ walk-steps/s for A, % of the FP32 issue roofline).
 One "step" = one pass of the hot path over the whole workload: every walk of
 every pole run to the eps-shell and binned into the (n_poles, n0 + n1) int64
 count rows (the reference's run_accumulate, S/backend.py:147-199, S/ =
-/root/reference/pkg/src/exitmeasure/), plus -- at N > 1 GPUs -- the NCCL
-all-gather of the count rows to every rank.
+/root/reference/pkg/src/exitmeasure/).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
                     [--precision fp32|ref64] [--chain max|woe]
@@ -13,9 +12,14 @@ all-gather of the count rows to every rank.
 
 Workload at N=1: BASELINE configs[1] (cfg2, the unit square with
 K=[[2,.8],[.8,1]], 256 poles x 1e5 walks, eps 1e-5, 512 edge bins).
-Multi-GPU: poles are sharded cyclically over ranks (pole i -> rank i mod N,
-RNG keyed by the global pole id), so per-GPU work shrinks as N grows
-("scaling": "strong", total work fixed).
+Multi-GPU (one process per GPU, torchrun): by default "scaling": "weak" --
+every rank walks all poles x n walks on its own replicate range [r n, (r+1) n)
+(walks are keyed by their global replicate index), no collective inside the
+timed region, and the rows are summed once (NCCL all-reduce) afterwards into
+the N*n-walk estimate.  `--scaling strong` shards the fixed workload's rows
+cyclically over the ranks (pole i -> rank i mod N, RNG keyed by the global
+pole id) with an NCCL all-gather of the count rows every step.
+Timing: CUDA events on each rank, max over ranks.
 """
 
 from __future__ import annotations
@@ -265,7 +269,19 @@ def run_ours(args):
     cfg = configs.get(args.config)
     if args.n_rep:
         cfg = cfg.subset(None, args.n_rep)
-    ids = np.arange(rank, cfg.n_poles, world)  # cyclic row shard
+    weak = args.scaling == "weak"
+    if weak:
+        # weak scaling: every rank walks ALL poles on its own replicate range
+        # [rank n, (rank + 1) n) (walks are keyed by their global replicate
+        # index, so the ranks' counts add up to the N*n-walk estimate exactly);
+        # no collective on the data path, one sum of the rows after timing
+        ids = np.arange(cfg.n_poles)
+        rep_start = rank * cfg.n_rep
+    else:
+        # strong scaling: cyclic row shard of the fixed workload + an NCCL
+        # all-gather of the count rows every step
+        ids = np.arange(rank, cfg.n_poles, world)
+        rep_start = 0
     geom = backend.pack_geometry(cfg.dom)
     s0 = backend.pack_side(cfg.fam0, cfg.d, cfg.eps)
     s1 = backend.pack_side(cfg.fam1, cfg.d, cfg.eps)
@@ -274,17 +290,18 @@ def run_ours(args):
                         pole_ids=ids, grid=args.grid)
     row = plan.n0 + plan.n1
     m_local = len(ids)
-    m_pad = -(-cfg.n_poles // world)
+    m_pad = m_local if weak else -(-cfg.n_poles // world)
     counts = torch.zeros((m_pad, row), dtype=torch.int64, device="cuda")
     stats = torch.zeros((3, m_pad), dtype=torch.int64, device="cuda")
-    gathered = torch.zeros((world * m_pad, row), dtype=torch.int64, device="cuda") if world > 1 else None
+    gathered = (torch.zeros((world * m_pad, row), dtype=torch.int64, device="cuda")
+                if world > 1 and not weak else None)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def one_step():
         plan.run_device(cfg.seed, cfg.n_rep, counts.data_ptr(), stats.data_ptr(),
-                        stream.cuda_stream)
-        if world > 1:
+                        stream.cuda_stream, rep_start)
+        if gathered is not None:
             dist.all_gather_into_tensor(gathered, counts)
 
     for _ in range(args.warmup):
@@ -310,6 +327,12 @@ def run_ours(args):
             launches += plan.last_launches()
         torch.cuda.synchronize()
     plan.check()  # budget errors of the (asynchronous) runs
+    combined_ok = None
+    if dist and weak:
+        # the one exchange, outside the timed region: sum the ranks' rows into
+        # the N*n-walk estimate and check every row counts all of its walks
+        dist.all_reduce(counts)
+        combined_ok = bool((counts.sum(dim=1) == world * cfg.n_rep).all().item())
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -323,7 +346,7 @@ def run_ours(args):
         steps_total_run = int(st.item())
     else:
         steps_total_run = steps_per_run
-    walks = cfg.total_walks * args.steps
+    walks = cfg.total_walks * (world if weak else 1) * args.steps
     value = walks / (tot_ms * 1e-3)
     steps_per_s = steps_total_run * args.steps / (tot_ms * 1e-3)
     clocks = clk.summary()
@@ -349,7 +372,10 @@ def run_ours(args):
                                        precision=plan.precision, chain=plan.chain,
                                        device=device, pole_ids=sub_ids)
             e2e_times.append(time.perf_counter() - t0)
-        e2e_val = len(sub_ids) * cfg.n_rep * world / float(np.median(e2e_times[1:]))
+        e2e_val = (len(sub_ids) * cfg.n_rep * (world if weak else 1)
+                   / float(np.median(e2e_times[1:])))
+        if not weak:
+            e2e_val *= world  # every rank walks its shard concurrently
         h2d = (cfg.poles[sub_ids].nbytes + s0.anchors.nbytes + s1.anchors.nbytes
                + geom.gi.nbytes + geom.gf.nbytes + cfg.kt.k_sqrt.nbytes)
         d2h = r.counts.nbytes + 3 * 8 * len(sub_ids)
@@ -367,14 +393,21 @@ def run_ours(args):
         line = {
             "metric": "walks/s", "value": value, "unit": "walks/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if weak else "strong",
+            "vs_baseline": None,
             "dtype": "f32" if plan.precision == "fp32" else "f64", "data": "synthetic",
             "steps_per_s": steps_per_s,
-            "mean_steps_per_walk": steps_total_run / cfg.total_walks,
+            "mean_steps_per_walk": steps_total_run / (cfg.total_walks * (world if weak else 1)),
             "config": {"workload": f"{cfg.name}: {cfg.n_poles} poles x {cfg.n_rep:.0e} walks, "
                                    f"eps {cfg.eps:g}, {plan.n0 + plan.n1} bins",
                        "precision": plan.precision, "chain": plan.chain,
-                       "parallelism": f"rows cyclic over {world} GPU(s)",
+                       "parallelism": (f"{world} GPU(s), each all poles x {cfg.n_rep:.0e} walks on "
+                                       "its own replicate range; rows summed once after timing"
+                                       + ("" if combined_ok is None else
+                                          f" (row sums {'ok' if combined_ok else 'WRONG'})")
+                                       if weak else
+                                       f"rows cyclic over {world} GPU(s), NCCL all-gather of "
+                                       "the count rows every step"),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "counts": "int64 (n_poles, n0+n1) rows + step stats"},
             "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
@@ -420,6 +453,9 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every rank walks all poles on its own replicate range "
+                         "(default); strong = cyclic row shard of the fixed workload")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
