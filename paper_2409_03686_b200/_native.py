@@ -153,8 +153,15 @@ def device_count() -> int:
     return int(lib().em_device_count())
 
 
+_seen_devices = 0
+
+
 def require_device(device: int = 0) -> None:
+    global _seen_devices
+    if device < _seen_devices:  # visible devices do not go away within a process
+        return
     n = device_count()
+    _seen_devices = n
     if device >= n:
         raise NativeError(f"no CUDA device {device} ({n} visible): the exit-measure "
                           "path runs on the GPU only (no CPU fallback)")
