@@ -6,17 +6,19 @@
 // src/exitmeasure/) re-designed for SIMT FP32 issue:
 //
 //  * RNG: Philox4x32-10 keyed (seed) with counter (draw, rep_lo, pole, rep_hi)
-//    -- one block per lane per batch of steps, so RNG is warp-uniform work,
-//    never a divergent per-lane refill.  2D: one 32-bit word per step (an
-//    angle); 3D: two words (z and an angle, Archimedes' projection).  No
-//    rejection loop (the reference's Marsaglia trials diverge on SIMT).
+//    -- blocks per lane per 8-step batch, so RNG is warp-uniform work, never
+//    a divergent per-lane refill.  2D: a 16-bit azimuth per step (one block
+//    per batch); 3D: a 16-bit z and a 16-bit azimuth (Archimedes' projection,
+//    two blocks per batch).  No rejection loop (the reference's Marsaglia
+//    trials diverge on SIMT).
 //  * Step: x <- x + r(x) K^{1/2} u, with r = sd (EM_CHAIN_WOE, the reference
 //    chain) or r = a certified lower bound of the largest inscribed
 //    K^{1/2}-ellipsoid (EM_CHAIN_MAX; exact for planes, closed form for balls
 //    and holes), shrunk by a relative + absolute FP32 margin so no step
 //    leaves the closed domain by more than an ulp.
-//  * Stop: Euclidean sd <= eps (the reference's shell, S/_kernel.pyx:177-180);
-//    points a rounding step outside count as exits too.
+//  * Stop: Euclidean sd <= eps (the reference's shell, S/_kernel.pyx:177-180)
+//    as one saturating FFMA that also masks the step; points a rounding step
+//    outside count as exits too.
 //  * Binning: owner component -> side (S/_kernel.pyx:145-156), then the
 //    nearest anchor of that side's family in O(1): circle/square blocks by
 //    angle / arc length (S/_kernel.pyx:260-313 without the window scan),
@@ -524,9 +526,6 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, flo
   x[1] = fmaf(rs, y1, x[1]);
   if (D == 3) x[2] = fmaf(rs, y2, x[2]);
 }
-
-// lane status
-enum : int { ST_IDLE = 0, ST_WALK = 1, ST_DONE = 2, ST_FAIL = 3 };
 
 constexpr int kWarps = 8;   // 256 threads per block
 constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
