@@ -12,13 +12,14 @@ count rows (the reference's run_accumulate, S/backend.py:147-199, S/ =
 
 Workload at N=1: BASELINE configs[1] (cfg2, the unit square with
 K=[[2,.8],[.8,1]], 256 poles x 1e5 walks, eps 1e-5, 512 edge bins).
-Multi-GPU (one process per GPU, torchrun): by default "scaling": "weak" --
-every rank walks all poles x n walks on its own replicate range [r n, (r+1) n)
-(walks are keyed by their global replicate index), no collective inside the
-timed region, and the rows are summed once (NCCL all-reduce) afterwards into
-the N*n-walk estimate.  `--scaling strong` shards the fixed workload's rows
-cyclically over the ranks (pole i -> rank i mod N, RNG keyed by the global
-pole id) with an NCCL all-gather of the count rows every step.
+Multi-GPU (one process per GPU, torchrun): by default "scaling": "strong", as
+north_star's target is stated (>= 85% strong-scaling efficiency at 8 GPUs):
+the fixed workload's rows are sharded cyclically over the ranks (pole i ->
+rank i mod N, RNG keyed by the global pole id) and every step ends with the
+NCCL all-gather of the count rows, inside the timed region.
+`--scaling weak` instead has every rank walk all poles x n walks on its own
+replicate range [r n, (r+1) n) (walks keyed by their global replicate index),
+no collective inside the timed region, rows summed once afterwards.
 Timing: CUDA events on each rank, max over ranks.
 """
 
@@ -453,9 +454,10 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = every rank walks all poles on its own replicate range "
-                         "(default); strong = cyclic row shard of the fixed workload")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong = cyclic row shard of the fixed workload + NCCL "
+                         "all-gather of the rows (default: north_star's strong-scaling "
+                         "target); weak = every rank walks all poles on its own replicate range")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
