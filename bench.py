@@ -48,8 +48,8 @@ F_STEP = {
     # kernels" derives each entry term by term from walk_f32.cu
     (1, "woe"): (11, 3), (1, "max"): (11, 3),   # K = I: both chains are the sphere step
     (2, "woe"): (15, 2), (2, "max"): (17, 2),
-    (3, "woe"): (21, 4), (3, "max"): (39, 7),    # concentric hole: shared |v|, |Av|, one rcp
-    (4, "woe"): (28, 4), (4, "max"): (44, 6),
+    (3, "woe"): (21, 4), (3, "max"): (38, 7),    # concentric hole: shared |v|, |Av|, one rcp
+    (4, "woe"): (28, 4), (4, "max"): (41, 6),
     (5, "woe"): (36, 4), (5, "max"): (46, 4),
 }
 

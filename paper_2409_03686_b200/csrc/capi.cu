@@ -593,6 +593,18 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     }
     for (int c = 0; c < 1 + nh + nn; ++c) P.comp_side[c] = g->comp_side[c];
     for (int i = 0; i < d * d; ++i) P.A[i] = (float)g->ksqrt[i];
+    {
+      double K[3][3] = {{0.0}};
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+          for (int k = 0; k < d; ++k) K[i][j] += g->ksqrt[k * d + i] * g->ksqrt[k * d + j];
+      P.Kq[0] = (float)K[0][0];
+      P.Kq[1] = (float)K[1][1];
+      P.Kq[2] = (float)K[2][2];
+      P.Kq[3] = (float)(2.0 * K[0][1]);
+      P.Kq[4] = (float)(2.0 * K[0][2]);
+      P.Kq[5] = (float)(2.0 * K[1][2]);
+    }
     for (int i = 0; i < d; ++i) {
       double n2 = 0.0;
       for (int k = 0; k < d; ++k) n2 += g->ksqrt[k * d + i] * g->ksqrt[k * d + i];

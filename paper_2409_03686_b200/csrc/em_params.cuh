@@ -91,6 +91,7 @@ struct F32Params {
   float notch[2];                               // notch corner in the frame
   signed char comp_side[kMaxComp];
   float A[9];       // K^{1/2}, row-major
+  float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v
   float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid
   float gk[3];      // g * keep (rounded down): face gain with the relative margin folded in
   float m2;         // sigma_min(A)^2 (hole bound)
