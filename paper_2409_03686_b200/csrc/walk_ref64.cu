@@ -25,36 +25,37 @@ __constant__ double kM2PI = 6.283185307179586476925286766559;
 constexpr double kInv53 = 1.0 / 9007199254740992.0;
 constexpr long long kBigIndex = 1LL << 62;
 
-// S/_kernel.pyx:57-81
-__device__ __forceinline__ void sample_direction(int d, unsigned long long seed,
-                                                 unsigned long long& draw,
-                                                 unsigned long long rep,
-                                                 unsigned long long pole, double* u) {
-  for (;;) {
-    u64x4 w = philox4x64_10(seed, 0ULL, draw, 0ULL, rep, pole);
-    draw += 1ULL;
-    double u0 = (double)(w.w0 >> 11) * kInv53;
-    double u1 = (double)(w.w1 >> 11) * kInv53;
-    double v1 = 2.0 * u0 - 1.0;
-    double v2 = 2.0 * u1 - 1.0;
-    double s = v1 * v1 + v2 * v2;
-    if (d == 2) {
-      if (s <= 1.0 && s > 0.0) {
-        double rs = sqrt(s);
-        u[0] = v1 / rs;
-        u[1] = v2 / rs;
-        return;
-      }
-    } else {
-      if (s < 1.0) {
-        double f = 2.0 * sqrt(1.0 - s);
-        u[0] = v1 * f;
-        u[1] = v2 * f;
-        u[2] = 1.0 - 2.0 * s;
-        return;
-      }
+// One Marsaglia trial of S/_kernel.pyx:57-81 (the reference loops until a
+// trial is accepted; the kernel below runs one trial per iteration so a
+// rejecting lane does not hold its warp -- same draws, same directions).
+__device__ __forceinline__ bool direction_trial(int d, unsigned long long seed,
+                                                unsigned long long& draw,
+                                                unsigned long long rep,
+                                                unsigned long long pole, double* u) {
+  u64x4 w = philox4x64_10(seed, 0ULL, draw, 0ULL, rep, pole);
+  draw += 1ULL;
+  double u0 = (double)(w.w0 >> 11) * kInv53;
+  double u1 = (double)(w.w1 >> 11) * kInv53;
+  double v1 = 2.0 * u0 - 1.0;
+  double v2 = 2.0 * u1 - 1.0;
+  double s = v1 * v1 + v2 * v2;
+  if (d == 2) {
+    if (s <= 1.0 && s > 0.0) {
+      double rs = sqrt(s);
+      u[0] = v1 / rs;
+      u[1] = v2 / rs;
+      return true;
+    }
+  } else {
+    if (s < 1.0) {
+      double f = 2.0 * sqrt(1.0 - s);
+      u[0] = v1 * f;
+      u[1] = v2 * f;
+      u[2] = 1.0 - 2.0 * s;
+      return true;
     }
   }
+  return false;
 }
 
 // S/_kernel.pyx:89-116
@@ -182,6 +183,15 @@ __device__ __forceinline__ long long wrap(long long k, long long count) {
   return k;
 }
 
+// wrap() of k + off for k already in [0, count) and |off| <= 2: one
+// conditional add/subtract (same value; the 64-bit modulo is ~60 instructions)
+__device__ __forceinline__ long long wrap_near(long long k, long long count) {
+  if (count < 3) return wrap(k, count);
+  if (k < 0) return k + count;
+  if (k >= count) return k - count;
+  return k;
+}
+
 // S/_kernel.pyx:242-320.  Extension: a block phase p (anchors at spacing*(k+p))
 // shifts the centre of the +-2 window by -p; the window still holds the
 // minimiser and its ties, so the lexicographic winner is unchanged and equals
@@ -200,7 +210,7 @@ __device__ long long assign_anchor(const double* x, int d, const Side64& s) {
       if (phase != 0.0) t = t - phase;
       long long k = wrap((long long)floor(t + 0.5), count);
       for (int off = -2; off < 3; ++off)
-        lex_update(x, d, s.anchors, start + wrap(k + off, count), best_d2, best_gi);
+        lex_update(x, d, s.anchors, start + wrap_near(k + off, count), best_d2, best_gi);
     } else if (kind == BLK_SQUARE) {
       double spacing = 8.0 * radius / (double)count;
       if (fabs(square_signed(cx, cy, radius, x)) <= 0.125 * spacing) {
@@ -221,7 +231,7 @@ __device__ long long assign_anchor(const double* x, int d, const Side64& s) {
         if (phase != 0.0) t = t - phase;
         long long k = wrap((long long)floor(t + 0.5), count);
         for (int off = -2; off < 3; ++off)
-          lex_update(x, d, s.anchors, start + wrap(k + off, count), best_d2, best_gi);
+          lex_update(x, d, s.anchors, start + wrap_near(k + off, count), best_d2, best_gi);
       } else {
         for (long long idx = 0; idx < count; ++idx)
           lex_update(x, d, s.anchors, start + idx, best_d2, best_gi);
@@ -246,6 +256,10 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   long long steps = 0, rep_off = 0;
   int pole = 0;
   bool active = false;
+  // 0: evaluate the distance of a new step (stop / budget checks), 1: drawing
+  // its direction -- a lane whose Marsaglia trial was rejected stays at 1
+  int phase = 0;
+  double sd = 0.0;
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
@@ -260,42 +274,47 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
         for (int j = 0; j < d; ++j) x[j] = P.poles[pole * d + j];
         draw = 0;
         steps = 0;
+        phase = 0;
         active = true;
       }
       if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
     }
     if (!active) continue;
-    // S/_kernel.pyx:176-197
-    const double sd = signed_dist(P, x);
-    if (sd <= P.eps) {
-      active = false;
-      if (MODE == 0) {
-        const int comp = owner_component(P, x);
-        const int side = P.comp_side[comp];
-        const long long winner = assign_anchor(x, d, P.side[side]);
-        const long long col = side ? W.col_off1 + winner : winner;
-        atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
-        acc_add(acc, W, pole, (unsigned long long)steps);
-      } else {
-        const long long o = (long long)pole * W.n_rep + rep_off;
-        for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
-        W.steps_out[o] = steps;
-        W.comp_out[o] = owner_component(P, x);
+    // S/_kernel.pyx:176-197, one direction trial per iteration
+    if (phase == 0) {
+      sd = signed_dist(P, x);
+      if (sd <= P.eps) {
+        active = false;
+        if (MODE == 0) {
+          const int comp = owner_component(P, x);
+          const int side = P.comp_side[comp];
+          const long long winner = assign_anchor(x, d, P.side[side]);
+          const long long col = side ? W.col_off1 + winner : winner;
+          atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+          acc_add(acc, W, pole, (unsigned long long)steps);
+        } else {
+          const long long o = (long long)pole * W.n_rep + rep_off;
+          for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
+          W.steps_out[o] = steps;
+          W.comp_out[o] = owner_component(P, x);
+        }
+        continue;
       }
-      continue;
-    }
-    if (steps >= P.max_steps) {
-      active = false;
-      atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
-      if (MODE == 1) {
-        const long long o = (long long)pole * W.n_rep + rep_off;
-        for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
-        W.steps_out[o] = steps;
-        W.comp_out[o] = 0;
+      if (steps >= P.max_steps) {
+        active = false;
+        atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
+        if (MODE == 1) {
+          const long long o = (long long)pole * W.n_rep + rep_off;
+          for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
+          W.steps_out[o] = steps;
+          W.comp_out[o] = 0;
+        }
+        continue;
       }
-      continue;
+      phase = 1;
     }
-    sample_direction(d, P.seed, draw, rep, pid, u);
+    if (!direction_trial(d, P.seed, draw, rep, pid, u)) continue;
+    phase = 0;
     const double* k = P.ks;
     if (d == 2) {
       double y0 = k[0] * u[0] + k[1] * u[1];
