@@ -246,6 +246,28 @@ __device__ long long assign_anchor(const double* x, int d, const Side64& s) {
 
 // mode 0: accumulate counts + step statistics (accumulate_chunk / run_accumulate)
 // mode 1: write exit points, steps, components (walk_exits_chunk / run_exits)
+constexpr int kWarps64 = 8;  // 256-thread blocks
+
+struct ExitQueue64 {
+  double x[64][3];
+  long long steps[64];
+  int pole[64];
+};
+
+// Bin one exit exactly as S/_kernel.pyx:445-464 (owner -> side -> anchor) and
+// count it; the step statistics go to this lane's per-pole accumulator.
+__device__ __forceinline__ void retire64(const Ref64Params& P, const double* xq, int pole,
+                                         long long steps, StepAcc& acc) {
+  const WorkOut& W = P.w;
+  double x[3] = {xq[0], xq[1], xq[2]};
+  const int comp = owner_component(P, x);
+  const int side = P.comp_side[comp];
+  const long long winner = assign_anchor(x, P.d, P.side[side]);
+  const long long col = side ? W.col_off1 + winner : winner;
+  atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+  acc_add(acc, W, pole, (unsigned long long)steps);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   const WorkOut& W = P.w;
@@ -260,6 +282,13 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   // its direction -- a lane whose Marsaglia trial was rejected stays at 1
   int phase = 0;
   double sd = 0.0;
+  // MODE 0: finished walks are queued per warp and binned 32 at a time with
+  // every lane active (binning one lane at a time would serialise the warp)
+  __shared__ ExitQueue64 q_all[kWarps64];
+  ExitQueue64& q = q_all[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int qn = 0;
   WarpPool wp;
   pool_init(wp);
   StepAcc acc;
@@ -279,28 +308,13 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
       }
       if (wp.exhausted && __ballot_sync(kFull, active) == 0) break;
     }
-    if (!active) continue;
     // S/_kernel.pyx:176-197, one direction trial per iteration
-    if (phase == 0) {
+    bool stop = false;
+    if (active && phase == 0) {
       sd = signed_dist(P, x);
       if (sd <= P.eps) {
-        active = false;
-        if (MODE == 0) {
-          const int comp = owner_component(P, x);
-          const int side = P.comp_side[comp];
-          const long long winner = assign_anchor(x, d, P.side[side]);
-          const long long col = side ? W.col_off1 + winner : winner;
-          atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
-          acc_add(acc, W, pole, (unsigned long long)steps);
-        } else {
-          const long long o = (long long)pole * W.n_rep + rep_off;
-          for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
-          W.steps_out[o] = steps;
-          W.comp_out[o] = owner_component(P, x);
-        }
-        continue;
-      }
-      if (steps >= P.max_steps) {
+        stop = true;
+      } else if (steps >= P.max_steps) {
         active = false;
         atomicMax(W.err_key, ~(unsigned long long)((long long)pole * W.n_rep + rep_off));
         if (MODE == 1) {
@@ -309,11 +323,36 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
           W.steps_out[o] = steps;
           W.comp_out[o] = 0;
         }
-        continue;
+      } else {
+        phase = 1;
       }
-      phase = 1;
     }
-    if (!direction_trial(d, P.seed, draw, rep, pid, u)) continue;
+    if (MODE == 0) {
+      const unsigned sm = __ballot_sync(kFull, stop);
+      if (sm) {
+        if (stop) {
+          const int slot = qn + __popc(sm & lt);
+          for (int j = 0; j < 3; ++j) q.x[slot][j] = j < d ? x[j] : 0.0;
+          q.pole[slot] = pole;
+          q.steps[slot] = steps;
+        }
+        qn += __popc(sm);
+        if (qn >= 32) {
+          __syncwarp();
+          const int slot = qn - 32 + lane;
+          retire64(P, q.x[slot], q.pole[slot], q.steps[slot], acc);
+          qn -= 32;
+          __syncwarp();
+        }
+      }
+    } else if (stop) {
+      const long long o = (long long)pole * W.n_rep + rep_off;
+      for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
+      W.steps_out[o] = steps;
+      W.comp_out[o] = owner_component(P, x);
+    }
+    if (stop) active = false;
+    if (!active || !direction_trial(d, P.seed, draw, rep, pid, u)) continue;
     phase = 0;
     const double* k = P.ks;
     if (d == 2) {
@@ -332,6 +371,8 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     steps = steps + 1;
   }
   if (MODE == 0) {
+    __syncwarp();
+    if (lane < qn) retire64(P, q.x[lane], q.pole[lane], q.steps[lane], acc);
     acc_flush(acc, W);
     stats_smem_flush(W);
   }
