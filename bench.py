@@ -47,11 +47,17 @@ F_STEP = {
     # (cfg, chain): (fp32 ops, xu ops) -- DESIGN.md "F_step of the implemented
     # kernels" derives each entry term by term from walk_f32.cu
     (1, "woe"): (11, 3), (1, "max"): (11, 3),   # K = I: both chains are the sphere step
-    (2, "woe"): (15, 2), (2, "max"): (17, 2),
-    (3, "woe"): (21, 4), (3, "max"): (38, 7),    # concentric hole: shared |v|, |Av|, one rcp
-    (4, "woe"): (28, 4), (4, "max"): (41, 6),
+    (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
+    (3, "woe"): (19, 4), (3, "max"): (34, 7),    # concentric hole: shared |v|, |Av|, one rcp
+    (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (5, "woe"): (36, 4), (5, "max"): (46, 4),
 }
+
+# the reference chain's FP32 ops per step (same counting
+# convention) and its measured steps per walk.  walks/s x F x steps is the
+# FP32 work the REFERENCE algorithm would have to issue to match our walks/s
+# (cfg5 has no reference path: the numpy WoE restatement's ~81 steps).
+F_REF = {1: (23.2, 12.6), 2: (25.2, 45.3), 3: (28.2, 59.5), 4: (33.9, 72.4), 5: (42.9, 81.0)}
 
 
 class ClockSampler:
@@ -366,7 +372,7 @@ def run_ours(args):
     if rank == 0:
         sub_ids = ids
         e2e_times = []
-        for i in range(max(2, min(args.steps, 5))):
+        for i in range(max(3, min(args.steps, 11))):
             t0 = time.perf_counter()
             r = backend.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles[sub_ids], cfg.seed,
                                        cfg.eps, 10**6, cfg.n_rep, s0, s1,
@@ -425,7 +431,13 @@ def run_ours(args):
                          "peak_measured_ffma": peak_ffma,
                          "frac_of_measured_ffma": achieved / peak_ffma,
                          "frac_at_max_clock": achieved / (info["sm_count"] * 128 *
-                                                          (clocks["sm_max_mhz"] or 1965) * 1e-6)},
+                                                          (clocks["sm_max_mhz"] or 1965) * 1e-6),
+                         "reference_chain_equivalent": {
+                             "frac": (value / world) * F_REF[cfg.index][0] * F_REF[cfg.index][1]
+                                     / (peak_nominal * 1e12),
+                             "note": "walks/s x the reference chain's FP32 ops/step x its "
+                                     "steps/walk (SURVEY 8d) / peak: the FP32 issue share the "
+                                     "reference algorithm would need for the same walks/s"}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "walks/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

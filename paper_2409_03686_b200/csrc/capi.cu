@@ -279,6 +279,45 @@ int sm_count_of(int dev) {
 }
 
 // smallest eigenvalue of a symmetric 2x2 / 3x3 matrix (Jacobi sweeps)
+// Cyclic Jacobi eigendecomposition of a symmetric d x d matrix (d <= 3):
+// eigenvalues in lam, eigenvectors as the COLUMNS of v (a = v diag(lam) v^T).
+static void sym_eig(const double* a_in, int d, double lam[3], double v[3][3]) {
+  double a[3][3] = {{0}};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) v[i][j] = i == j ? 1.0 : 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) a[i][j] = a_in[i * d + j];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) off += a[p][q] * a[p][q];
+    if (off < 1e-32) break;
+    for (int p = 0; p < d; ++p)
+      for (int q = p + 1; q < d; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < d; ++k) {
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < d; ++k) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < d; ++k) {
+          const double vkp = v[k][p], vkq = v[k][q];
+          v[k][p] = c * vkp - s * vkq;
+          v[k][q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 3; ++i) lam[i] = i < d ? a[i][i] : 0.0;
+}
+
 double sym_min_eig(const double* a_in, int d) {
   double a[3][3] = {{0}};
   for (int i = 0; i < d; ++i)
@@ -576,11 +615,48 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       scale = std::max(scale, gf[d]);
     }
     for (int j = 0; j < 3; ++j) P.frame[j] = (float)frame[j];
+    // Ball domains: rotate the frame onto the eigenbasis of A = K^{1/2}
+    // (A = Q diag(Ad) Q^T).  2D box on the max chain: sheared axes (see
+    // F32Params::phase).  Both are exact reformulations of the same step.
+    double Qd[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+    double Adiag[3] = {1.0, 1.0, 1.0};
+    P.rot = (g->gi[1] == 0 && nn == 0 && !ident) ? 1 : 0;
+    P.phase = (d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0 && o.chain == EM_CHAIN_MAX && !ident) ? 1 : 0;
+    if (P.rot) sym_eig(g->ksqrt, d, Adiag, Qd);
+    for (int i = 0; i < 3; ++i) {
+      P.Ad[i] = (float)Adiag[i];
+      P.Kd[i] = (float)(Adiag[i] * Adiag[i]);
+      for (int j = 0; j < 3; ++j) P.Q[3 * i + j] = (float)Qd[i][j];
+    }
+    double axd[3] = {1.0, 1.0, 1.0};
+    if (P.phase) {
+      const double* A = g->ksqrt;  // 2 x 2, symmetric
+      const double R0 = std::hypot(A[0], A[1]), R1 = std::hypot(A[2], A[3]);
+      const double dD = std::atan2(A[3], A[2]) - std::atan2(A[1], A[0]);
+      axd[0] = R0;
+      axd[1] = R1 * std::sin(dD);
+      P.shk = (float)(std::cos(dD) / std::sin(dD));
+    }
+    for (int i = 0; i < 3; ++i) P.ax[i] = (float)axd[i];
+    // world point -> kernel coordinates
+    auto to_kernel = [&](const double* w, float* out) {
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int j = 0; j < d; ++j) v[j] = w[j] - frame[j];
+      for (int j = 0; j < d; ++j) {
+        double t = 0.0;
+        if (P.rot) {
+          for (int i = 0; i < d; ++i) t += Qd[i][j] * v[i];
+        } else {
+          t = v[j] / axd[j];
+        }
+        out[j] = (float)t;
+      }
+    };
     P.concentric = (g->gi[1] == 0 && nh > 0) ? 1 : 0;
     for (int h = 0; h < nh; ++h) {
       const int off = d + 1 + h * (d + 1);
+      to_kernel(gf + off, P.hc[h]);
       for (int j = 0; j < d; ++j) {
-        P.hc[h][j] = (float)(gf[off + j] - frame[j]);
         if (gf[off + j] != gf[j]) P.concentric = 0;
       }
       P.hr[h] = (float)gf[off + d];
@@ -643,11 +719,40 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     P.keep = 1.0f - P.shrink_rel;
     for (int i = 0; i < 3; ++i)  // rounded down: the folded margin is never smaller
       P.gk[i] = std::nextafter((float)((double)P.g[i] * (double)P.keep), 0.0f);
+    if (P.phase) {
+      // sheared box: kernel box [-bs_i, bs_i]; face i within eps <=> s_i =
+      // sb_i - |xs_i| <= 0 with sb_i = bs_i - eps / |ax_i|; bound r_i = m_i /
+      // R_i = g_i (s_i + (bs_i - sb_i)) with g_0 = 1, g_1 = |sin D|, shrunk
+      // by keep and by an absolute margin of a few ulps of the kernel box
+      const double gax[2] = {1.0, std::fabs(axd[1]) / std::hypot(g->ksqrt[2], g->ksqrt[3])};
+      double bsmax = 1.0;
+      float sbmin = 0.0f;
+      for (int i = 0; i < 2; ++i) {
+        const float bs = (float)(gf[d] / std::fabs(axd[i]));
+        bsmax = std::max(bsmax, (double)bs);
+        P.sb[i] = (float)((double)bs - eps / std::fabs(axd[i]));
+        sbmin = i == 0 ? P.sb[i] : std::min(sbmin, P.sb[i]);
+      }
+      const double sa = bsmax * 1.1920928955078125e-07;
+      for (int i = 0; i < 2; ++i) {
+        const float bs = (float)(gf[d] / std::fabs(axd[i]));
+        const double gk = gax[i] * (double)P.keep;
+        P.sg[i] = std::nextafter((float)gk, 0.0f);
+        const double off = gk * ((double)bs - (double)P.sb[i]) - gax[i] * sa;
+        float c = (float)off;
+        if ((double)c > off) c = std::nextafter(c, -1.0f);
+        P.sc[i] = c;
+      }
+      // every positive s is >= ulp(sb_min) / 2 (Sterbenz near sb, larger
+      // below): a power-of-two scale 2^k >= 2 / ulp(sb_min) maps it to >= 1
+      int ex = 0;
+      std::frexp((double)sbmin, &ex);  // sb in [2^(ex-1), 2^ex), ulp = 2^(ex-24)
+      P.ss_scale = std::ldexp(1.0f, 25 - ex + 1);
+    }
     P.one_bits = 0x3f800000u;
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);
     std::vector<float> pf(n_poles * 4, 0.0f);
-    for (int64_t i = 0; i < n_poles; ++i)
-      for (int j = 0; j < d; ++j) pf[i * 4 + j] = (float)(poles[i * d + j] - frame[j]);
+    for (int64_t i = 0; i < n_poles; ++i) to_kernel(poles + i * d, &pf[i * 4]);
     put(pf.data(), (size_t)n_poles * 16, (void**)&P.poles);
     for (int s = 0; s < 2; ++s) {
       const em_side* S = sides[s];

@@ -90,6 +90,28 @@ struct F32Params {
   float hr2[EM_MAX_HOLES];                      // hole radii squared
   float notch[2];                               // notch corner in the frame
   signed char comp_side[kMaxComp];
+  // Ball domains (rot = 1): the frame is also rotated onto the eigenbasis of
+  // A = K^{1/2} (A = Q diag(Ad) Q^T, world = frame + Q x).  Balls are
+  // rotation invariant and a uniform direction stays uniform, so the step is
+  // y = diag(Ad) u and |Av|^2 = sum Kd_i v_i^2 (3D: 11 -> 5 ops for y, 9 -> 4
+  // for the quadratic form).
+  int rot;
+  float Q[9];       // row-major 3x3 (d x d block used)
+  float Ad[3], Kd[3];
+  // 2D box on the max chain (phase = 1): with c, s = cos, sin of the step
+  // angle phi and rows a_i = R_i (cos d_i, sin d_i) of A, a uniform direction
+  // is y_0 = R_0 cos(phi), y_1 = R_1 cos(phi - D) after the shift phi = theta
+  // - d_0 (D = d_1 - d_0).  The kernel stores xs_0 = x_0 / R_0 and xs_1 =
+  // x_1 / (R_1 sin D), so a step is xs_0 += r c, xs_1 += r (k c + s) with
+  // k = cot D: 3 FFMAs instead of the 2x2 product and 2 updates (6 ops).
+  // The face bound of axis i is r_i = m_i / R_i = g_i * (scaled distance).
+  int phase;
+  float ax[3];      // frame coordinate = ax_i * kernel coordinate (R_0, R_1 sin D)
+  float sb[3];      // stop thresholds: s_i = sb_i - |xs_i| <= 0  <=>  face distance <= eps
+  float sg[3];      // bound gain (keep folded in, rounded down): r_i = s_i sg_i + sc_i
+  float sc[3];      // bound offset (rounded down)
+  float shk;        // k = cot D
+  float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major
   float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v
   float g[3];       // 1/|A e_i|: face-plane gain of the maximal ellipsoid

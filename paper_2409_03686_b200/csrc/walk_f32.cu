@@ -67,6 +67,28 @@ __device__ __forceinline__ float quad_K(const F32Params& P, float v0, float v1, 
   return fmaf(v2, q[2] * v2, fmaf(v1, t1, v0 * t0));
 }
 
+// |v|^2 and |Av|^2 of an offset v.  In the rotated ball frame (DIAG, A =
+// diag(Ad)) both come from the three squares: 3D 8 ops instead of 12.
+template <int D, bool DIAG>
+__device__ __forceinline__ void norm_quad(const F32Params& P, float v0, float v1, float v2,
+                                          float& s2, float& aa) {
+  if (DIAG) {
+    const float p0 = v0 * v0, p1 = v1 * v1;
+    if (D == 2) {
+      s2 = p0 + p1;
+      aa = fmaf(P.Kd[0], p0, P.Kd[1] * p1);
+    } else {
+      const float p2 = v2 * v2;
+      s2 = p0 + p1 + p2;
+      aa = fmaf(P.Kd[0], p0, fmaf(P.Kd[1], p1, P.Kd[2] * p2));
+    }
+    return;
+  }
+  s2 = v0 * v0 + v1 * v1;
+  if (D == 3) s2 = fmaf(v2, v2, s2);
+  aa = quad_K<D>(P, v0, v1, v2);
+}
+
 template <int NH>
 __device__ __forceinline__ int n_holes(const F32Params& P) {
   return NH >= 0 ? NH : P.n_holes;
@@ -78,6 +100,7 @@ template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, float& e, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
+  constexpr bool DIAG = OUTER == OUTER_BALL && !IDENT;  // rotated ball frame
   if (OUTER == OUTER_BALL && NH == 1 && MAXC && P.concentric) {
     // annulus / spherical shell: one |v| and one |Av| serve both bounds, and
     //   r = min(q_o / D_o, max(q_h / D_h, e_h)) = min(q_o / D_o, n_h / D_h)
@@ -85,13 +108,12 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     // single reciprocal replaces two divisions (XU-bound step: 10 -> 7 MUFU)
     const float v0 = x[0], v1 = x[1];
     const float v2 = D == 3 ? x[2] : 0.0f;
-    float s2 = v0 * v0 + v1 * v1;
-    if (D == 3) s2 = fmaf(v2, v2, s2);
+    float s2, aa;  // |v|^2, |Av|^2
+    norm_quad<D, DIAG>(P, v0, v1, v2, s2, aa);
     const float s = fsqrt(s2);
     const float rho = P.hr[0];
     const float eo = P.oR - s, eh = s - rho;
     e = fminf(eo, eh);
-    const float aa = quad_K<D>(P, v0, v1, v2);  // |Av|^2
     const float a = fsqrt(aa);
     const float qo = P.oR2 - s2;  // R^2 - |v|^2
     const float Do = a + fsqrt(fmaxf(aa + qo, 0.0f));
@@ -106,8 +128,13 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     // kernel frame: the outer ball is centred at the origin
     const float v0 = x[0], v1 = x[1];
     const float v2 = D == 3 ? x[2] : 0.0f;
-    float s2 = v0 * v0 + v1 * v1;
-    if (D == 3) s2 = fmaf(v2, v2, s2);
+    float s2, aa = 0.0f;  // |x|^2, |Ax|^2
+    if (MAXC) {
+      norm_quad<D, DIAG>(P, v0, v1, v2, s2, aa);
+    } else {
+      s2 = v0 * v0 + v1 * v1;
+      if (D == 3) s2 = fmaf(v2, v2, s2);
+    }
     if (MAXC && NH == 0) {
       // stop test on |x|^2 itself (no |x| needed): e > eps <=> |x|^2 <
       // (R - eps)^2, returned already as the FFMA.SAT stop margin (see dist)
@@ -117,7 +144,6 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
     }
     if (MAXC) {
       // |x + rAu|^2 <= s^2 + 2 r |Av| + r^2 <= R^2  =>  r <= q / (a + sqrt(a^2 + q))
-      const float aa = quad_K<D>(P, v0, v1, v2);  // |Av|^2
       const float q = P.oR2 - s2;  // R^2 - |x|^2
       r = fdiv(q, fsqrt(aa) + fsqrt(fmaxf(aa + q, 0.0f)));
     } else {
@@ -159,15 +185,19 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
   for (int h = 0; h < nh; ++h) {
     const float v0 = x[0] - P.hc[h][0], v1 = x[1] - P.hc[h][1];
     const float v2 = D == 3 ? x[2] - P.hc[h][2] : 0.0f;
-    float s2 = v0 * v0 + v1 * v1;
-    if (D == 3) s2 = fmaf(v2, v2, s2);
+    float s2, aa = 0.0f;  // |v|^2, |Av|^2
+    if (MAXC) {
+      norm_quad<D, DIAG>(P, v0, v1, v2, s2, aa);
+    } else {
+      s2 = v0 * v0 + v1 * v1;
+      if (D == 3) s2 = fmaf(v2, v2, s2);
+    }
     const float s = fsqrt(s2);
     const float rho = P.hr[h];
     const float eh = s - rho;
     e = fminf(e, eh);
     if (MAXC) {
       // min_u |v + rAu|^2 >= s^2 - 2 r |Av| + r^2 m^2 >= rho^2
-      const float aa = quad_K<D>(P, v0, v1, v2);  // |Av|^2
       const float q = s2 - P.hr2[h];  // |v|^2 - rho^2
       const float rh = fdiv(q, fsqrt(aa) + fsqrt(fmaxf(fmaf(-P.m2, q, aa), 0.0f)));
       r = fminf(r, fmaxf(rh, eh));
@@ -184,11 +214,28 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
 // The first output is the stop margin t: t <= 0 exactly when e <= eps, and
 // t >= 1 otherwise (t = (e - eps) 2^k by one FFMA, or the ball's |x|^2 form),
 // so __saturatef(t) is the lane's 0/1 walking mask.
+// The 2D box on the max chain keeps its axes scaled by |row i of A| (see
+// F32Params::phase): the stop test and both face bounds come from the two
+// scaled face distances s_i = sb_i - |xs_i| directly.
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+struct Phase {
+  static constexpr bool value =
+      D == 2 && OUTER == OUTER_BOX && NH == 0 && CHAIN == EM_CHAIN_MAX && !IDENT;
+};
+
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& t, float& r) {
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
   constexpr bool S2STOP = MAXC && OUTER == OUTER_BALL && NH == 0;
+  if (Phase<D, OUTER, NH, CHAIN, IDENT>::value) {
+    // s_i <= 0 exactly when face i is within eps; any positive s_i scales to
+    // >= 1 (ss_scale), so sat(t) is the 0/1 walking mask
+    const float s0 = P.sb[0] - fabsf(x[0]), s1 = P.sb[1] - fabsf(x[1]);
+    t = fminf(s0, s1) * P.ss_scale;
+    r = fminf(fmaf(s0, P.sg[0], P.sc[0]), fmaf(s1, P.sg[1], P.sc[1]));
+    return;
+  }
   float e;
   dist_raw<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
   t = S2STOP ? e : fmaf(e, P.stop_scale, P.stop_bias);
@@ -479,10 +526,30 @@ __device__ __forceinline__ float angle_of(unsigned fbits) {
   return fmaf(__uint_as_float(fbits), kAngScale, kAngBias);
 }
 
-template <int D, bool IDENT>
+template <int D, int OUTER, bool IDENT, bool PHASE>
 __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, float z,
                                      unsigned afbits) {
+  constexpr bool DIAG = OUTER == OUTER_BALL && !IDENT;
+  if (PHASE) {
+    // sheared axes (F32Params::phase): xs_0 += r c, xs_1 += r (k c + s)
+    float sn, cs;
+    __sincosf(angle_of(afbits), &sn, &cs);
+    x[0] = fmaf(rs, cs, x[0]);
+    x[1] = fmaf(rs, fmaf(P.shk, cs, sn), x[1]);
+    return;
+  }
   float u0, u1, u2 = 0.0f;
+  if (D == 3 && DIAG) {
+    // rotated ball frame: y = diag(Ad) u, the axis gains folded into rho
+    const float th = angle_of(afbits);
+    const float rho = fsqrt(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+    float sn, cs;
+    __sincosf(th, &sn, &cs);
+    x[0] = fmaf(rs, (P.Ad[0] * rho) * cs, x[0]);
+    x[1] = fmaf(rs, (P.Ad[1] * rho) * sn, x[1]);
+    x[2] = fmaf(rs, P.Ad[2] * z, x[2]);
+    return;
+  }
   if (D == 2) {
     __sincosf(angle_of(afbits), &u1, &u0);
   } else {
@@ -495,7 +562,10 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, flo
     u2 = z;
   }
   float y0 = u0, y1 = u1, y2 = u2;
-  if (!IDENT) {
+  if (DIAG) {
+    y0 = P.Ad[0] * u0;
+    y1 = P.Ad[1] * u1;
+  } else if (!IDENT) {
     if (D == 2) {
       y0 = fmaf(P.A[0], u0, P.A[1] * u1);
       y1 = fmaf(P.A[2], u0, P.A[3] * u1);
@@ -515,14 +585,44 @@ constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
 
 // Bin one exit (owner component -> side -> nearest anchor), count it, and
 // add its step count to this lane's per-pole accumulator.
-template <int D, int OUTER, int NH, int BINK, int SMEM>
+// Kernel coordinates -> world coordinates: undo the rotated ball frame /
+// the scaled box axes, then the origin shift.
+template <int D, int OUTER, bool PHASE>
+__device__ __forceinline__ void to_world(const F32Params& P, const float* x, float* xw) {
+  if (OUTER == OUTER_BALL) {
+    if (P.rot) {
+      const float* Q = P.Q;
+      if (D == 2) {
+        xw[0] = fmaf(Q[0], x[0], fmaf(Q[1], x[1], P.frame[0]));
+        xw[1] = fmaf(Q[3], x[0], fmaf(Q[4], x[1], P.frame[1]));
+        xw[2] = 0.0f;
+      } else {
+        xw[0] = fmaf(Q[0], x[0], fmaf(Q[1], x[1], fmaf(Q[2], x[2], P.frame[0])));
+        xw[1] = fmaf(Q[3], x[0], fmaf(Q[4], x[1], fmaf(Q[5], x[2], P.frame[1])));
+        xw[2] = fmaf(Q[6], x[0], fmaf(Q[7], x[1], fmaf(Q[8], x[2], P.frame[2])));
+      }
+      return;
+    }
+  } else if (PHASE) {
+    xw[0] = fmaf(P.ax[0], x[0], P.frame[0]);
+    xw[1] = fmaf(P.ax[1], x[1], P.frame[1]);
+    xw[2] = 0.0f;
+    return;
+  }
+  xw[0] = x[0] + P.frame[0];
+  xw[1] = x[1] + P.frame[1];
+  xw[2] = D == 3 ? x[2] + P.frame[2] : 0.0f;
+}
+
+template <int D, int OUTER, int NH, int BINK, int SMEM, bool PHASE>
 __device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
                                        StepAcc& acc) {
   const WorkOut& W = P.w;
   int side;
   if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
   else side = P.comp_side[0];
-  const float xw[3] = {x[0] + P.frame[0], x[1] + P.frame[1], D == 3 ? x[2] + P.frame[2] : 0.0f};
+  float xw[3];
+  to_world<D, OUTER, PHASE>(P, x, xw);
   const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
@@ -548,6 +648,7 @@ struct ExitQueue {
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
 __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
+  constexpr bool PHASE = Phase<D, OUTER, NH, CHAIN, IDENT>::value;
   __shared__ ExitQueue q_all[kWarps];
   // lane id, lane mask and the queue's shared-window address are made opaque
   // (empty asm) so the compiler keeps them in registers instead of
@@ -604,14 +705,23 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
                          : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qb + kQueue * 16u + slot * 4u)
                          : "memory");
-            retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(pw), es, acc);
+            retire<D, OUTER, NH, BINK, SMEM, PHASE>(P, ex, __float_as_int(pw), es, acc);
             qn -= 32;
             __syncwarp();
           }
         }
       } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
-        for (int j = 0; j < D; ++j) W.x_out[o * D + j] = (double)x[j] + (double)P.frame[j];
+        double xd[3] = {(double)x[0], (double)x[1], D == 3 ? (double)x[2] : 0.0};
+        if (OUTER == OUTER_BALL && P.rot) {
+          double t[3] = {0.0, 0.0, 0.0};
+          for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) t[i] += (double)P.Q[3 * i + j] * xd[j];
+          for (int i = 0; i < D; ++i) xd[i] = t[i];
+        } else if (PHASE) {
+          for (int i = 0; i < D; ++i) xd[i] *= (double)P.ax[i];
+        }
+        for (int j = 0; j < D; ++j) W.x_out[o * D + j] = xd[j] + (double)P.frame[j];
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, x);
       }
@@ -662,8 +772,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
         float t, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         wm = __saturatef(t);
-        step<D, IDENT>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
-                       angle_bits<D>(wv, k, P.one_bits));
+        step<D, OUTER, IDENT, PHASE>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                                     angle_bits<D>(wv, k, P.one_bits));
         sf += wm;
       }
       walking = wm != 0.0f;
@@ -679,8 +789,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
         const float rs = walking ? r : 0.0f;
-        step<D, IDENT>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
-                       angle_bits<D>(wv, k, P.one_bits));
+        step<D, OUTER, IDENT, PHASE>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                                     angle_bits<D>(wv, k, P.one_bits));
         steps += walking;
       }
       // budget overruns: report (smallest key wins), drop from the live set
@@ -701,7 +811,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       const ExitQueue& q = q_all[threadIdx.x >> 5];
       const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM>(P, ex, __float_as_int(e.w), q.s[lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM, PHASE>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
     acc_flush<SMEM>(acc, W);
     stats_smem_flush<SMEM>(W);
@@ -794,9 +904,19 @@ __global__ void bin_points_f32_kernel(const F32Params P, const double* pts, long
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= n) return;
   float xf[3] = {0.0f, 0.0f, 0.0f}, xw[3] = {0.0f, 0.0f, 0.0f};
+  double v[3] = {0.0, 0.0, 0.0};
   for (int k = 0; k < D; ++k) {
     xw[k] = (float)pts[j * D + k];
-    xf[k] = (float)(pts[j * D + k] - (double)P.frame[k]);
+    v[k] = pts[j * D + k] - (double)P.frame[k];
+  }
+  if (OUTER == OUTER_BALL && P.rot) {  // Q^T v: the frame the hole centres live in
+    for (int k = 0; k < D; ++k) {
+      double t = 0.0;
+      for (int i = 0; i < D; ++i) t += (double)P.Q[3 * i + k] * v[i];
+      xf[k] = (float)t;
+    }
+  } else {
+    for (int k = 0; k < D; ++k) xf[k] = (float)v[k];
   }
   const int comp = f32::owner<D, OUTER, -1>(P, xf);
   const int side = P.comp_side[comp];
