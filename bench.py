@@ -50,7 +50,7 @@ F_STEP = {
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
     (3, "woe"): (19, 4), (3, "max"): (34, 7),    # concentric hole: shared |v|, |Av|, one rcp
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
-    (5, "woe"): (36, 4), (5, "max"): (46, 4),
+    (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
 }
 
 # the reference chain's FP32 ops per step (same counting

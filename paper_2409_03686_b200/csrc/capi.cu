@@ -616,26 +616,58 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     }
     for (int j = 0; j < 3; ++j) P.frame[j] = (float)frame[j];
     // Ball domains: rotate the frame onto the eigenbasis of A = K^{1/2}
-    // (A = Q diag(Ad) Q^T).  2D box on the max chain: sheared axes (see
-    // F32Params::phase).  Both are exact reformulations of the same step.
+    // (A = Q diag(Ad) Q^T).  Box / L-box on the max chain: sheared axes (see
+    // F32Params::shear).  Both are exact reformulations of the same step.
     double Qd[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
     double Adiag[3] = {1.0, 1.0, 1.0};
     P.rot = (g->gi[1] == 0 && nn == 0 && !ident) ? 1 : 0;
-    P.phase = (d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0 && o.chain == EM_CHAIN_MAX && !ident) ? 1 : 0;
+    P.shear = (g->gi[1] == 1 && nh == 0 && o.chain == EM_CHAIN_MAX && !ident && (d == 3 || nn == 0)) ? 1 : 0;
     if (P.rot) sym_eig(g->ksqrt, d, Adiag, Qd);
     for (int i = 0; i < 3; ++i) {
       P.Ad[i] = (float)Adiag[i];
       P.Kd[i] = (float)(Adiag[i] * Adiag[i]);
       for (int j = 0; j < 3; ++j) P.Q[3 * i + j] = (float)Qd[i][j];
     }
-    double axd[3] = {1.0, 1.0, 1.0};
-    if (P.phase) {
-      const double* A = g->ksqrt;  // 2 x 2, symmetric
-      const double R0 = std::hypot(A[0], A[1]), R1 = std::hypot(A[2], A[3]);
-      const double dD = std::atan2(A[3], A[2]) - std::atan2(A[1], A[0]);
-      axd[0] = R0;
-      axd[1] = R1 * std::sin(dD);
-      P.shk = (float)(std::cos(dD) / std::sin(dD));
+    double axd[3] = {1.0, 1.0, 1.0}, shear_g[3] = {1.0, 1.0, 1.0};
+    if (P.shear) {
+      const double* A = g->ksqrt;  // d x d, symmetric, rows a_i
+      double Rn[3] = {0.0, 0.0, 0.0}, ah[3][3] = {{0.0}};
+      for (int i = 0; i < d; ++i) {
+        for (int j = 0; j < d; ++j) Rn[i] += A[i * d + j] * A[i * d + j];
+        Rn[i] = std::sqrt(Rn[i]);
+        for (int j = 0; j < d; ++j) ah[i][j] = A[i * d + j] / Rn[i];
+      }
+      if (d == 2) {
+        // u = (c, s) in the frame where a_0 = R_0 e1: a_1 = R_1 (cos D, sin D)
+        const double dD = std::atan2(ah[1][1], ah[1][0]) - std::atan2(ah[0][1], ah[0][0]);
+        axd[0] = Rn[0];
+        axd[1] = Rn[1] * std::sin(dD);
+        P.shk[0] = (float)(std::cos(dD) / std::sin(dD));
+      } else {
+        // e3 = a_0 / R_0, e1 = the unit part of a_1 orthogonal to e3, e2 = e3 x e1
+        double e1[3], e2[3], e3[3];
+        for (int j = 0; j < 3; ++j) e3[j] = ah[0][j];
+        const double cb = ah[1][0] * e3[0] + ah[1][1] * e3[1] + ah[1][2] * e3[2];
+        for (int j = 0; j < 3; ++j) e1[j] = ah[1][j] - cb * e3[j];
+        const double sbt = std::sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+        for (int j = 0; j < 3; ++j) e1[j] /= sbt;
+        e2[0] = e3[1] * e1[2] - e3[2] * e1[1];
+        e2[1] = e3[2] * e1[0] - e3[0] * e1[2];
+        e2[2] = e3[0] * e1[1] - e3[1] * e1[0];
+        double gm[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < 3; ++j) {
+          gm[0] += ah[2][j] * e1[j];
+          gm[1] += ah[2][j] * e2[j];
+          gm[2] += ah[2][j] * e3[j];
+        }
+        axd[0] = Rn[0];
+        axd[1] = Rn[1] * sbt;
+        axd[2] = Rn[2] * gm[1];
+        P.shk[0] = (float)(cb / sbt);
+        P.shk[1] = (float)(gm[0] / gm[1]);
+        P.shk[2] = (float)(gm[2] / gm[1]);
+      }
+      for (int i = 0; i < d; ++i) shear_g[i] = std::fabs(axd[i]) / Rn[i];
     }
     for (int i = 0; i < 3; ++i) P.ax[i] = (float)axd[i];
     // world point -> kernel coordinates
@@ -719,26 +751,25 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     P.keep = 1.0f - P.shrink_rel;
     for (int i = 0; i < 3; ++i)  // rounded down: the folded margin is never smaller
       P.gk[i] = std::nextafter((float)((double)P.g[i] * (double)P.keep), 0.0f);
-    if (P.phase) {
+    if (P.shear) {
       // sheared box: kernel box [-bs_i, bs_i]; face i within eps <=> s_i =
       // sb_i - |xs_i| <= 0 with sb_i = bs_i - eps / |ax_i|; bound r_i = m_i /
-      // R_i = g_i (s_i + (bs_i - sb_i)) with g_0 = 1, g_1 = |sin D|, shrunk
-      // by keep and by an absolute margin of a few ulps of the kernel box
-      const double gax[2] = {1.0, std::fabs(axd[1]) / std::hypot(g->ksqrt[2], g->ksqrt[3])};
+      // R_i = g_i (s_i + (bs_i - sb_i)), shrunk by keep and by an absolute
+      // margin of a few ulps of the kernel box
       double bsmax = 1.0;
       float sbmin = 0.0f;
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < d; ++i) {
         const float bs = (float)(gf[d] / std::fabs(axd[i]));
         bsmax = std::max(bsmax, (double)bs);
         P.sb[i] = (float)((double)bs - eps / std::fabs(axd[i]));
         sbmin = i == 0 ? P.sb[i] : std::min(sbmin, P.sb[i]);
       }
       const double sa = bsmax * 1.1920928955078125e-07;
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < d; ++i) {
         const float bs = (float)(gf[d] / std::fabs(axd[i]));
-        const double gk = gax[i] * (double)P.keep;
+        const double gk = shear_g[i] * (double)P.keep;
         P.sg[i] = std::nextafter((float)gk, 0.0f);
-        const double off = gk * ((double)bs - (double)P.sb[i]) - gax[i] * sa;
+        const double off = gk * ((double)bs - (double)P.sb[i]) - shear_g[i] * sa;
         float c = (float)off;
         if ((double)c > off) c = std::nextafter(c, -1.0f);
         P.sc[i] = c;

@@ -98,19 +98,23 @@ struct F32Params {
   int rot;
   float Q[9];       // row-major 3x3 (d x d block used)
   float Ad[3], Kd[3];
-  // 2D box on the max chain (phase = 1): with c, s = cos, sin of the step
-  // angle phi and rows a_i = R_i (cos d_i, sin d_i) of A, a uniform direction
-  // is y_0 = R_0 cos(phi), y_1 = R_1 cos(phi - D) after the shift phi = theta
-  // - d_0 (D = d_1 - d_0).  The kernel stores xs_0 = x_0 / R_0 and xs_1 =
-  // x_1 / (R_1 sin D), so a step is xs_0 += r c, xs_1 += r (k c + s) with
-  // k = cot D: 3 FFMAs instead of the 2x2 product and 2 updates (6 ops).
-  // The face bound of axis i is r_i = m_i / R_i = g_i * (scaled distance).
-  int phase;
-  float ax[3];      // frame coordinate = ax_i * kernel coordinate (R_0, R_1 sin D)
+  // Box / L-box on the max chain without holes (shear = 1): a uniform
+  // direction u is uniform in ANY orthonormal frame, so it is drawn in the
+  // frame (e1, e2, e3) where row a_0 of A is R_0 e3 and row a_1 lies in the
+  // (e1, e3) plane (2D: u = (c, s) with a_0 = R_0 e1).  With the axes stored
+  // sheared, xs_i = x_i / ax_i, the step x += r A u becomes
+  //   2D: xs_0 += r c,  xs_1 += r (k c + s)                       (3 FFMA)
+  //   3D: xs_0 += r z,  xs_1 += r (rc + k1 z),
+  //       xs_2 += r (rs + k2 rc + k3 z)    (rc, rs = rho cos, rho sin; 8 ops)
+  // instead of the d x d product and d updates (2D 6 ops, 3D 14).  The face
+  // bound of axis i is r_i = m_i / R_i = g_i * (sheared distance), g_i =
+  // |ax_i| / R_i; the notch (world axes) keeps its world-unit bounds.
+  int shear;
+  float ax[3];      // frame coordinate = ax_i * kernel coordinate
   float sb[3];      // stop thresholds: s_i = sb_i - |xs_i| <= 0  <=>  face distance <= eps
   float sg[3];      // bound gain (keep folded in, rounded down): r_i = s_i sg_i + sc_i
   float sc[3];      // bound offset (rounded down)
-  float shk;        // k = cot D
+  float shk[3];     // 2D: k = cot(d_1 - d_0); 3D: k1, k2, k3
   float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major
   float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v

@@ -211,16 +211,17 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
 // FP32 safety margin: r = r_exact * keep - shrink_abs.  Box faces fold the
 // margin into their gain (one FFMA per face instead of an FMUL per face plus
 // a final FFMA); every other shape applies it once at the end.
-// The first output is the stop margin t: t <= 0 exactly when e <= eps, and
-// t >= 1 otherwise (t = (e - eps) 2^k by one FFMA, or the ball's |x|^2 form),
-// so __saturatef(t) is the lane's 0/1 walking mask.
-// The 2D box on the max chain keeps its axes scaled by |row i of A| (see
-// F32Params::phase): the stop test and both face bounds come from the two
-// scaled face distances s_i = sb_i - |xs_i| directly.
+// The first output is the lane's 0/1 walking mask t = sat(m): the stop
+// margin m is <= 0 exactly when e <= eps and >= 1 otherwise (m = (e - eps)
+// 2^k by one FFMA, or the ball's |x|^2 form), so the saturation folds into
+// the instruction that computes m.
+// Box / L-box on the max chain without holes keeps its axes sheared (see
+// F32Params::shear): the stop test and the face bounds come from the sheared
+// face distances s_i = sb_i - |xs_i| directly.
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
-struct Phase {
-  static constexpr bool value =
-      D == 2 && OUTER == OUTER_BOX && NH == 0 && CHAIN == EM_CHAIN_MAX && !IDENT;
+struct Shear {
+  static constexpr bool value = OUTER != OUTER_BALL && NH == 0 && CHAIN == EM_CHAIN_MAX &&
+                                !IDENT && (D == 3 || OUTER == OUTER_BOX);
 };
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
@@ -228,17 +229,30 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
   constexpr bool S2STOP = MAXC && OUTER == OUTER_BALL && NH == 0;
-  if (Phase<D, OUTER, NH, CHAIN, IDENT>::value) {
+  if (Shear<D, OUTER, NH, CHAIN, IDENT>::value) {
     // s_i <= 0 exactly when face i is within eps; any positive s_i scales to
     // >= 1 (ss_scale), so sat(t) is the 0/1 walking mask
     const float s0 = P.sb[0] - fabsf(x[0]), s1 = P.sb[1] - fabsf(x[1]);
-    t = fminf(s0, s1) * P.ss_scale;
+    const float s2 = D == 3 ? P.sb[2] - fabsf(x[2]) : kInf;
     r = fminf(fmaf(s0, P.sg[0], P.sc[0]), fmaf(s1, P.sg[1], P.sc[1]));
+    if (D == 3) r = fminf(r, fmaf(s2, P.sg[2], P.sc[2]));
+    if (OUTER == OUTER_LBOX) {
+      // notch prism in world units (corner offsets from the frame axes)
+      const float qx = fmaf(-P.ax[0], x[0], P.notch[0]), qy = fmaf(-P.ax[1], x[1], P.notch[1]);
+      const float nx = fmaxf(qx, 0.0f), ny = fmaxf(qy, 0.0f);
+      const float en = fsqrt(fmaf(nx, nx, ny * ny));
+      t = fminf(__saturatef(fminf(fminf(s0, s1), s2) * P.ss_scale),
+                __saturatef(fmaf(en, P.stop_scale, P.stop_bias)));
+      r = fminf(r, fmaxf(fmaf(en, P.keep, -P.shrink_abs),
+                         fmaxf(fmaf(qx, P.gk[0], -P.shrink_abs), fmaf(qy, P.gk[1], -P.shrink_abs))));
+    } else {
+      t = __saturatef(fminf(fminf(s0, s1), s2) * P.ss_scale);
+    }
     return;
   }
   float e;
   dist_raw<D, OUTER, NH, CHAIN, IDENT>(P, x, e, r);
-  t = S2STOP ? e : fmaf(e, P.stop_scale, P.stop_bias);
+  t = __saturatef(S2STOP ? e : fmaf(e, P.stop_scale, P.stop_bias));
   if (!FOLD) r = fmaf(r, P.keep, -P.shrink_abs);
 }
 
@@ -526,16 +540,27 @@ __device__ __forceinline__ float angle_of(unsigned fbits) {
   return fmaf(__uint_as_float(fbits), kAngScale, kAngBias);
 }
 
-template <int D, int OUTER, bool IDENT, bool PHASE>
+template <int D, int OUTER, bool IDENT, bool SHEAR>
 __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, float z,
                                      unsigned afbits) {
   constexpr bool DIAG = OUTER == OUTER_BALL && !IDENT;
-  if (PHASE) {
-    // sheared axes (F32Params::phase): xs_0 += r c, xs_1 += r (k c + s)
-    float sn, cs;
-    __sincosf(angle_of(afbits), &sn, &cs);
-    x[0] = fmaf(rs, cs, x[0]);
-    x[1] = fmaf(rs, fmaf(P.shk, cs, sn), x[1]);
+  if (SHEAR) {
+    // sheared axes (F32Params::shear)
+    if (D == 2) {
+      float sn, cs;
+      __sincosf(angle_of(afbits), &sn, &cs);
+      x[0] = fmaf(rs, cs, x[0]);
+      x[1] = fmaf(rs, fmaf(P.shk[0], cs, sn), x[1]);
+    } else {
+      const float th = angle_of(afbits);
+      const float rho = fsqrt(fmaxf(fmaf(-z, z, 1.0f), 0.0f));
+      float sn, cs;
+      __sincosf(th, &sn, &cs);
+      const float rc = rho * cs, rsn = rho * sn;
+      x[0] = fmaf(rs, z, x[0]);
+      x[1] = fmaf(rs, fmaf(P.shk[0], z, rc), x[1]);
+      x[2] = fmaf(rs, fmaf(P.shk[1], rc, fmaf(P.shk[2], z, rsn)), x[2]);
+    }
     return;
   }
   float u0, u1, u2 = 0.0f;
@@ -585,44 +610,44 @@ constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
 
 // Bin one exit (owner component -> side -> nearest anchor), count it, and
 // add its step count to this lane's per-pole accumulator.
-// Kernel coordinates -> world coordinates: undo the rotated ball frame /
-// the scaled box axes, then the origin shift.
-template <int D, int OUTER, bool PHASE>
-__device__ __forceinline__ void to_world(const F32Params& P, const float* x, float* xw) {
-  if (OUTER == OUTER_BALL) {
-    if (P.rot) {
-      const float* Q = P.Q;
-      if (D == 2) {
-        xw[0] = fmaf(Q[0], x[0], fmaf(Q[1], x[1], P.frame[0]));
-        xw[1] = fmaf(Q[3], x[0], fmaf(Q[4], x[1], P.frame[1]));
-        xw[2] = 0.0f;
-      } else {
-        xw[0] = fmaf(Q[0], x[0], fmaf(Q[1], x[1], fmaf(Q[2], x[2], P.frame[0])));
-        xw[1] = fmaf(Q[3], x[0], fmaf(Q[4], x[1], fmaf(Q[5], x[2], P.frame[1])));
-        xw[2] = fmaf(Q[6], x[0], fmaf(Q[7], x[1], fmaf(Q[8], x[2], P.frame[2])));
-      }
-      return;
-    }
-  } else if (PHASE) {
-    xw[0] = fmaf(P.ax[0], x[0], P.frame[0]);
-    xw[1] = fmaf(P.ax[1], x[1], P.frame[1]);
-    xw[2] = 0.0f;
-    return;
-  }
-  xw[0] = x[0] + P.frame[0];
-  xw[1] = x[1] + P.frame[1];
-  xw[2] = D == 3 ? x[2] + P.frame[2] : 0.0f;
+// Kernel coordinates -> frame coordinates (the frame the owner test reads:
+// rotated for balls, whose hole centres are stored rotated; unsheared for
+// boxes) and -> world coordinates.
+template <int D, int OUTER, bool SHEAR>
+__device__ __forceinline__ void to_frame(const F32Params& P, const float* x, float* xf) {
+  for (int i = 0; i < 3; ++i) xf[i] = (i < D) ? (SHEAR ? P.ax[i] * x[i] : x[i]) : 0.0f;
 }
 
-template <int D, int OUTER, int NH, int BINK, int SMEM, bool PHASE>
+template <int D, int OUTER>
+__device__ __forceinline__ void frame_to_world(const F32Params& P, const float* xf, float* xw) {
+  if (OUTER == OUTER_BALL && P.rot) {
+    const float* Q = P.Q;
+    if (D == 2) {
+      xw[0] = fmaf(Q[0], xf[0], fmaf(Q[1], xf[1], P.frame[0]));
+      xw[1] = fmaf(Q[3], xf[0], fmaf(Q[4], xf[1], P.frame[1]));
+      xw[2] = 0.0f;
+    } else {
+      xw[0] = fmaf(Q[0], xf[0], fmaf(Q[1], xf[1], fmaf(Q[2], xf[2], P.frame[0])));
+      xw[1] = fmaf(Q[3], xf[0], fmaf(Q[4], xf[1], fmaf(Q[5], xf[2], P.frame[1])));
+      xw[2] = fmaf(Q[6], xf[0], fmaf(Q[7], xf[1], fmaf(Q[8], xf[2], P.frame[2])));
+    }
+    return;
+  }
+  xw[0] = xf[0] + P.frame[0];
+  xw[1] = xf[1] + P.frame[1];
+  xw[2] = D == 3 ? xf[2] + P.frame[2] : 0.0f;
+}
+
+template <int D, int OUTER, int NH, int BINK, int SMEM, bool SHEAR>
 __device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
                                        StepAcc& acc) {
   const WorkOut& W = P.w;
+  float xf[3], xw[3];
+  to_frame<D, OUTER, SHEAR>(P, x, xf);
   int side;
-  if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, x)];
+  if (OUTER == OUTER_LBOX || NH != 0) side = P.comp_side[owner<D, OUTER, NH>(P, xf)];
   else side = P.comp_side[0];
-  float xw[3];
-  to_world<D, OUTER, PHASE>(P, x, xw);
+  frame_to_world<D, OUTER>(P, xf, xw);
   const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
@@ -648,7 +673,7 @@ struct ExitQueue {
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
 __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
-  constexpr bool PHASE = Phase<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool SHEAR = Shear<D, OUTER, NH, CHAIN, IDENT>::value;
   __shared__ ExitQueue q_all[kWarps];
   // lane id, lane mask and the queue's shared-window address are made opaque
   // (empty asm) so the compiler keeps them in registers instead of
@@ -705,25 +730,27 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
                          : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qb + kQueue * 16u + slot * 4u)
                          : "memory");
-            retire<D, OUTER, NH, BINK, SMEM, PHASE>(P, ex, __float_as_int(pw), es, acc);
+            retire<D, OUTER, NH, BINK, SMEM, SHEAR>(P, ex, __float_as_int(pw), es, acc);
             qn -= 32;
             __syncwarp();
           }
         }
       } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
+        float xf[3];
+        to_frame<D, OUTER, SHEAR>(P, x, xf);
         double xd[3] = {(double)x[0], (double)x[1], D == 3 ? (double)x[2] : 0.0};
         if (OUTER == OUTER_BALL && P.rot) {
           double t[3] = {0.0, 0.0, 0.0};
           for (int i = 0; i < D; ++i)
             for (int j = 0; j < D; ++j) t[i] += (double)P.Q[3 * i + j] * xd[j];
           for (int i = 0; i < D; ++i) xd[i] = t[i];
-        } else if (PHASE) {
+        } else if (SHEAR) {
           for (int i = 0; i < D; ++i) xd[i] *= (double)P.ax[i];
         }
         for (int j = 0; j < D; ++j) W.x_out[o * D + j] = xd[j] + (double)P.frame[j];
         W.steps_out[o] = steps;
-        W.comp_out[o] = owner<D, OUTER, NH>(P, x);
+        W.comp_out[o] = owner<D, OUTER, NH>(P, xf);
       }
       if (pool_take_fast(wp, need, W, pole, rep_off, eq, lt)) {
         if (pole != cpole) {
@@ -771,8 +798,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       for (int k = 0; k < K; ++k) {
         float t, r;
         dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
-        wm = __saturatef(t);
-        step<D, OUTER, IDENT, PHASE>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+        wm = t;  // already the saturated 0/1 mask
+        step<D, OUTER, IDENT, SHEAR>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
                                      angle_bits<D>(wv, k, P.one_bits));
         sf += wm;
       }
@@ -789,7 +816,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
         const float rs = walking ? r : 0.0f;
-        step<D, OUTER, IDENT, PHASE>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+        step<D, OUTER, IDENT, SHEAR>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
                                      angle_bits<D>(wv, k, P.one_bits));
         steps += walking;
       }
@@ -811,7 +838,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       const ExitQueue& q = q_all[threadIdx.x >> 5];
       const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM, PHASE>(P, ex, __float_as_int(e.w), q.s[lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM, SHEAR>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
     acc_flush<SMEM>(acc, W);
     stats_smem_flush<SMEM>(W);
