@@ -745,6 +745,15 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       const int k = 24 - (ex - 1) + 2;
       P.s2_scale = std::ldexp(1.0f, k);
       P.s2_bias = c * P.s2_scale;
+      if (nh >= 1) {
+        // concentric hole: the same construction for |x|^2 > (rho + eps)^2
+        const double rho = gf[d + 1 + d];
+        const float ch = (float)((rho + eps) * (rho + eps));
+        std::frexp((double)ch, &ex);
+        const int kh = 24 - (ex - 1) + 2;
+        P.h2_scale = std::ldexp(1.0f, kh);
+        P.h2_bias = -ch * P.h2_scale;
+      }
     }
     P.shrink_rel = 4.0e-6f;
     P.shrink_abs = (float)(scale * 1.1920928955078125e-07);

@@ -124,6 +124,7 @@ struct F32Params {
   float eps;
   float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
   float oR2, s2_scale, s2_bias;  // ball: R^2 and sat(-|x|^2 s + b) = [|x|^2 < (R - eps)^2]
+  float h2_scale, h2_bias;       // concentric hole: sat(|x|^2 s + b) = [|x|^2 > (rho + eps)^2]
   float shrink_rel, shrink_abs;  // step safety margins
   float keep;                    // 1 - shrink_rel
   unsigned one_bits;             // 0x3f800000 (1.0f), opaque to the compiler: PRMT operand

@@ -101,29 +101,6 @@ __device__ __forceinline__ void dist_raw(const F32Params& P, const float* x, flo
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
   constexpr bool DIAG = OUTER == OUTER_BALL && !IDENT;  // rotated ball frame
-  if (OUTER == OUTER_BALL && NH == 1 && MAXC && P.concentric) {
-    // annulus / spherical shell: one |v| and one |Av| serve both bounds, and
-    //   r = min(q_o / D_o, max(q_h / D_h, e_h)) = min(q_o / D_o, n_h / D_h)
-    // with n_h = max(q_h, e_h D_h) is picked by cross-multiplication, so a
-    // single reciprocal replaces two divisions (XU-bound step: 10 -> 7 MUFU)
-    const float v0 = x[0], v1 = x[1];
-    const float v2 = D == 3 ? x[2] : 0.0f;
-    float s2, aa;  // |v|^2, |Av|^2
-    norm_quad<D, DIAG>(P, v0, v1, v2, s2, aa);
-    const float s = fsqrt(s2);
-    const float rho = P.hr[0];
-    const float eo = P.oR - s, eh = s - rho;
-    e = fminf(eo, eh);
-    const float a = fsqrt(aa);
-    const float qo = P.oR2 - s2;  // R^2 - |v|^2
-    const float Do = a + fsqrt(fmaxf(aa + qo, 0.0f));
-    const float qh = s2 - P.hr2[0];  // |v|^2 - rho^2
-    const float Dh = a + fsqrt(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
-    const float nh = fmaxf(qh, eh * Dh);
-    const bool outer = qo * Dh <= nh * Do;
-    r = fdiv(outer ? qo : nh, outer ? Do : Dh);
-    return;
-  }
   if (OUTER == OUTER_BALL) {
     // kernel frame: the outer ball is centred at the origin
     const float v0 = x[0], v1 = x[1];
@@ -229,6 +206,28 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
   constexpr bool MAXC = (CHAIN == EM_CHAIN_MAX) && !IDENT;
   constexpr bool FOLD = MAXC && OUTER != OUTER_BALL && NH == 0;
   constexpr bool S2STOP = MAXC && OUTER == OUTER_BALL && NH == 0;
+  constexpr bool DIAG = OUTER == OUTER_BALL && !IDENT;  // rotated ball frame
+  if (OUTER == OUTER_BALL && NH == 1 && MAXC && P.concentric) {
+    // annulus / spherical shell: one |v|^2 and one |Av|^2 serve both bounds,
+    //   r = min(q_o / D_o, q_h / D_h),  q_o = R^2 - |v|^2,  q_h = |v|^2 - rho^2
+    // picked by cross-multiplication, so a single reciprocal replaces two
+    // divisions; both stop tests run on |v|^2 against (R - eps)^2 and
+    // (rho + eps)^2, so |v| itself is never formed (XU-bound step: 6 MUFU)
+    const float v0 = x[0], v1 = x[1];
+    const float v2 = D == 3 ? x[2] : 0.0f;
+    float s2, aa;  // |v|^2, |Av|^2
+    norm_quad<D, DIAG>(P, v0, v1, v2, s2, aa);
+    t = fminf(__saturatef(fmaf(s2, -P.s2_scale, P.s2_bias)),
+              __saturatef(fmaf(s2, P.h2_scale, P.h2_bias)));
+    const float a = fsqrt(aa);
+    const float qo = P.oR2 - s2;
+    const float Do = a + fsqrt(fmaxf(aa + qo, 0.0f));
+    const float qh = s2 - P.hr2[0];
+    const float Dh = a + fsqrt(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
+    const bool outer = qo * Dh <= qh * Do;
+    r = fmaf(fdiv(outer ? qo : qh, outer ? Do : Dh), P.keep, -P.shrink_abs);
+    return;
+  }
   if (Shear<D, OUTER, NH, CHAIN, IDENT>::value) {
     // s_i <= 0 exactly when face i is within eps; any positive s_i scales to
     // >= 1 (ss_scale), so sat(t) is the 0/1 walking mask
