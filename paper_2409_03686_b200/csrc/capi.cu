@@ -38,6 +38,8 @@ cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const do
                                   long long n, long long* comp, long long* side, long long* bin,
                                   cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
+cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, long long n_poles,
+                              unsigned long long* stats, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
@@ -231,6 +233,7 @@ struct em_plan {
   const double* radii_dev[2] = {nullptr, nullptr};
   // one output block: counts (n_poles x row) | stats (3 x n_poles) | misc (err, ticket)
   DevBuf counts, stats, misc;
+  DevBuf scopies;  // step-statistics copies (WorkOut::stat_copies > 1)
   PinBuf pin;  // host staging of the output block
   bool pin_valid = false;
   unsigned long long *blk_counts = nullptr, *blk_stats = nullptr, *blk_misc = nullptr;
@@ -558,6 +561,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   w.ssq = w.ssum + n_poles;
   w.smax = w.ssq + n_poles;
   w.smem_stats = 0;  // decided per launch (plan_launch)
+  w.stat_copies = 1;
 
   const em_side* sides[2] = {s0, s1};
   if (p->precision == EM_PREC_REF64) {
@@ -912,11 +916,27 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     // atomics on 3 * n_poles addresses; big jobs flush rarely and keep the
     // register path (no end-of-kernel burst of per-block flushes)
     w->smem_stats = (p->n_poles <= 128 && rb < 256) ? 1 : 0;
+    // many warps per pole (few rows in flight, e.g. a row shard): the
+    // per-lane statistics flushes of one chunk all hit the same 3 addresses
+    // and serialise in L2; spread them over copies folded by a second kernel
+    w->stat_copies = 1;
+    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats && warps > 32.0 * (double)p->n_poles) {
+      int c = 2;
+      while (c < 64 && (double)c * 16.0 * (double)p->n_poles < warps) c *= 2;
+      w->stat_copies = c;
+    }
   }
   w->counts = counts;
-  w->ssum = stats;
-  w->ssq = stats + p->n_poles;
-  w->smax = stats + 2 * p->n_poles;
+  unsigned long long* sdst = stats;
+  if (w->stat_copies > 1) {
+    if (p->scopies.alloc((size_t)w->stat_copies * 3 * p->n_poles * 8) != cudaSuccess)
+      return fail(EM_ERR_NOMEM, "cudaMalloc: statistics copies");
+    sdst = p->scopies.as<unsigned long long>();
+    EM_CUDA(cudaMemsetAsync(sdst, 0, (size_t)w->stat_copies * 3 * p->n_poles * 8, s));
+  }
+  w->ssum = sdst;
+  w->ssq = sdst + p->n_poles;
+  w->smax = sdst + 2 * p->n_poles;
   const int64_t row = p->n0 + p->n1;
   int64_t launches = 0;
   if (mode == 0 && counts == p->blk_counts) {
@@ -947,8 +967,13 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
                      grid, p->block, s);
     }
     if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("walk kernel launch: ") + cudaGetErrorString(e));
-    EM_CUDA(cudaEventRecord(p->ev1, s));
     launches = 1;
+    if (w->stat_copies > 1) {
+      e = launch_stats_fold(sdst, w->stat_copies, p->n_poles, stats, s);
+      if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("statistics fold: ") + cudaGetErrorString(e));
+      launches = 2;
+    }
+    EM_CUDA(cudaEventRecord(p->ev1, s));
   }
   p->last_launches = launches;
   p->last_walks = total;

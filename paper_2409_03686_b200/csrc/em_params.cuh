@@ -55,6 +55,10 @@ struct WorkOut {
   unsigned long long* counts;                  // (n_poles, row_len)
   int row_len, col_off1;                       // side-1 column offset
   int smem_stats;                              // per-block shared stats table (n_poles <= 1024)
+  // > 1: ssum/ssq/smax are rows of a (stat_copies, 3, n_poles) scratch, each
+  // warp flushes into copy (warp + lane) mod stat_copies, and a second kernel
+  // folds the copies (spreads the flush atomics when many warps share a pole)
+  int stat_copies;
   unsigned long long *ssum, *ssq, *smax;
   // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
   // output block means "no failure" and the smallest key wins

@@ -188,9 +188,13 @@ __device__ __forceinline__ void acc_flush(StepAcc& a, const WorkOut& W) {
       atomicAdd(&t[W.n_poles + a.pole], a.sq);
       atomicMax(&t[2 * W.n_poles + a.pole], a.mx);
     } else {
-      atomicAdd(&W.ssum[a.pole], a.sum);
-      atomicAdd(&W.ssq[a.pole], a.sq);
-      atomicMax(&W.smax[a.pole], a.mx);
+      // W.stat_copies is a power of two; 1 = flush straight into the output
+      const long long off =
+          (long long)(((threadIdx.x >> 5) + (threadIdx.x & 31) + blockIdx.x * 8) & (W.stat_copies - 1)) *
+          3 * W.n_poles;
+      atomicAdd(&W.ssum[off + a.pole], a.sum);
+      atomicAdd(&W.ssq[off + a.pole], a.sq);
+      atomicMax(&W.smax[off + a.pole], a.mx);
     }
   }
   a.sum = a.sq = a.mx = 0;

@@ -964,6 +964,27 @@ cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const do
   return cudaGetLastError();
 }
 
+// ---- fold the step-statistics copies (WorkOut::stat_copies) ----
+__global__ void stats_fold_kernel(const unsigned long long* scratch, int copies, long long n_poles,
+                                  unsigned long long* stats) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over 3 n_poles
+  if (i >= 3 * n_poles) return;
+  const bool is_max = i >= 2 * n_poles;
+  unsigned long long v = 0;
+  for (int c = 0; c < copies; ++c) {
+    const unsigned long long w = scratch[(long long)c * 3 * n_poles + i];
+    v = is_max ? (w > v ? w : v) : v + w;
+  }
+  stats[i] = v;
+}
+
+cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, long long n_poles,
+                              unsigned long long* stats, cudaStream_t s) {
+  const long long n = 3 * n_poles;
+  stats_fold_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scratch, copies, n_poles, stats);
+  return cudaGetLastError();
+}
+
 // ---- FP32 issue-rate micro-benchmark (roofline denominator) ----
 __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
   float v[8];
