@@ -911,18 +911,21 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
     w->rb = rb;
     w->n_chunks = (unsigned long long)p->n_poles * (unsigned long long)((n_rep + rb - 1) / rb);
-    // small chunks mean a pole change (a statistics flush) almost every walk:
-    // collect those flushes in a per-block shared table instead of global
-    // atomics on 3 * n_poles addresses; big jobs flush rarely and keep the
-    // register path (no end-of-kernel burst of per-block flushes)
-    w->smem_stats = (p->n_poles <= 128 && rb < 256) ? 1 : 0;
-    // many warps per pole (few rows in flight, e.g. a row shard): the
-    // per-lane statistics flushes of one chunk all hit the same 3 addresses
-    // and serialise in L2; spread them over copies folded by a second kernel
+    // minimum chunks (tiny jobs: ~1 walk per lane per chunk) mean a pole
+    // change (a statistics flush) almost every walk: collect those flushes in
+    // per-warp shared tables instead of global atomics (cfg1: 7x); bigger
+    // jobs keep the register path (no end-of-kernel burst of table flushes;
+    // a 32-pole row shard of cfg2 is 14% faster without the tables)
+    w->smem_stats = (p->n_poles <= 128 && rb < 64) ? 1 : 0;
+    // every lane flushes its per-pole statistics once per chunk, i.e. ~32
+    // atomics per address per rb x n_poles walks; when that product is small
+    // (few rows, e.g. a row shard, or few walks per row) the flushes
+    // serialise on the 3 n_poles addresses in L2: spread them over copies
+    // (folded by a second kernel) so every address sees <= 32 / 2^18 per walk
     w->stat_copies = 1;
-    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats && warps > 32.0 * (double)p->n_poles) {
-      int c = 2;
-      while (c < 64 && (double)c * 16.0 * (double)p->n_poles < warps) c *= 2;
+    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats) {
+      int c = 1;
+      while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 262144.0) c *= 2;
       w->stat_copies = c;
     }
   }
