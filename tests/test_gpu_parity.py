@@ -311,3 +311,64 @@ def test_fp32_grid_binning_equals_exact(B, idx):
             bins[prec] = plan.bin_points(x)
     for a, b in zip(bins["fp32"], bins["ref64"]):
         assert int((a != b).sum()) <= 2  # FP32 rounding at an exact Voronoi tie
+
+
+def _frame_case(golden_cases, name):
+    """Geometries that exercise the FP32 kernel's frame reformulations with an
+    anisotropic K: balls (rotated onto K's eigenbasis) with off-centre holes
+    and a 3D concentric shell, and a 3D box (sheared axes).  Anchors come from
+    the reference's golden cases (S/ generic blocks) or, for the box, from a
+    seeded generic set on its faces."""
+    from paper_2409_03686_b200.conductivity import make_tensor
+
+    k2 = make_tensor(np.array([[2.0, 0.8], [0.8, 1.0]])).k_sqrt
+    k3 = make_tensor(np.array([[3.0, 1.0, 0.0], [1.0, 2.0, 0.5], [0.0, 0.5, 1.0]])).k_sqrt
+    if name == "box3d":
+        rng = np.random.default_rng(7)
+        pts = rng.uniform(-0.5, 0.5, size=(90, 3))
+        ax = np.arange(90) % 3
+        pts[np.arange(90), ax] = np.where(rng.random(90) < 0.5, -0.5, 0.5)
+        blk = np.array([[0, 0, 90]], dtype=np.int64)
+        side0 = (pts, blk, np.zeros((1, 4)))
+        side1 = (np.zeros((0, 3)), np.array([[0, 0, 0]], dtype=np.int64), np.zeros((1, 4)))
+        gi = np.array([3, 1, 0], dtype=np.int64)
+        gf = np.array([0.0, 0.0, 0.0, 0.5])
+        poles = np.array([[0.1, -0.2, 0.15], [-0.3, 0.25, -0.1]])
+        return gi, gf, np.array([0], dtype=np.int8), k3, poles, side0, side1
+    c = case(golden_cases, name)
+    d = int(c["gi"][0])
+    second = {"disc": [-0.5, 0.2], "five": [0.0, 0.0], "shell3d": [-0.3, 0.5, 0.4]}[name]
+    poles = np.array([c["pole"], second])
+    return (c["gi"], c["gf"], c["comp_side"], k2 if d == 2 else k3, poles,
+            (c["a0"], c["blk0"], c["blkf0"]), (c["a1"], c["blk1"], c["blkf1"]))
+
+
+@pytest.mark.parametrize("name", ["disc", "five", "shell3d", "box3d"])
+@pytest.mark.parametrize("chain", ["woe", "max"])
+def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, chain):
+    """FP32 (rotated ball frames with holes, sheared 3D box axes) vs the
+    oracle's FP64 reference chain: exact row sums, entry-wise exact binomial
+    tests at family-wise level 1e-4, row chi^2 homogeneity."""
+    from helpers import P_Z4, exact_two_sample_p
+
+    gi, gf, cs, ks, poles, a0, a1 = _frame_case(golden_cases, name)
+    d = int(gi[0])
+    eps = 1e-5
+    geom = B.GeomPack(gi, gf, cs)
+    s0 = B.SidePack(a0[0], a0[1], a0[2], 0, np.zeros(0), 2)
+    s1 = B.SidePack(a1[0], a1[1], a1[2], 0, np.zeros(0), 2)
+    n_fp32, n_ref = 300_000, 20_000
+    with B.Plan(geom, ks, poles, eps, 10**6, s0, s1, precision="fp32", chain=chain) as plan:
+        r = plan.run(4242, n_fp32)
+    assert np.array_equal(r.counts.sum(1), np.full(len(poles), n_fp32))
+    raw0, raw1, *_ = oracle.run_accumulate_packed(gi, gf, cs, ks, poles, 99, eps, 10**6, n_ref,
+                                                  a0, a1)
+    ref = np.concatenate([raw0, raw1], axis=1)
+    p = exact_two_sample_p(r.counts, n_fp32, ref, n_ref)
+    m = p.size
+    worst = np.unravel_index(p.argmin(), p.shape)
+    assert p.min() >= 1e-4 / m, (p.min(), worst, r.counts[worst], ref[worst])
+    assert int((p < P_Z4).sum()) <= exceed_quantile(m, q=0.99999)
+    rows = row_chi2_pvalues(r.counts, n_fp32, ref, n_ref)
+    assert rows.min() > 1e-5 / len(rows), rows.min()
+    assert d in (2, 3)
