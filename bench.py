@@ -222,6 +222,13 @@ def profiled_traffic(cfg_index: int, precision: str, chain: str):
         return None
 
 
+def workload_name(cfg) -> str:
+    """The workload string both arms put in config.workload."""
+    bins = (len(cfg.fam0) if cfg.fam0 is not None else 0) + len(cfg.fam1)
+    return (f"{cfg.name}: {cfg.n_poles} poles x {cfg.n_rep:.0e} walks, eps {cfg.eps:g}, "
+            f"{bins} bins")
+
+
 def run_reference(args):
     world, rank, _ = _dist_env()
     if rank != 0:
@@ -248,8 +255,9 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "steps_per_s": sps, "mean_steps_per_walk": info[4],
-        "config": {"workload": cfg.name, "poles": cfg.n_poles, "walks_per_pole": n_sample,
-                   "eps": cfg.eps},
+        "config": {"workload": workload_name(cfg), "precision": "fp64 (the reference chain)",
+                   "sample_per_step": f"{cfg.n_poles} poles x {n_sample} walks",
+                   "threads": threads},
         "cpu_baseline": {"value": wps, "unit": "walks/s", "cores": threads, "kind": info[2],
                          "sample": sample},
         "e2e": {"value": wps, "unit": "walks/s", "h2d_bytes_per_step": 0,
@@ -405,8 +413,7 @@ def run_ours(args):
             "dtype": "f32" if plan.precision == "fp32" else "f64", "data": "synthetic",
             "steps_per_s": steps_per_s,
             "mean_steps_per_walk": steps_total_run / (cfg.total_walks * (world if weak else 1)),
-            "config": {"workload": f"{cfg.name}: {cfg.n_poles} poles x {cfg.n_rep:.0e} walks, "
-                                   f"eps {cfg.eps:g}, {plan.n0 + plan.n1} bins",
+            "config": {"workload": workload_name(cfg),
                        "precision": plan.precision, "chain": plan.chain,
                        "parallelism": (f"{world} GPU(s), each all poles x {cfg.n_rep:.0e} walks on "
                                        "its own replicate range; rows summed once after timing"
