@@ -26,8 +26,11 @@ There is no CPU fallback: a missing library or device raises NativeError.
 from __future__ import annotations
 
 import ctypes
-import weakref
+import hashlib
 import os
+import threading
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -454,11 +457,47 @@ class Plan:
         return int(v.value)
 
 
+# Plans of recent run_accumulate calls, keyed by the content of every input
+# that shapes the plan (geometry, K, poles, pole ids, both sides, eps, budget,
+# precision, chain, device): a repeated call with the same inputs (a parameter
+# sweep over seeds or walk counts, the reference's benchmark loop) skips plan
+# creation and the input upload.  Results are detached from the plan, so a
+# cached plan is reusable as soon as run() returns; a plan busy in another
+# thread is bypassed with a one-shot plan.
+_PLAN_CACHE: "OrderedDict[tuple, tuple[Plan, threading.Lock]]" = OrderedDict()
+_PLAN_CACHE_LOCK = threading.Lock()
+_PLAN_CACHE_SIZE = 4
+
+
+def _plan_key(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
+              pole_ids) -> tuple:
+    """(scalars + dtypes/shapes, concatenated array bytes): the plan's full
+    input content, compared exactly (no digest: ~5 us for cfg2's 12 KiB)."""
+    arrays = (geom.gi, geom.gf, geom.comp_side, ksqrt, poles, pole_ids,
+              side0.anchors, side0.blk, side0.blkf, side0.idw_radii, getattr(side0, "blk_phase", None),
+              side1.anchors, side1.blk, side1.blkf, side1.idw_radii, getattr(side1, "blk_phase", None))
+    # the reference's own SidePack (plugin path) has the same fields minus blk_phase
+    meta = [float(eps), int(max_steps), int(side0.weights_kind), int(side0.idw_power),
+            int(side1.weights_kind), int(side1.idw_power), precision, chain, device]
+    parts = []
+    for a in arrays:
+        if a is None:
+            meta.append(None)
+        else:
+            a = np.asarray(a)
+            meta.append((a.dtype.str, a.shape))
+            parts.append(a.tobytes())
+    return tuple(meta), b"".join(parts)
+
+
 def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_rep: int,
                    side0, side1, threads: int | None = None, *, precision: str | None = None,
                    chain: str | None = None, device: int | None = None,
-                   pole_ids=None) -> AccumulateResult:
+                   pole_ids=None, cache: bool = True) -> AccumulateResult:
     """All (pole, replicate) walks in one kernel launch (S/backend.py:147-199).
+
+    ``cache=False`` builds (and uploads) a one-shot plan even when a cached
+    plan for the same inputs exists.
 
     ``threads`` is accepted for signature compatibility and ignored.  Raises
     WalkBudgetError(pole, replicate, max_steps) for the lexicographically
@@ -474,9 +513,48 @@ def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_r
                                 z, z.copy(), z.copy(), 0, np.zeros((0, int(side0.size + side1.size)),
                                                                    dtype=np.int64),
                                 n0=int(side0.size))
-    with Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
-              pole_ids) as plan:
-        return plan.run(seed, n_rep)
+    precision = (precision or default_precision()).lower()
+    chain = (chain or default_chain(precision)).lower()
+    device = default_device() if device is None else int(device)
+    if not cache:
+        with Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
+                  pole_ids) as plan:
+            return plan.run(seed, n_rep)
+    key = _plan_key(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
+                    pole_ids)
+    with _PLAN_CACHE_LOCK:
+        hit = _PLAN_CACHE.get(key)
+        if hit is not None:
+            _PLAN_CACHE.move_to_end(key)
+    if hit is not None and hit[1].acquire(blocking=False):
+        try:
+            return hit[0].run(seed, n_rep)
+        finally:
+            hit[1].release()
+    plan = Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
+                pole_ids)
+    lock = threading.Lock()
+    with lock:
+        res = plan.run(seed, n_rep)
+    if hit is None:
+        with _PLAN_CACHE_LOCK:
+            if key not in _PLAN_CACHE:
+                _PLAN_CACHE[key] = (plan, lock)
+                while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+                    _PLAN_CACHE.popitem(last=False)
+                return res
+    plan.close()
+    return res
+
+
+def clear_plan_cache() -> None:
+    """Release the plans cached by run_accumulate."""
+    with _PLAN_CACHE_LOCK:
+        items = list(_PLAN_CACHE.values())
+        _PLAN_CACHE.clear()
+    for plan, lock in items:
+        with lock:
+            plan.close()
 
 
 def run_exits(dom, ksqrt, pole_xy, pole_index: int, seed: int, eps: float, max_steps: int,

@@ -140,3 +140,46 @@ def test_fp32_replicate_limit(B, cfg2):
     with B.Plan(geom, cfg2.kt.k_sqrt, cfg2.poles[:1], cfg2.eps, 10**6, s0, s1, "fp32") as plan:
         with pytest.raises(NativeError, match="2\\^31"):
             plan.run(cfg2.seed, 2**31)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "ref64"])
+def test_plan_cache_reuse_is_exact(B, cfg2, precision):
+    """run_accumulate reuses a cached plan for identical inputs: repeated
+    calls give identical rows, a new seed or walk count reruns the same plan,
+    and changed inputs (poles edited in place) build a new plan."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    s0, s1 = _sides(B, cfg2)
+    poles = cfg2.poles[:8].copy()
+    B.clear_plan_cache()
+
+    def call(seed, n=2000, p=poles):
+        return B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, p, seed, cfg2.eps, 10**6, n, s0, s1,
+                                precision=precision)
+
+    a = call(5)
+    assert len(B._PLAN_CACHE) == 1
+    b = call(5)
+    assert np.array_equal(a.counts, b.counts) and np.array_equal(a.steps_sum, b.steps_sum)
+    c = call(6, 3000)
+    assert len(B._PLAN_CACHE) == 1 and c.counts.sum() == 8 * 3000
+    with B.Plan(B.pack_geometry(cfg2.dom), cfg2.kt.k_sqrt, poles, cfg2.eps, 10**6, s0, s1,
+                precision=precision) as plan:
+        fresh = plan.run(6, 3000)
+    assert np.array_equal(c.counts, fresh.counts)
+    # concurrent callers: one takes the cached plan, the others one-shot plans
+    with ThreadPoolExecutor(4) as ex:
+        outs = list(ex.map(lambda _: call(5), range(4)))
+    for o in outs:
+        assert np.array_equal(o.counts, a.counts)
+    p2 = poles.copy()
+    p2[0] *= 0.5
+    d = call(5, p=p2)
+    assert len(B._PLAN_CACHE) == 2
+    assert not np.array_equal(d.counts[0], a.counts[0])
+    assert np.array_equal(d.counts[1:], a.counts[1:])
+    e = B.run_accumulate(cfg2.dom, cfg2.kt.k_sqrt, poles, 5, cfg2.eps, 10**6, 2000, s0, s1,
+                         precision=precision, cache=False)
+    assert np.array_equal(e.counts, a.counts) and len(B._PLAN_CACHE) == 2
+    B.clear_plan_cache()
+    assert len(B._PLAN_CACHE) == 0
