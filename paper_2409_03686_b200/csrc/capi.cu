@@ -921,11 +921,11 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     // atomics per address per rb x n_poles walks; when that product is small
     // (few rows, e.g. a row shard, or few walks per row) the flushes
     // serialise on the 3 n_poles addresses in L2: spread them over copies
-    // (folded by a second kernel) so every address sees <= 32 / 2^18 per walk
+    // (folded by a second kernel) so every address sees <= 32 / 2^17 per walk
     w->stat_copies = 1;
     if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats) {
       int c = 1;
-      while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 262144.0) c *= 2;
+      while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 131072.0) c *= 2;
       w->stat_copies = c;
     }
   }
