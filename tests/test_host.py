@@ -217,3 +217,44 @@ def test_spectral_requires_a_device():
         spectral.svd(np.ones(3))
     with pytest.raises(ValidationError):
         spectral.sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]))
+
+
+def test_plan_cache_key_is_exact_content():
+    """The run_accumulate plan cache keys on the exact bytes of every input
+    (no digest): equal content -> equal key; any changed element, dtype,
+    shape, scalar or option -> a different key; the reference's SidePack
+    (no blk_phase field) is accepted."""
+    from dataclasses import dataclass
+
+    from paper_2409_03686_b200 import backend as B, configs
+
+    cfg = configs.get(2)
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, 2, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 2, cfg.eps)
+    args = (geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, 10**6, s0, s1, "fp32", "max", 0, None)
+    k = B._plan_key(*args)
+    assert B._plan_key(*(geom, cfg.kt.k_sqrt.copy(), cfg.poles.copy()) + args[3:]) == k
+    p2 = cfg.poles.copy()
+    p2[17, 1] = np.nextafter(p2[17, 1], 1.0)
+    assert B._plan_key(geom, cfg.kt.k_sqrt, p2, *args[3:]) != k
+    assert B._plan_key(*args[:3], cfg.eps * 2, *args[4:]) != k
+    assert B._plan_key(*args[:7], "ref64", *args[8:]) != k
+    assert B._plan_key(*args[:10], np.arange(cfg.n_poles)) != k
+    a1 = s1.anchors.copy()
+    a1[0, 0] += 1e-12
+    s1b = B.SidePack(a1, s1.blk, s1.blkf, s1.weights_kind, s1.idw_radii, s1.idw_power,
+                     s1.blk_phase)
+    assert B._plan_key(*args[:6], s1b, *args[7:]) != k
+
+    @dataclass(frozen=True)
+    class RefSidePack:  # the reference's field set (S/backend.py:57-68)
+        anchors: np.ndarray
+        blk: np.ndarray
+        blkf: np.ndarray
+        weights_kind: int
+        idw_radii: np.ndarray
+        idw_power: int
+
+    r1 = RefSidePack(s1.anchors, s1.blk, s1.blkf, s1.weights_kind, s1.idw_radii, s1.idw_power)
+    assert B._plan_key(*args[:6], r1, *args[7:]) != k  # no phase -> different plan
