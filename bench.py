@@ -222,6 +222,28 @@ def profiled_traffic(cfg_index: int, precision: str, chain: str):
         return None
 
 
+def profiled_issue(cfg_index: int, precision: str, chain: str):
+    """Issue-slot and pipe utilisation of the walk kernel from the same
+    committed capture (the FP32-issue roofline's direct evidence), or None."""
+    import csv
+
+    f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
+    if cfg_index != 2 or precision != "fp32" or chain != "max" or not f.exists():
+        return None
+    vals = {row[0]: row[1] for row in csv.reader(open(f)) if len(row) == 3}
+    keys = {"issue_active": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "pipe_fma": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+            "pipe_alu": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "pipe_xu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "warps_active": "sm__warps_active.avg.pct_of_peak_sustained_active"}
+    try:
+        out = {k: round(float(vals[v]) / 100.0, 4) for k, v in keys.items()}
+    except (KeyError, ValueError):
+        return None
+    out["source"] = "profiles/r01_cfg2_walk_f32_ncu_raw.csv (fractions of peak)"
+    return out
+
+
 def workload_name(cfg) -> str:
     """The workload string both arms put in config.workload."""
     bins = (len(cfg.fam0) if cfg.fam0 is not None else 0) + len(cfg.fam1)
@@ -439,6 +461,7 @@ def run_ours(args):
                          "frac_of_measured_ffma": achieved / peak_ffma,
                          "frac_at_max_clock": achieved / (info["sm_count"] * 128 *
                                                           (clocks["sm_max_mhz"] or 1965) * 1e-6),
+                         "ncu": profiled_issue(cfg.index, plan.precision, plan.chain),
                          "reference_chain_equivalent": {
                              "frac": (value / world) * F_REF[cfg.index][0] * F_REF[cfg.index][1]
                                      / (peak_nominal * 1e12),
