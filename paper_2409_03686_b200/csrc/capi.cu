@@ -38,6 +38,8 @@ cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const do
                                   long long n, long long* comp, long long* side, long long* bin,
                                   cudaStream_t s);
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
+cudaError_t launch_zero_ranges(unsigned long long* const* ptrs, const long long* words, int n,
+                               cudaStream_t s);
 cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, long long n_poles,
                               unsigned long long* stats, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
@@ -245,11 +247,12 @@ struct em_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_walks = 0, last_steps = 0, last_launches = 0, last_n_rep = 0;
+  bool last_timed = false;  // ev0 / ev1 bracket the last walk kernel
   cudaStream_t last_stream = nullptr;  // stream of the last run_device
   ~em_plan() {
     // buffers go back to the shared cache: nothing in flight may still use them
     if (stream) cudaStreamSynchronize(stream);
-    if (last_launches && ev1) cudaEventSynchronize(ev1);
+    if (last_timed && ev1) cudaEventSynchronize(ev1);
     give_back(device, stream, ev0, ev1);
     give_back(device, nullptr, ev_up, nullptr);
   }
@@ -935,22 +938,42 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     if (p->scopies.alloc((size_t)w->stat_copies * 3 * p->n_poles * 8) != cudaSuccess)
       return fail(EM_ERR_NOMEM, "cudaMalloc: statistics copies");
     sdst = p->scopies.as<unsigned long long>();
-    EM_CUDA(cudaMemsetAsync(sdst, 0, (size_t)w->stat_copies * 3 * p->n_poles * 8, s));
   }
   w->ssum = sdst;
   w->ssq = sdst + p->n_poles;
   w->smax = sdst + 2 * p->n_poles;
   const int64_t row = p->n0 + p->n1;
   int64_t launches = 0;
-  if (mode == 0 && counts == p->blk_counts) {
-    EM_CUDA(cudaMemsetAsync(p->blk_counts, 0, p->blk_words * 8, s));  // counts | stats | misc
-  } else {
-    if (mode == 0) {
-      EM_CUDA(cudaMemsetAsync(counts, 0, (size_t)p->n_poles * row * 8, s));
-      EM_CUDA(cudaMemsetAsync(stats, 0, (size_t)p->n_poles * 3 * 8, s));
+  {
+    // every output the kernels accumulate into, zeroed by ONE launch:
+    // counts | stats | misc (one block on the host path), the statistics
+    // copies (the fold then overwrites the caller's stats)
+    unsigned long long* zp[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long zn[4] = {0, 0, 0, 0};
+    if (mode == 0 && counts == p->blk_counts) {
+      zp[0] = p->blk_counts;
+      zn[0] = (long long)p->blk_words;
+    } else {
+      if (mode == 0) {
+        zp[0] = counts;
+        zn[0] = (long long)p->n_poles * row;
+        if (w->stat_copies == 1) {
+          zp[1] = stats;
+          zn[1] = 3 * (long long)p->n_poles;
+        }
+      }
+      zp[2] = p->blk_misc;
+      zn[2] = 8;
     }
-    EM_CUDA(cudaMemsetAsync(p->blk_misc, 0, 64, s));
+    if (w->stat_copies > 1) {
+      zp[3] = sdst;
+      zn[3] = (long long)w->stat_copies * 3 * p->n_poles;
+    }
+    cudaError_t ze = launch_zero_ranges(zp, zn, 4, s);
+    if (ze != cudaSuccess) return fail(EM_ERR_CUDA, std::string("zero outputs: ") + cudaGetErrorString(ze));
+    launches = 1;
   }
+  p->last_timed = false;
   if (total > 0) {
     const int64_t lanes_needed = (total + 31) / 32 * 32;
     int grid = p->grid;
@@ -970,12 +993,13 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
                      grid, p->block, s);
     }
     if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("walk kernel launch: ") + cudaGetErrorString(e));
-    launches = 1;
+    launches += 1;
     if (w->stat_copies > 1) {
       e = launch_stats_fold(sdst, w->stat_copies, p->n_poles, stats, s);
       if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("statistics fold: ") + cudaGetErrorString(e));
-      launches = 2;
+      launches += 1;
     }
+    p->last_timed = true;
     EM_CUDA(cudaEventRecord(p->ev1, s));
   }
   p->last_launches = launches;
@@ -995,7 +1019,7 @@ static int plan_finish(em_plan* p, cudaStream_t s, int64_t n_rep, em_outputs* ou
   }
   const unsigned long long err = errv ? ~errv : ~0ULL;
   float ms = 0.0f;
-  if (p->last_launches) {
+  if (p->last_timed) {
     EM_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   }
   p->last_ms = ms;
@@ -1267,7 +1291,7 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
   if (idw_fallbacks) *idw_fallbacks = fb;
   if (err_pole) *err_pole = -1;
   if (err_rep) *err_rep = -1;
-  p->last_launches = 3;
+  p->last_launches += 2;  // + the IDW normaliser and scatter kernels
   return EM_OK;
 }
 

@@ -27,6 +27,8 @@
 //    em_pool.cuh: concurrent walks spread over all rows, so no hot address).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "em_params.cuh"
 #include "em_pool.cuh"
 #include "em_rng.cuh"
@@ -961,6 +963,40 @@ cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const do
   else if (outer == OUTER_BALL) bin_points_f32_kernel<3, OUTER_BALL><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
   else if (outer == OUTER_BOX) bin_points_f32_kernel<3, OUTER_BOX><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
   else bin_points_f32_kernel<3, OUTER_LBOX><<<g, 128, 0, s>>>(P, pts, n, comp, side, bin);
+  return cudaGetLastError();
+}
+
+// ---- zero up to 4 output ranges with ONE launch (instead of a memset each) ----
+struct ZeroRanges {
+  unsigned long long* p[4];
+  long long n[4];  // 8-byte words
+};
+
+__global__ void zero_ranges_kernel(const ZeroRanges z, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long j = i;
+    int r = 0;
+    while (j >= z.n[r]) j -= z.n[r++];
+    z.p[r][j] = 0ULL;
+  }
+}
+
+cudaError_t launch_zero_ranges(unsigned long long* const* ptrs, const long long* words, int n,
+                               cudaStream_t s) {
+  ZeroRanges z{};
+  long long total = 0;
+  int k = 0;
+  for (int i = 0; i < n && k < 4; ++i)
+    if (ptrs[i] && words[i] > 0) {
+      z.p[k] = ptrs[i];
+      z.n[k] = words[i];
+      total += words[i];
+      ++k;
+    }
+  if (total == 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((total + 255) / 256, 148LL * 8);
+  zero_ranges_kernel<<<(unsigned)blocks, 256, 0, s>>>(z, total);
   return cudaGetLastError();
 }
 
