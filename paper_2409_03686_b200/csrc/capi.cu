@@ -984,6 +984,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     if (s != p->stream) EM_CUDA(cudaStreamWaitEvent(s, p->ev_up, 0));
     if (p->precision == EM_PREC_REF64) {
       p->p64.seed = seed;
+      for (int r = 0; r < 10; ++r) p->p64.rk0[r] = seed + (unsigned long long)r * 0x9E3779B97F4A7C15ULL;
       e = launch_ref64(p->p64, mode, grid, p->block, s);
     } else {
       p->p32.key0 = (unsigned)(seed & 0xffffffffULL);

@@ -77,6 +77,7 @@ struct Ref64Params {
   double eps;
   long long max_steps;
   unsigned long long seed;
+  unsigned long long rk0[10];  // seed + r W0: Philox4x64 round keys (key word 1 is 0)
   const double* poles;  // (n_poles, d)
   Side64 side[2];
   WorkOut w;

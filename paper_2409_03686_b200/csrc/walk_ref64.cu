@@ -28,14 +28,46 @@ constexpr long long kBigIndex = 1LL << 62;
 // One Marsaglia trial of S/_kernel.pyx:57-81 (the reference loops until a
 // trial is accepted; the kernel below runs one trial per iteration so a
 // rejecting lane does not hold its warp -- same draws, same directions).
-__device__ __forceinline__ bool direction_trial(int d, unsigned long long seed,
+// Words 0 and 1 of Philox4x64-10 at key (seed, 0), counter (draw, 0, rep,
+// pole) -- exactly philox4x64_10 (em_rng.cuh) on the reference's stream
+// layout (S/_kernel.pyx:37-63) -- with the seed's round keys seed + r W0 read
+// from the params (constant-bank XOR operands instead of a 64-bit key add per
+// round) and round 0's M1 * rep, constant over a walk, passed in.
+__device__ __forceinline__ void philox_w01(const unsigned long long* rk0, unsigned long long draw,
+                                           unsigned long long h1r, unsigned long long l1r,
+                                           unsigned long long pole, unsigned long long& w0,
+                                           unsigned long long& w1) {
+  const unsigned long long M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+  const unsigned long long W1 = 0xBB67AE8584CAA73BULL;
+  // round 0: c = (draw, 0, rep, pole), k = (seed, 0)
+  unsigned long long c0 = h1r ^ rk0[0];
+  unsigned long long c1 = l1r;
+  unsigned long long c2 = __umul64hi(M0, draw) ^ pole;
+  unsigned long long c3 = M0 * draw;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    const unsigned long long hi0 = __umul64hi(M0, c0), lo0 = M0 * c0;
+    const unsigned long long hi1 = __umul64hi(M1, c2), lo1 = M1 * c2;
+    const unsigned long long n0 = hi1 ^ c1 ^ rk0[r];
+    const unsigned long long n2 = hi0 ^ c3 ^ ((unsigned long long)r * W1);
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  w0 = c0;
+  w1 = c1;
+}
+
+__device__ __forceinline__ bool direction_trial(int d, const unsigned long long* rk0,
                                                 unsigned long long& draw,
-                                                unsigned long long rep,
+                                                unsigned long long h1r, unsigned long long l1r,
                                                 unsigned long long pole, double* u) {
-  u64x4 w = philox4x64_10(seed, 0ULL, draw, 0ULL, rep, pole);
+  unsigned long long w0, w1;
+  philox_w01(rk0, draw, h1r, l1r, pole, w0, w1);
   draw += 1ULL;
-  double u0 = (double)(w.w0 >> 11) * kInv53;
-  double u1 = (double)(w.w1 >> 11) * kInv53;
+  double u0 = (double)(w0 >> 11) * kInv53;
+  double u1 = (double)(w1 >> 11) * kInv53;
   double v1 = 2.0 * u0 - 1.0;
   double v2 = 2.0 * u1 - 1.0;
   double s = v1 * v1 + v2 * v2;
@@ -275,6 +307,7 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
   double x[3] = {0.0, 0.0, 0.0};
   double u[3];
   unsigned long long draw = 0, rep = 0, pid = 0;
+  unsigned long long h1r = 0, l1r = 0;  // M1 * rep (Philox round 0, fixed per walk)
   long long steps = 0, rep_off = 0;
   int pole = 0;
   bool active = false;
@@ -299,6 +332,8 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
     if (need) {
       if (pool_take(wp, need, W, pole, rep_off)) {
         rep = (unsigned long long)(W.rep_start + rep_off);
+        h1r = __umul64hi(0xCA5A826395121157ULL, rep);
+        l1r = 0xCA5A826395121157ULL * rep;
         pid = W.pole_ids ? (unsigned long long)W.pole_ids[pole] : (unsigned long long)pole;
         for (int j = 0; j < d; ++j) x[j] = P.poles[pole * d + j];
         draw = 0;
@@ -352,7 +387,7 @@ __global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
       W.comp_out[o] = owner_component(P, x);
     }
     if (stop) active = false;
-    if (!active || !direction_trial(d, P.seed, draw, rep, pid, u)) continue;
+    if (!active || !direction_trial(d, P.rk0, draw, h1r, l1r, pid, u)) continue;
     phase = 0;
     const double* k = P.ks;
     if (d == 2) {
