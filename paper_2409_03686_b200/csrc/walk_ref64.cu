@@ -301,7 +301,7 @@ __device__ __forceinline__ void retire64(const Ref64Params& P, const double* xq,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) walk_ref64_kernel(const Ref64Params P) {
+__global__ void __launch_bounds__(256, 4) walk_ref64_kernel(const Ref64Params P) {
   const WorkOut& W = P.w;
   const int d = P.d;
   double x[3] = {0.0, 0.0, 0.0};
