@@ -30,6 +30,7 @@ EM_PREC_REF64 = 0
 EM_PREC_FP32 = 1
 EM_CHAIN_WOE = 0
 EM_CHAIN_MAX = 1
+EM_CHAIN_TANGENT = 2
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
@@ -100,6 +101,7 @@ def lib():
         "em_plan_last_stats": ([_p, _p, _p, _p], ctypes.c_int),
         "em_plan_check": ([_p, _p, _p], ctypes.c_int),
         "em_plan_last_launches": ([_p, _p], ctypes.c_int),
+        "em_plan_chain": ([_p], ctypes.c_int),
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),
                                ctypes.POINTER(EmSide), _p, _p, _i64, _u64, _dbl, _i64, _i64,

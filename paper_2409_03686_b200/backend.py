@@ -14,9 +14,12 @@ Two arithmetic paths (``precision``):
   exits and step statistics to the reference kernel for the same inputs.
 * ``"fp32"``: the production kernel (Philox4x32 streams, FP32 state, O(1)
   binning); statistically identical exit law, not bit-identical.  With
-  ``chain="max"`` (default for fp32) each step uses the largest certified
-  K^{1/2}-ellipsoid instead of the reference's sd-scaled one (fewer steps,
-  same stopping shell and exit law).
+  ``chain="max"`` each step uses the largest certified K^{1/2}-ellipsoid
+  instead of the reference's sd-scaled one (fewer steps, same stopping shell
+  and exit law); ``chain="tangent"`` (default for fp32) walks on the largest
+  balls tangent to the nearest face in whitened coordinates where the
+  geometry has that step (2D boxes), sampling each ball's harmonic measure
+  exactly (quadratic approach to the boundary), and runs "max" elsewhere.
 
 ``EXITMEASURE_B200_PRECISION`` / ``EXITMEASURE_B200_CHAIN`` set the defaults
 process-wide (the analogue of the reference's ``EXITMEASURE_BACKEND``).
@@ -45,7 +48,9 @@ _WEIGHT_KINDS = {"voronoi": 0, "idw": 1}
 _BLOCK_KIND = {"generic": 0, "circle": 1, "square": 2, "sphere": 0}
 _PRECISIONS = {"ref64": N.EM_PREC_REF64, "fp64": N.EM_PREC_REF64, "exact": N.EM_PREC_REF64,
                "fp32": N.EM_PREC_FP32}
-_CHAINS = {"woe": N.EM_CHAIN_WOE, "reference": N.EM_CHAIN_WOE, "max": N.EM_CHAIN_MAX}
+_CHAINS = {"woe": N.EM_CHAIN_WOE, "reference": N.EM_CHAIN_WOE, "max": N.EM_CHAIN_MAX,
+           "tangent": N.EM_CHAIN_TANGENT}
+_CHAIN_NAMES = {N.EM_CHAIN_WOE: "woe", N.EM_CHAIN_MAX: "max", N.EM_CHAIN_TANGENT: "tangent"}
 
 
 def default_precision() -> str:
@@ -56,7 +61,7 @@ def default_chain(precision: str) -> str:
     env = os.environ.get("EXITMEASURE_B200_CHAIN")
     if env:
         return env.lower()
-    return "woe" if _PRECISIONS[precision] == N.EM_PREC_REF64 else "max"
+    return "woe" if _PRECISIONS[precision] == N.EM_PREC_REF64 else "tangent"
 
 
 def default_device() -> int:
@@ -327,6 +332,9 @@ class Plan:
                                        ctypes.byref(opt), ctypes.byref(h)), "em_plan_create")
         self._h = h
         self.max_steps = int(max_steps)
+        # the chain the plan runs: "tangent" becomes "max" where the geometry
+        # has no tangent-ball step (em_plan_chain)
+        self.chain = _CHAIN_NAMES.get(int(N.lib().em_plan_chain(h)), chain)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -490,6 +490,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   const em_options& o = opt ? *opt : dflt;
   if (o.precision != EM_PREC_REF64 && o.precision != EM_PREC_FP32)
     return fail(EM_ERR_INVALID, "unknown precision");
+  if (o.chain != EM_CHAIN_WOE && o.chain != EM_CHAIN_MAX && o.chain != EM_CHAIN_TANGENT)
+    return fail(EM_ERR_INVALID, "unknown chain");
   if (o.precision == EM_PREC_REF64 && o.chain != EM_CHAIN_WOE)
     return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
   if (o.precision != EM_PREC_REF64 && (s0->wkind == 1 || s1->wkind == 1))
@@ -505,6 +507,14 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->device = o.device;
   p->precision = o.precision;
   p->chain = o.chain;
+  if (o.precision == EM_PREC_FP32 && o.chain == EM_CHAIN_TANGENT) {
+    // tangent-ball steps exist for 2D boxes without holes and K != I
+    bool id = true;
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j)
+        if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) id = false;
+    if (!(d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0 && !id)) p->chain = EM_CHAIN_MAX;
+  }
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
   p->n_holes = nh;
@@ -628,7 +638,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     double Qd[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
     double Adiag[3] = {1.0, 1.0, 1.0};
     P.rot = (g->gi[1] == 0 && nn == 0 && !ident) ? 1 : 0;
-    P.shear = (g->gi[1] == 1 && nh == 0 && o.chain == EM_CHAIN_MAX && !ident && (d == 3 || nn == 0)) ? 1 : 0;
+    P.shear = (g->gi[1] == 1 && nh == 0 && p->chain == EM_CHAIN_MAX && !ident && (d == 3 || nn == 0)) ? 1 : 0;
+    P.tangent = p->chain == EM_CHAIN_TANGENT ? 1 : 0;
     if (P.rot) sym_eig(g->ksqrt, d, Adiag, Qd);
     for (int i = 0; i < 3; ++i) {
       P.Ad[i] = (float)Adiag[i];
@@ -675,6 +686,23 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         P.shk[2] = (float)(gm[2] / gm[1]);
       }
       for (int i = 0; i < d; ++i) shear_g[i] = std::fabs(axd[i]) / Rn[i];
+    }
+    double tcd = 0.0;
+    if (P.tangent) {
+      // xt_i = x_i / R_i: the whitened point's coordinate along face normal i
+      const double* A = g->ksqrt;
+      double Rn[2], ah[2][2];
+      for (int i = 0; i < 2; ++i) {
+        Rn[i] = std::hypot(A[2 * i], A[2 * i + 1]);
+        ah[i][0] = A[2 * i] / Rn[i];
+        ah[i][1] = A[2 * i + 1] / Rn[i];
+        axd[i] = Rn[i];
+      }
+      tcd = ah[0][0] * ah[1][0] + ah[0][1] * ah[1][1];
+      P.tcd = (float)tcd;
+      P.tsd = (float)std::sqrt(std::max(0.0, 1.0 - tcd * tcd));
+      P.tim = (float)(1.0 / (1.0 - tcd));
+      P.tip = (float)(1.0 / (1.0 + tcd));
     }
     for (int i = 0; i < 3; ++i) P.ax[i] = (float)axd[i];
     // world point -> kernel coordinates
@@ -792,9 +820,27 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       }
       // every positive s is >= ulp(sb_min) / 2 (Sterbenz near sb, larger
       // below): a power-of-two scale 2^k >= 2 / ulp(sb_min) maps it to >= 1
+      // (the tangent chain below uses the same construction)
       int ex = 0;
       std::frexp((double)sbmin, &ex);  // sb in [2^(ex-1), 2^ex), ulp = 2^(ex-24)
       P.ss_scale = std::ldexp(1.0f, 25 - ex + 1);
+    }
+    if (P.tangent) {
+      // whitened half-widths and stop thresholds; the ball radius is shrunk
+      // by keep and by a few ulps of the whitened box (coordinate rounding)
+      float sbmin = 0.0f;
+      double btmax = 1.0;
+      for (int i = 0; i < 2; ++i) {
+        P.tbt[i] = (float)(gf[d] / axd[i]);
+        P.tsb[i] = (float)((double)P.tbt[i] - eps / axd[i]);
+        sbmin = i == 0 ? P.tsb[i] : std::min(sbmin, P.tsb[i]);
+        btmax = std::max(btmax, (double)P.tbt[i]);
+      }
+      int ex = 0;
+      std::frexp((double)sbmin, &ex);
+      P.ss_scale = std::ldexp(1.0f, 25 - ex + 1);
+      P.tkeep = P.keep;
+      P.tsa = (float)(btmax * 2.384185791015625e-07);  // 2^-22
     }
     P.one_bits = 0x3f800000u;
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);
@@ -1159,6 +1205,8 @@ int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int6
   if (steps) *steps = p->last_steps;
   return EM_OK;
 }
+
+int em_plan_chain(const em_plan* p) { return p ? p->chain : -1; }
 
 int em_plan_last_launches(const em_plan* p, int64_t* launches) {
   if (!p || !launches) return fail(EM_ERR_INVALID, "null");

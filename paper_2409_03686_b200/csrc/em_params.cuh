@@ -120,6 +120,16 @@ struct F32Params {
   float sg[3];      // bound gain (keep folded in, rounded down): r_i = s_i sg_i + sc_i
   float sc[3];      // bound offset (rounded down)
   float shk[3];     // 2D: k = cot(d_1 - d_0); 3D: k1, k2, k3
+  // 2D box on the tangent-ball chain (tangent = 1): axis i stored as
+  // xt_i = x_i / R_i (R_i = |row i of A|), i.e. the whitened point's
+  // coordinate along the unit face normal: the whitened face distances are
+  // bt_i - |xt_i| (ax[] holds R_i for the way back)
+  int tangent;
+  float tbt[2];     // whitened half-widths bhi / R_i
+  float tsb[2];     // stop thresholds bt_i - eps / R_i (<= 0 margin: face within eps)
+  float tcd, tsd;   // cos, sin of the angle between the two face normals (sin > 0)
+  float tim, tip;   // 1 / (1 - cD), 1 / (1 + cD)
+  float tkeep, tsa; // ball radius shrink: rho keep - sa
   float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major
   float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v

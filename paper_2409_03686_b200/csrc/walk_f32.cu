@@ -606,6 +606,68 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, flo
   if (D == 3) x[2] = fmaf(rs, y2, x[2]);
 }
 
+// Walk on tangent balls (EM_CHAIN_TANGENT, 2D box without holes), in the
+// stored coordinates xt_i = x_i / R_i (F32Params::tangent).  In whitened
+// coordinates z (x = A z) the box is a parallelogram whose face i is
+// a_i . z = +-bt_i with unit normal a_i = (row i of A) / R_i, and xt_i =
+// a_i . z, so the whitened face distances are m_i = bt_i - |xt_i|.  For the
+// nearest face i (sign s = sign xt_i, inward normal n = -s a_i) the foot of
+// z is f = z - m n, and the largest ball tangent to face i at f that stays
+// inside the parallelogram has radius
+//   rho = min(bt_i, (bt_j - xt_j(f)) / (1 - s c), (bt_j + xt_j(f)) / (1 + s c))
+// with c = a_i . a_j and xt_j(f) = xt_j + s m c (distances are affine, the
+// ball must clear the opposite face and both faces of the other axis).  rho
+// >= m always (the centred ball of radius m is one such ball), so the ball
+// contains z.  Seen from z at depth m below the tangent point, the exit
+// point of Brownian motion from the ball is the Moebius image of a uniform
+// point: its angle t from the tangent point has tan(t/2) = m / (2 rho - m)
+// tan(psi) with psi uniform in (-pi/2, pi/2).  With N = m sin psi, D =
+// (2 rho - m) cos psi, E = N^2 + D^2 the exit lies at depth 2 rho N^2 / E
+// below the face and tangential offset 2 rho N D / E from the foot -- on the
+// sphere exactly, whatever the rounding of (sin, cos).  Near a face the depth
+// contracts quadratically (m -> ~m^2 / 2 rho) instead of by a factor ~2.
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+struct Tangent {
+  static constexpr bool value =
+      CHAIN == EM_CHAIN_TANGENT && D == 2 && OUTER == OUTER_BOX && NH == 0 && !IDENT;
+};
+
+// One tangent-ball step from x: the 0/1 walking mask (sat of the Euclidean
+// stop margin, as everywhere) and the candidate next point n0, n1.  The
+// caller keeps x for lanes that do not walk (stopped, idle: their candidate
+// is not meaningful).  word: 32 random bits for psi.
+__device__ __forceinline__ float tangent_step(const F32Params& P, const float* x, unsigned word,
+                                              unsigned one_bits, float& n0, float& n1) {
+  const float a0 = fabsf(x[0]), a1 = fabsf(x[1]);
+  const float m0 = P.tbt[0] - a0, m1 = P.tbt[1] - a1;
+  const float wm = __saturatef(fminf(P.tsb[0] - a0, P.tsb[1] - a1) * P.ss_scale);
+  const bool p0 = m0 <= m1;  // nearest face: axis 0
+  const float m = fminf(m0, m1);
+  const float xi = p0 ? x[0] : x[1], xj = p0 ? x[1] : x[0];
+  const float bti = p0 ? P.tbt[0] : P.tbt[1], btj = p0 ? P.tbt[1] : P.tbt[0];
+  const float sg = copysignf(1.0f, xi);                    // s
+  const float scd = sg * P.tcd;                             // s c
+  const float fj = fmaf(m, scd, xj);                       // foot, other axis
+  const bool pos = xi >= 0.0f;
+  const float inv_m = pos ? P.tim : P.tip;                 // 1 / (1 - s c)
+  const float inv_p = pos ? P.tip : P.tim;                 // 1 / (1 + s c)
+  float rho = fminf(bti, fminf((btj - fj) * inv_m, (btj + fj) * inv_p));
+  rho = fmaf(fmaxf(rho, m), P.tkeep, -P.tsa);
+  // psi uniform in [-pi/2, pi/2): 23 bits into the mantissa of 1.0f
+  const float psi = fmaf(__uint_as_float(one_bits | (word >> 9)), kPi, -1.5f * kPi);
+  float sn, cs;
+  __sincosf(psi, &sn, &cs);
+  const float N = m * sn, Dd = fmaf(2.0f, rho, -m) * cs;
+  const float NN = N * N;
+  const float g = fdiv(rho + rho, fmaf(Dd, Dd, NN));
+  const float dep = g * NN, off = g * N * Dd;              // depth below face i, offset along it
+  const float ni = sg * (bti - dep);  // may lie past the centre line: no copysign
+  const float nj = fmaf(off, P.tsd, fmaf(-dep, scd, fj));
+  n0 = p0 ? ni : nj;
+  n1 = p0 ? nj : ni;
+  return wm;
+}
+
 constexpr int kWarps = 8;   // 256 threads per block
 constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
 
@@ -702,7 +764,12 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
   StepAcc acc;
   acc_init(acc);
   if (MODE == 0) stats_smem_init<SMEM>(W);
-  constexpr int K = Batch<D>::kSteps;
+  constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool SCALED = SHEAR || TANG;  // axes stored scaled (to_frame)
+  // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
+  // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
+  constexpr int K = TANG ? 4 : Batch<D>::kSteps;
+  constexpr int NB = TANG ? 1 : Batch<D>::kBlocks;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
@@ -731,7 +798,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
                          : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qb + kQueue * 16u + slot * 4u)
                          : "memory");
-            retire<D, OUTER, NH, BINK, SMEM, SHEAR>(P, ex, __float_as_int(pw), es, acc);
+            retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, __float_as_int(pw), es, acc);
             qn -= 32;
             __syncwarp();
           }
@@ -739,14 +806,14 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
         float xf[3];
-        to_frame<D, OUTER, SHEAR>(P, x, xf);
+        to_frame<D, OUTER, SCALED>(P, x, xf);
         double xd[3] = {(double)x[0], (double)x[1], D == 3 ? (double)x[2] : 0.0};
         if (OUTER == OUTER_BALL && P.rot) {
           double t[3] = {0.0, 0.0, 0.0};
           for (int i = 0; i < D; ++i)
             for (int j = 0; j < D; ++j) t[i] += (double)P.Q[3 * i + j] * xd[j];
           for (int i = 0; i < D; ++i) xd[i] = t[i];
-        } else if (SHEAR) {
+        } else if (SCALED) {
           for (int i = 0; i < D; ++i) xd[i] *= (double)P.ax[i];
         }
         for (int j = 0; j < D; ++j) W.x_out[o * D + j] = xd[j] + (double)P.frame[j];
@@ -775,11 +842,11 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       if (wp.exhausted && live == 0) break;
     }
     // ---- a batch of K steps on one or two Philox blocks, branch-free ----
-    unsigned wv[4 * Batch<D>::kBlocks];
+    unsigned wv[4 * NB];
     const unsigned draw = (unsigned)steps / (unsigned)K;
 #pragma unroll
-    for (int b = 0; b < Batch<D>::kBlocks; ++b) {
-      const uint4 w = philox4x32_10(P.rk, draw * Batch<D>::kBlocks + b, rep_lo, cpid, rep_hi);
+    for (int b = 0; b < NB; ++b) {
+      const uint4 w = philox4x32_10(P.rk, draw * NB + b, rep_lo, cpid, rep_hi);
       wv[4 * b] = w.x;
       wv[4 * b + 1] = w.y;
       wv[4 * b + 2] = w.z;
@@ -797,11 +864,19 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       float wm = 0.0f, sf = 0.0f;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float t, r;
-        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
-        wm = t;  // already the saturated 0/1 mask
-        step<D, OUTER, IDENT, SHEAR>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
-                                     angle_bits<D>(wv, k, P.one_bits));
+        if (TANG) {
+          float n0, n1;
+          wm = tangent_step(P, x, wv[k], P.one_bits, n0, n1);
+          const bool go = wm != 0.0f;
+          x[0] = go ? n0 : x[0];
+          x[1] = go ? n1 : x[1];
+        } else {
+          float t, r;
+          dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
+          wm = t;  // already the saturated 0/1 mask
+          step<D, OUTER, IDENT, SHEAR>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                                       angle_bits<D>(wv, k, P.one_bits));
+        }
         sf += wm;
       }
       walking = wm != 0.0f;
@@ -810,15 +885,21 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       int failed = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float t, r;
-        dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
+        float t, r, n0 = 0.0f, n1 = 0.0f;
+        if (TANG) t = tangent_step(P, x, wv[k], P.one_bits, n0, n1);
+        else dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         const int stop = walking & (t <= 0.0f);
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
-        const float rs = walking ? r : 0.0f;
-        step<D, OUTER, IDENT, SHEAR>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
-                                     angle_bits<D>(wv, k, P.one_bits));
+        if (TANG) {
+          x[0] = walking ? n0 : x[0];
+          x[1] = walking ? n1 : x[1];
+        } else {
+          const float rs = walking ? r : 0.0f;
+          step<D, OUTER, IDENT, SHEAR>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
+                                       angle_bits<D>(wv, k, P.one_bits));
+        }
         steps += walking;
       }
       // budget overruns: report (smallest key wins), drop from the live set
@@ -839,7 +920,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       const ExitQueue& q = q_all[threadIdx.x >> 5];
       const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM, SHEAR>(P, ex, __float_as_int(e.w), q.s[lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
     acc_flush<SMEM>(acc, W);
     stats_smem_flush<SMEM>(W);
@@ -890,6 +971,19 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
       return pick_bin<2, OUTER_BALL, -1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
     }
     if (outer == OUTER_BOX) {
+      if (nh_mode == 0 && chain == EM_CHAIN_TANGENT && !ident) {
+        // the tangent-ball chain exists for this one geometry (capi.cu
+        // resolves EM_CHAIN_TANGENT to EM_CHAIN_MAX everywhere else)
+        if (mode != 0) return walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+        if (bink == BIN_SQUARE)
+          return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_SQUARE, 1>
+                      : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_SQUARE, 0>;
+        if (bink == BIN_GRID)
+          return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
+                      : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
+        return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+      }
       if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink, smem);
       return pick_bin<2, OUTER_BOX, -1, BIN_ANY, BIN_ANY>(mode, chain, ident, bink, smem);
     }

@@ -220,7 +220,7 @@ def test_fp32_cfg1_matches_poisson_kernel(B, chain):
                                                       (3, 32, 400_000, 30_000),
                                                       (4, 16, 200_000, 10_000),
                                                       (5, 8, 100_000, 2_000)])
-@pytest.mark.parametrize("chain", ["woe", "max"])
+@pytest.mark.parametrize("chain", ["woe", "max", "tangent"])
 def test_fp32_matches_oracle_statistically(B, oracle, idx, n_poles, n_fp32, n_ref, chain):
     """FP32 counts vs the oracle's FP64 reference chain at reduced size
     (SURVEY.md Appendix B): exact row sums; entry-wise EXACT conditional
@@ -323,6 +323,22 @@ def _frame_case(golden_cases, name):
 
     k2 = make_tensor(np.array([[2.0, 0.8], [0.8, 1.0]])).k_sqrt
     k3 = make_tensor(np.array([[3.0, 1.0, 0.0], [1.0, 2.0, 0.5], [0.0, 0.5, 1.0]])).k_sqrt
+    if name == "box2d":
+        # square off the origin with a strongly anisotropic K (the tangent
+        # chain's geometry, away from cfg2's square and K)
+        rng = np.random.default_rng(8)
+        pts = np.column_stack([rng.uniform(0.1, 0.7, 80), rng.uniform(0.3, 0.9, 80)])
+        side = np.arange(80) % 4
+        pts[side == 0, 0], pts[side == 1, 0] = 0.1, 0.7
+        pts[side == 2, 1], pts[side == 3, 1] = 0.3, 0.9
+        blk = np.array([[0, 0, 80]], dtype=np.int64)
+        side0 = (pts, blk, np.zeros((1, 4)))
+        side1 = (np.zeros((0, 2)), np.array([[0, 0, 0]], dtype=np.int64), np.zeros((1, 4)))
+        k = make_tensor(np.array([[1.0, -0.9], [-0.9, 1.2]])).k_sqrt
+        gi = np.array([2, 1, 0], dtype=np.int64)
+        gf = np.array([0.4, 0.6, 0.3])  # Box(center, h): [0.1, 0.7] x [0.3, 0.9]
+        poles = np.array([[0.2, 0.5], [0.6, 0.85]])
+        return gi, gf, np.array([0], dtype=np.int8), k, poles, side0, side1
     if name == "box3d":
         rng = np.random.default_rng(7)
         pts = rng.uniform(-0.5, 0.5, size=(90, 3))
@@ -343,12 +359,13 @@ def _frame_case(golden_cases, name):
             (c["a0"], c["blk0"], c["blkf0"]), (c["a1"], c["blk1"], c["blkf1"]))
 
 
-@pytest.mark.parametrize("name", ["disc", "five", "shell3d", "box3d"])
-@pytest.mark.parametrize("chain", ["woe", "max"])
+@pytest.mark.parametrize("name", ["disc", "five", "shell3d", "box3d", "box2d"])
+@pytest.mark.parametrize("chain", ["woe", "max", "tangent"])
 def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, chain):
-    """FP32 (rotated ball frames with holes, sheared 3D box axes) vs the
-    oracle's FP64 reference chain: exact row sums, entry-wise exact binomial
-    tests at family-wise level 1e-4, row chi^2 homogeneity."""
+    """FP32 (rotated ball frames with holes, sheared 3D box axes, the 2D
+    tangent-ball chain) vs the oracle's FP64 reference chain: exact row sums,
+    entry-wise exact binomial tests at family-wise level 1e-4, row chi^2
+    homogeneity."""
     from helpers import P_Z4, exact_two_sample_p
 
     gi, gf, cs, ks, poles, a0, a1 = _frame_case(golden_cases, name)
@@ -372,3 +389,30 @@ def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, c
     rows = row_chi2_pvalues(r.counts, n_fp32, ref, n_ref)
     assert rows.min() > 1e-5 / len(rows), rows.min()
     assert d in (2, 3)
+
+
+def test_fp32_tangent_chain_engages(B):
+    """chain="tangent" runs the tangent-ball step on a 2D box (about 4 steps
+    per walk on cfg2 instead of ~16 for "max") and resolves to "max" where the
+    geometry has no tangent-ball step (annulus, K = I box)."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(2).subset(16)
+    geom = B.pack_geometry(cfg.dom)
+    s0, s1 = B.pack_side(cfg.fam0, 2, cfg.eps), B.pack_side(cfg.fam1, 2, cfg.eps)
+    spw = {}
+    for chain in ("tangent", "max"):
+        with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            r = plan.run(3, 20000)
+        spw[chain] = r.steps_sum.sum() / (16 * 20000)
+    assert spw["tangent"] < 6.0 < 12.0 < spw["max"], spw
+    c3 = configs.get(3).subset(4)
+    with B.Plan(B.pack_geometry(c3.dom), c3.kt.k_sqrt, c3.poles, c3.eps, 10**6,
+                B.pack_side(c3.fam0, 2, c3.eps), B.pack_side(c3.fam1, 2, c3.eps),
+                precision="fp32", chain="tangent") as plan:
+        assert plan.chain == "max"
+    with B.Plan(geom, np.eye(2), cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32",
+                chain="tangent") as plan:
+        assert plan.chain == "max"
