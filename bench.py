@@ -48,7 +48,7 @@ F_STEP = {
     # kernels" derives each entry term by term from walk_f32.cu
     (1, "woe"): (11, 3), (1, "max"): (11, 3),   # K = I: both chains are the sphere step
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
-    (2, "tangent"): (46, 3),                     # tangent balls: ~4x fewer, costlier steps
+    (2, "tangent"): (44, 3),                     # tangent balls: ~4x fewer, costlier steps
     (3, "woe"): (19, 4), (3, "max"): (31, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch

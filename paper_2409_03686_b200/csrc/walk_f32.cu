@@ -616,7 +616,8 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, flo
 // inside the parallelogram has radius
 //   rho = min(bt_i, (bt_j - xt_j(f)) / (1 - s c), (bt_j + xt_j(f)) / (1 + s c))
 // with c = a_i . a_j and xt_j(f) = xt_j + s m c (distances are affine, the
-// ball must clear the opposite face and both faces of the other axis).  rho
+// ball must clear the opposite face and both faces of the other axis; the
+// kernel evaluates it mirrored by s, which removes the sign selects).  rho
 // >= m always (the centred ball of radius m is one such ball), so the ball
 // contains z.  Seen from z at depth m below the tangent point, the exit
 // point of Brownian motion from the ball is the Moebius image of a uniform
@@ -645,13 +646,12 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
   const float m = fminf(m0, m1);
   const float xi = p0 ? x[0] : x[1], xj = p0 ? x[1] : x[0];
   const float bti = p0 ? P.tbt[0] : P.tbt[1], btj = p0 ? P.tbt[1] : P.tbt[0];
+  // work in the frame mirrored by s = sign xt_i (s xt_j, faces j at -+bt_j
+  // swap roles), where the foot is fs = s xt_j + m c and the two face-j
+  // limits are (bt_j - fs) / (1 - c) and (bt_j + fs) / (1 + c): no selects
   const float sg = copysignf(1.0f, xi);                    // s
-  const float scd = sg * P.tcd;                             // s c
-  const float fj = fmaf(m, scd, xj);                       // foot, other axis
-  const bool pos = xi >= 0.0f;
-  const float inv_m = pos ? P.tim : P.tip;                 // 1 / (1 - s c)
-  const float inv_p = pos ? P.tip : P.tim;                 // 1 / (1 + s c)
-  float rho = fminf(bti, fminf((btj - fj) * inv_m, (btj + fj) * inv_p));
+  const float fj = fmaf(m, P.tcd, sg * xj);                // s * foot_j
+  float rho = fminf(bti, fminf((btj - fj) * P.tim, (btj + fj) * P.tip));
   rho = fmaf(fmaxf(rho, m), P.tkeep, -P.tsa);
   // psi uniform in [-pi/2, pi/2): 23 bits into the mantissa of 1.0f
   const float psi = fmaf(__uint_as_float(one_bits | (word >> 9)), kPi, -1.5f * kPi);
@@ -662,7 +662,7 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
   const float g = fdiv(rho + rho, fmaf(Dd, Dd, NN));
   const float dep = g * NN, off = g * N * Dd;              // depth below face i, offset along it
   const float ni = sg * (bti - dep);  // may lie past the centre line: no copysign
-  const float nj = fmaf(off, P.tsd, fmaf(-dep, scd, fj));
+  const float nj = sg * fmaf(off, P.tsd, fmaf(-dep, P.tcd, fj));
   n0 = p0 ? ni : nj;
   n1 = p0 ? nj : ni;
   return wm;
