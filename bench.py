@@ -192,6 +192,9 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
 
 # walks per pole per step of the `--impl reference` arm (~0.2-1 s of CPU work
 # per step on 16 host threads, so a K-step run ends in minutes) ...
+# chain of the committed cfg2 capture (profiles/r01_cfg2_walk_f32_ncu_raw.csv)
+PROFILED_CHAIN = "tangent"
+
 REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
 # ... and of the in-bench `cpu_baseline` leg: about 10 s of CPU work on the
 # GPU box's 16 host threads (cfg1: the whole 3.2e5-walk workload), see
@@ -206,7 +209,7 @@ def profiled_traffic(cfg_index: int, precision: str, chain: str):
     import csv
 
     f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
-    if cfg_index != 2 or precision != "fp32" or chain != "max" or not f.exists():
+    if cfg_index != 2 or precision != "fp32" or chain != PROFILED_CHAIN or not f.exists():
         return None
     vals = {}
     for row in csv.reader(open(f)):
@@ -229,7 +232,7 @@ def profiled_issue(cfg_index: int, precision: str, chain: str):
     import csv
 
     f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
-    if cfg_index != 2 or precision != "fp32" or chain != "max" or not f.exists():
+    if cfg_index != 2 or precision != "fp32" or chain != PROFILED_CHAIN or not f.exists():
         return None
     vals = {row[0]: row[1] for row in csv.reader(open(f)) if len(row) == 3}
     keys = {"issue_active": "smsp__issue_active.avg.pct_of_peak_sustained_active",
