@@ -508,12 +508,15 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->precision = o.precision;
   p->chain = o.chain;
   if (o.precision == EM_PREC_FP32 && o.chain == EM_CHAIN_TANGENT) {
-    // tangent-ball steps exist for 2D boxes without holes and K != I
+    // tangent-ball steps exist for boxes without holes and K != I: 2D boxes,
+    // 3D boxes and the 3D L-box
     bool id = true;
     for (int i = 0; i < d; ++i)
       for (int j = 0; j < d; ++j)
         if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) id = false;
-    if (!(d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0 && !id)) p->chain = EM_CHAIN_MAX;
+    const bool ok2 = d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0;
+    const bool ok3 = d == 3 && g->gi[1] == 1 && nh == 0 && nn <= 1;
+    if (!((ok2 || ok3) && !id)) p->chain = EM_CHAIN_MAX;
   }
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
@@ -688,21 +691,23 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       for (int i = 0; i < d; ++i) shear_g[i] = std::fabs(axd[i]) / Rn[i];
     }
     double tcd = 0.0;
+    double tah[3][3] = {{0.0}};  // unit whitened face normals a_i (rows of A / R_i)
     if (P.tangent) {
       // xt_i = x_i / R_i: the whitened point's coordinate along face normal i
       const double* A = g->ksqrt;
-      double Rn[2], ah[2][2];
-      for (int i = 0; i < 2; ++i) {
-        Rn[i] = std::hypot(A[2 * i], A[2 * i + 1]);
-        ah[i][0] = A[2 * i] / Rn[i];
-        ah[i][1] = A[2 * i + 1] / Rn[i];
-        axd[i] = Rn[i];
+      for (int i = 0; i < d; ++i) {
+        double n2 = 0.0;
+        for (int j = 0; j < d; ++j) n2 += A[i * d + j] * A[i * d + j];
+        axd[i] = std::sqrt(n2);
+        for (int j = 0; j < d; ++j) tah[i][j] = A[i * d + j] / axd[i];
       }
-      tcd = ah[0][0] * ah[1][0] + ah[0][1] * ah[1][1];
-      P.tcd = (float)tcd;
-      P.tsd = (float)std::sqrt(std::max(0.0, 1.0 - tcd * tcd));
-      P.tim = (float)(1.0 / (1.0 - tcd));
-      P.tip = (float)(1.0 / (1.0 + tcd));
+      if (d == 2) {
+        tcd = tah[0][0] * tah[1][0] + tah[0][1] * tah[1][1];
+        P.tcd = (float)tcd;
+        P.tsd = (float)std::sqrt(std::max(0.0, 1.0 - tcd * tcd));
+        P.tim = (float)(1.0 / (1.0 - tcd));
+        P.tip = (float)(1.0 / (1.0 + tcd));
+      }
     }
     for (int i = 0; i < 3; ++i) P.ax[i] = (float)axd[i];
     // world point -> kernel coordinates
@@ -829,18 +834,63 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       // whitened half-widths and stop thresholds; the ball radius is shrunk
       // by keep and by a few ulps of the whitened box (coordinate rounding)
       float sbmin = 0.0f;
-      double btmax = 1.0;
-      for (int i = 0; i < 2; ++i) {
+      double btmax = 1.0, gain = 1.0;
+      for (int i = 0; i < d; ++i) {
         P.tbt[i] = (float)(gf[d] / axd[i]);
         P.tsb[i] = (float)((double)P.tbt[i] - eps / axd[i]);
         sbmin = i == 0 ? P.tsb[i] : std::min(sbmin, P.tsb[i]);
         btmax = std::max(btmax, (double)P.tbt[i]);
       }
+      if (d == 3) {
+        // per nearest face i: cosines, tangent frame, face-limit gains (see
+        // F32Params::t3); the frame of face i: e1 = the unit part of a_j
+        // (j = i + 1) orthogonal to a_i, e2 = a_i x e1
+        for (int i = 0; i < 3; ++i) {
+          float* T = P.t3[i];
+          for (int k = 0; k < 24; ++k) T[k] = 0.0f;
+          const int j = (i + 1) % 3;
+          double C[3], e1[3], e2[3];
+          for (int l = 0; l < 3; ++l)
+            C[l] = tah[i][0] * tah[l][0] + tah[i][1] * tah[l][1] + tah[i][2] * tah[l][2];
+          C[i] = 1.0;
+          for (int k = 0; k < 3; ++k) e1[k] = tah[j][k] - C[j] * tah[i][k];
+          const double en = std::sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+          for (int k = 0; k < 3; ++k) e1[k] /= en;
+          e2[0] = tah[i][1] * e1[2] - tah[i][2] * e1[1];
+          e2[1] = tah[i][2] * e1[0] - tah[i][0] * e1[2];
+          e2[2] = tah[i][0] * e1[1] - tah[i][1] * e1[0];
+          for (int l = 0; l < 3; ++l) {
+            const double bt = (double)P.tbt[l];
+            T[l] = (float)C[l];
+            if (l != i) {
+              T[3 + l] = (float)(tah[l][0] * e1[0] + tah[l][1] * e1[1] + tah[l][2] * e1[2]);
+              T[6 + l] = (float)(tah[l][0] * e2[0] + tah[l][1] * e2[1] + tah[l][2] * e2[2]);
+              T[9 + l] = (float)(bt / (1.0 - C[l]));
+              T[12 + l] = (float)(1.0 / (1.0 - C[l]));
+              gain = std::max(gain, 1.0 / (1.0 - std::fabs(C[l])));
+            } else {
+              T[9 + l] = 3.0e38f;  // no limit from face +bt_i (the tangent face)
+              T[12 + l] = 0.0f;
+            }
+            T[15 + l] = (float)(bt / (1.0 + C[l]));
+            T[18 + l] = (float)(1.0 / (1.0 + C[l]));
+          }
+        }
+        if (nn) {
+          const int off = (d + 1) * (1 + nh);
+          P.tn[0] = (float)((gf[off] - frame[0]) / axd[0]);
+          P.tn[1] = (float)((gf[off + 1] - frame[1]) / axd[1]);
+        }
+      } else {
+        gain = std::max(1.0 / (1.0 - std::fabs(tcd)), 1.0);
+      }
       int ex = 0;
       std::frexp((double)sbmin, &ex);
       P.ss_scale = std::ldexp(1.0f, 25 - ex + 1);
       P.tkeep = P.keep;
-      P.tsa = (float)(btmax * 2.384185791015625e-07);  // 2^-22
+      // a few ulps of the whitened box per coordinate, amplified by the
+      // face-limit gains 1 / (1 -+ c)
+      P.tsa = (float)(btmax * 2.384185791015625e-07 * (d == 3 ? gain : 1.0));  // 2^-22
     }
     P.one_bits = 0x3f800000u;
     P.max_steps = (int)std::min<int64_t>(max_steps, 2147483647LL);

@@ -125,11 +125,20 @@ struct F32Params {
   // coordinate along the unit face normal: the whitened face distances are
   // bt_i - |xt_i| (ax[] holds R_i for the way back)
   int tangent;
-  float tbt[2];     // whitened half-widths bhi / R_i
-  float tsb[2];     // stop thresholds bt_i - eps / R_i (<= 0 margin: face within eps)
+  float tbt[3];     // whitened half-widths bhi / R_i
+  float tsb[3];     // stop thresholds bt_i - eps / R_i (<= 0 margin: face within eps)
   float tcd, tsd;   // cos, sin of the angle between the two face normals (sin > 0)
   float tim, tip;   // 1 / (1 - cD), 1 / (1 + cD)
   float tkeep, tsa; // ball radius shrink: rho keep - sa
+  // 3D box / L-box on the tangent-ball chain: per nearest face i one row of
+  // kTanRow floats (copied to shared memory per block, indexed per lane):
+  //   C[3]  = a_i . a_l (whitened face-normal cosines, C[i] = 1)
+  //   P1[3], P2[3] = a_l . e1, a_l . e2 (orthonormal tangent frame of face i)
+  //   Bm[3] = bt_l / (1 - C_il) (l == i: +huge), tim[3] = 1 / (1 - C_il) (l == i: 0)
+  //   Bp[3] = bt_l / (1 + C_il),                 tip[3] = 1 / (1 + C_il)
+  // padded to 24 floats (six float4) per row
+  float t3[3][24];
+  float tn[2];      // L-box: notch planes in stored coordinates, notch_q / R_q
   float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major
   float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v

@@ -630,7 +630,8 @@ __device__ __forceinline__ void step(const F32Params& P, float* x, float rs, flo
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 struct Tangent {
   static constexpr bool value =
-      CHAIN == EM_CHAIN_TANGENT && D == 2 && OUTER == OUTER_BOX && NH == 0 && !IDENT;
+      CHAIN == EM_CHAIN_TANGENT && NH == 0 && !IDENT &&
+      ((D == 2 && OUTER == OUTER_BOX) || (D == 3 && (OUTER == OUTER_BOX || OUTER == OUTER_LBOX)));
 };
 
 // One tangent-ball step from x: the 0/1 walking mask (sat of the Euclidean
@@ -665,6 +666,82 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
   const float nj = sg * fmaf(off, P.tsd, fmaf(-dep, P.tcd, fj));
   n0 = p0 ? ni : nj;
   n1 = p0 ? nj : ni;
+  return wm;
+}
+
+// 3D box / L-box on tangent balls, same stored coordinates xt_i = a_i . z
+// (F32Params::t3 holds the per-face constants, T below is face i's row in
+// shared memory).  For the nearest face i (side s, depth m), in the frame
+// mirrored by s the foot has coordinates F_l = s xt_l + m C_il (F_i = bt_i)
+// and the ball tangent there must clear the other five faces:
+//   rho <= min_l min((bt_l - F_l) / (1 - C_il), (bt_l + F_l) / (1 + C_il))
+// (l = i: only the opposite face, (bt_i + F_i) / 2 = bt_i).  The L-box adds
+// the notch W = {xt_0 >= tn_0, xt_1 >= tn_1}: its two planes are candidate
+// tangent faces too (depth d_q = tn_q - xt_q, side s = +1; a ball on the
+// far side of either plane misses W), and a ball tangent to a box face must
+// lie beyond one of them: rho <= max_q (tn_q - xt_q(f)) / (1 - s C_iq)
+// (the centre's distance to the half-space W lies in; a sufficient test).
+// Brownian motion from z, on the axis at depth m below the tangent point,
+// leaves the ball at polar angle t from that point with |z - y| uniform in
+// 1 / |z - y| (3D Poisson kernel), i.e. with V uniform the exit lies at depth
+//   dep = (m / den)^2 2 (1 - V) (rho + (rho - m) V),  den = m + 2 (rho - m) V
+// below the face (no cancellation as m -> 0) and at tangential distance
+// sqrt(dep (2 rho - dep)) along a uniform azimuth.  V and the azimuth take
+// 16 bits each of one 32-bit word: 2^32 cells of equal harmonic measure
+// (the midpoint rule of the 3D directions).
+template <int OUTER>
+__device__ __forceinline__ float tangent_step3(const F32Params& P, const float* tab, const float* x,
+                                               unsigned word, unsigned one_bits, float* nx) {
+  const float a0 = fabsf(x[0]), a1 = fabsf(x[1]), a2 = fabsf(x[2]);
+  const float m0 = P.tbt[0] - a0, m1 = P.tbt[1] - a1, m2 = P.tbt[2] - a2;
+  float wm = __saturatef(fminf(fminf(P.tsb[0] - a0, P.tsb[1] - a1), P.tsb[2] - a2) * P.ss_scale);
+  float m = fminf(fminf(m0, m1), m2);
+  int i = m0 == m ? 0 : (m1 == m ? 1 : 2);
+  float sg = copysignf(1.0f, i == 0 ? x[0] : (i == 1 ? x[1] : x[2]));
+  bool notch = false;
+  if (OUTER == OUTER_LBOX) {
+    // Euclidean distance to the notch prism (world units) for the stop test
+    const float qx = fmaf(-P.ax[0], x[0], P.notch[0]), qy = fmaf(-P.ax[1], x[1], P.notch[1]);
+    const float ex = fmaxf(qx, 0.0f), ey = fmaxf(qy, 0.0f);
+    const float en = fsqrt(fmaf(ex, ex, ey * ey));
+    wm = fminf(wm, __saturatef(fmaf(en, P.stop_scale, P.stop_bias)));
+    const float d0 = P.tn[0] - x[0], d1 = P.tn[1] - x[1];
+    const float dn = fmaxf(d0, d1);
+    notch = dn < m;
+    i = notch ? (d0 >= d1 ? 0 : 1) : i;
+    sg = notch ? 1.0f : sg;
+    m = fminf(m, dn);
+  }
+  const float4* T = reinterpret_cast<const float4*>(tab + i * 24);
+  const float4 t0 = T[0], t1 = T[1], t2 = T[2], t3 = T[3], t4 = T[4], t5 = T[5];
+  const float C[3] = {t0.x, t0.y, t0.z}, P1[3] = {t0.w, t1.x, t1.y}, P2[3] = {t1.z, t1.w, t2.x};
+  const float Bm[3] = {t2.y, t2.z, t2.w}, tim[3] = {t3.x, t3.y, t3.z};
+  const float Bp[3] = {t3.w, t4.x, t4.y}, tip[3] = {t4.z, t4.w, t5.x};
+  float F[3], rho = kInf;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    F[l] = fmaf(m, C[l], sg * x[l]);
+    rho = fminf(rho, fminf(fmaf(-F[l], tim[l], Bm[l]), fmaf(F[l], tip[l], Bp[l])));
+  }
+  if (OUTER == OUTER_LBOX) {
+    const bool pos = sg > 0.0f;
+    const float r0 = (P.tn[0] - sg * F[0]) * (pos ? tim[0] : tip[0]);
+    const float r1 = (P.tn[1] - sg * F[1]) * (pos ? tim[1] : tip[1]);
+    rho = notch ? rho : fminf(rho, fmaxf(r0, r1));
+  }
+  rho = fmaf(fmaxf(rho, m), P.tkeep, -P.tsa);
+  // V2 = 2V = (2k + 1) / 2^16 from the high half-word, azimuth from the low
+  const float fv = __uint_as_float(__byte_perm(word, one_bits, 0x7632u));
+  const float v2 = fmaf(fv, 256.0f, -256.0f) + 1.52587890625e-05f;
+  const float h = rho - m;
+  const float g = fdiv(m, fmaf(h, v2, m));
+  const float dep = (g * g) * ((2.0f - v2) * fmaf(0.5f * h, v2, rho));
+  const float tr = fsqrt(fmaxf(dep * fmaf(2.0f, rho, -dep), 0.0f));
+  float sn, cs;
+  __sincosf(angle_of(__byte_perm(word, one_bits, 0x7610u)), &sn, &cs);
+  const float tc = tr * cs, ts = tr * sn;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) nx[l] = sg * fmaf(ts, P2[l], fmaf(tc, P1[l], fmaf(-dep, C[l], F[l])));
   return wm;
 }
 
@@ -766,6 +843,15 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
   if (MODE == 0) stats_smem_init<SMEM>(W);
   constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
   constexpr bool SCALED = SHEAR || TANG;  // axes stored scaled (to_frame)
+  // 3D tangent chain: the per-face constant rows, indexed per lane
+  __shared__ __align__(16) float ttab[(TANG && D == 3) ? 72 : 1];
+  if (TANG && D == 3) {
+    if (threadIdx.x == 0) {  // constant indices: no dynamic parameter-space indexing
+#pragma unroll
+      for (int k = 0; k < 72; ++k) ttab[k] = P.t3[k / 24][k % 24];
+    }
+    __syncthreads();
+  }
   // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
   // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
   constexpr int K = TANG ? 4 : Batch<D>::kSteps;
@@ -865,11 +951,12 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (TANG) {
-          float n0, n1;
-          wm = tangent_step(P, x, wv[k], P.one_bits, n0, n1);
+          float nx[3];
+          if (D == 2) wm = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
+          else wm = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
           const bool go = wm != 0.0f;
-          x[0] = go ? n0 : x[0];
-          x[1] = go ? n1 : x[1];
+#pragma unroll
+          for (int l = 0; l < D; ++l) x[l] = go ? nx[l] : x[l];
         } else {
           float t, r;
           dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
@@ -885,16 +972,17 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       int failed = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float t, r, n0 = 0.0f, n1 = 0.0f;
-        if (TANG) t = tangent_step(P, x, wv[k], P.one_bits, n0, n1);
+        float t, r, nx[3] = {0.0f, 0.0f, 0.0f};
+        if (TANG && D == 2) t = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
+        else if (TANG) t = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
         else dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         const int stop = walking & (t <= 0.0f);
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
         if (TANG) {
-          x[0] = walking ? n0 : x[0];
-          x[1] = walking ? n1 : x[1];
+#pragma unroll
+          for (int l = 0; l < D; ++l) x[l] = walking ? nx[l] : x[l];
         } else {
           const float rs = walking ? r : 0.0f;
           step<D, OUTER, IDENT, SHEAR>(P, x, rs, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
@@ -992,6 +1080,23 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
   if (outer == OUTER_BALL) {
     if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
     return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
+  }
+  if (nh_mode == 0 && chain == EM_CHAIN_TANGENT && !ident && outer != OUTER_BALL) {
+    // 3D box / L-box on tangent balls (capi.cu resolves the chain)
+    if (outer == OUTER_BOX) {
+      if (mode != 0) return walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+      if (bink == BIN_GRID)
+        return smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
+                    : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
+      return smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                  : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+    }
+    if (mode != 0) return walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+    if (bink == BIN_GRID)
+      return smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
+                  : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
+    return smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
   }
   if (outer == OUTER_BOX) {
     if (nh_mode == 0) return pick_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
