@@ -52,6 +52,7 @@ F_STEP = {
     (3, "woe"): (19, 4), (3, "max"): (31, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
+    (5, "tangent"): (101, 5),                    # tangent balls in 3D, notch planes as faces
 }
 
 # the reference chain's FP32 ops per step (same counting

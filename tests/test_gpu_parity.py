@@ -393,8 +393,9 @@ def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, c
 
 def test_fp32_tangent_chain_engages(B):
     """chain="tangent" runs the tangent-ball step on a 2D box (about 4 steps
-    per walk on cfg2 instead of ~16 for "max") and resolves to "max" where the
-    geometry has no tangent-ball step (annulus, K = I box)."""
+    per walk on cfg2 instead of ~16 for "max") and on the 3D L-box (about 6
+    instead of ~39 on cfg5), and resolves to "max" where the geometry has no
+    tangent-ball step (annulus, ball, K = I box)."""
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(2).subset(16)
@@ -416,3 +417,61 @@ def test_fp32_tangent_chain_engages(B):
     with B.Plan(geom, np.eye(2), cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32",
                 chain="tangent") as plan:
         assert plan.chain == "max"
+    # 3D: the L-box (cfg5) walks on tangent balls too, ~6 steps instead of ~39
+    c5 = configs.get(5).subset(8)
+    g5 = B.pack_geometry(c5.dom)
+    t0, t1 = B.pack_side(c5.fam0, 3, c5.eps), B.pack_side(c5.fam1, 3, c5.eps)
+    for chain in ("tangent", "max"):
+        with B.Plan(g5, c5.kt.k_sqrt, c5.poles, c5.eps, 10**6, t0, t1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            r = plan.run(3, 20000)
+        spw["5" + chain] = r.steps_sum.sum() / (8 * 20000)
+    assert spw["5tangent"] < 10.0 < 25.0 < spw["5max"], spw
+    # the unit ball (cfg4) has no tangent-ball step
+    c4 = configs.get(4).subset(4)
+    with B.Plan(B.pack_geometry(c4.dom), c4.kt.k_sqrt, c4.poles, c4.eps, 10**6,
+                B.pack_side(c4.fam0, 3, c4.eps), B.pack_side(c4.fam1, 3, c4.eps),
+                precision="fp32", chain="tangent") as plan:
+        assert plan.chain == "max"
+
+
+@pytest.mark.parametrize("idx,n_poles", [(2, 16), (5, 16)])
+def test_fp32_tangent_matches_max_chain_grouped(B, idx, n_poles):
+    """High-power check of the tangent-ball chain against the max chain (both
+    FP32, the max chain itself checked against the oracle above) at 10^6
+    walks per pole: exact row sums, per-pole Gamma_1 hit fractions within 4.5
+    binomial standard errors (family-wise), and two-sample chi^2 over 64
+    groups of consecutive bins with every per-pole p-value above 1e-4/poles
+    and Fisher's combined p above 1e-4 -- sensitive to biases of ~1e-3 in
+    any group's mass, far below the per-entry tests' reach."""
+    from scipy import stats
+
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(idx).subset(n_poles)
+    geom = B.pack_geometry(cfg.dom)
+    s0, s1 = B.pack_side(cfg.fam0, cfg.d, cfg.eps), B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    n = 10**6
+    res = {}
+    for chain, seed in (("max", 101), ("tangent", 202)):
+        with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            res[chain] = plan.run(seed, n).counts.astype(np.float64)
+    a, b = res["max"], res["tangent"]
+    assert (a.sum(1) == n).all() and (b.sum(1) == n).all()
+    n1 = len(cfg.fam1)
+    f1a, f1b = a[:, -n1:].sum(1) / n, b[:, -n1:].sum(1) / n
+    p = (f1a + f1b) / 2
+    z = (f1b - f1a) / np.sqrt(2 * p * (1 - p) / n)
+    assert np.abs(z).max() < 4.5, z
+    edges = np.linspace(0, a.shape[1], 65).astype(int)[:-1]
+    ga, gb = np.add.reduceat(a, edges, axis=1), np.add.reduceat(b, edges, axis=1)
+    pv = []
+    for i in range(n_poles):
+        tab = np.vstack([ga[i], gb[i]])
+        pv.append(stats.chi2_contingency(tab[:, tab.sum(0) > 0])[1])
+    pv = np.array(pv)
+    assert pv.min() > 1e-4 / n_poles, pv
+    assert stats.combine_pvalues(pv)[1] > 1e-4, pv
