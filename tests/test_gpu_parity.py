@@ -461,8 +461,9 @@ def test_fp32_tangent_matches_max_chain_grouped(B, idx, n_poles):
             res[chain] = plan.run(seed, n).counts.astype(np.float64)
     a, b = res["max"], res["tangent"]
     assert (a.sum(1) == n).all() and (b.sum(1) == n).all()
-    n1 = len(cfg.fam1)
-    f1a, f1b = a[:, -n1:].sum(1) / n, b[:, -n1:].sum(1) / n
+    n0 = len(cfg.fam0) if cfg.fam0 is not None else 0
+    f1a, f1b = (cfg.split(c[:, :n0], c[:, n0:])[1].sum(1) / n for c in (a, b))
+    assert (0 < f1a).all() and (f1a < 1).all()
     p = (f1a + f1b) / 2
     z = (f1b - f1a) / np.sqrt(2 * p * (1 - p) / n)
     assert np.abs(z).max() < 4.5, z
