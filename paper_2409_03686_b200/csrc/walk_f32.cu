@@ -695,9 +695,23 @@ __device__ __forceinline__ float tangent_step3(const F32Params& P, const float* 
   const float a0 = fabsf(x[0]), a1 = fabsf(x[1]), a2 = fabsf(x[2]);
   const float m0 = P.tbt[0] - a0, m1 = P.tbt[1] - a1, m2 = P.tbt[2] - a2;
   float wm = __saturatef(fminf(fminf(P.tsb[0] - a0, P.tsb[1] - a1), P.tsb[2] - a2) * P.ss_scale);
-  float m = fminf(fminf(m0, m1), m2);
-  int i = m0 == m ? 0 : (m1 == m ? 1 : 2);
-  float sg = copysignf(1.0f, i == 0 ? x[0] : (i == 1 ? x[1] : x[2]));
+  // nearest face as a running argmin carrying the face's coordinate and the
+  // offset of its constant row (selects only, no index arithmetic)
+  float m = m0, xi = x[0];
+  int off = 0;
+  {
+    const bool b = m1 < m;
+    m = fminf(m, m1);
+    xi = b ? x[1] : xi;
+    off = b ? 24 : off;
+  }
+  {
+    const bool b = m2 < m;
+    m = fminf(m, m2);
+    xi = b ? x[2] : xi;
+    off = b ? 48 : off;
+  }
+  float sg = copysignf(1.0f, xi);
   bool notch = false;
   if (OUTER == OUTER_LBOX) {
     // Euclidean distance to the notch prism (world units) for the stop test
@@ -708,11 +722,11 @@ __device__ __forceinline__ float tangent_step3(const F32Params& P, const float* 
     const float d0 = P.tn[0] - x[0], d1 = P.tn[1] - x[1];
     const float dn = fmaxf(d0, d1);
     notch = dn < m;
-    i = notch ? (d0 >= d1 ? 0 : 1) : i;
+    off = notch ? (d0 >= d1 ? 0 : 24) : off;
     sg = notch ? 1.0f : sg;
     m = fminf(m, dn);
   }
-  const float4* T = reinterpret_cast<const float4*>(tab + i * 24);
+  const float4* T = reinterpret_cast<const float4*>(tab + off);
   const float4 t0 = T[0], t1 = T[1], t2 = T[2], t3 = T[3], t4 = T[4], t5 = T[5];
   const float C[3] = {t0.x, t0.y, t0.z}, P1[3] = {t0.w, t1.x, t1.y}, P2[3] = {t1.z, t1.w, t2.x};
   const float Bm[3] = {t2.y, t2.z, t2.w}, tim[3] = {t3.x, t3.y, t3.z};
