@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <thread>
 #include <vector>
 
 namespace em {
@@ -76,8 +77,11 @@ bool build_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G
     lo[j] -= margin;
     hi[j] += margin;
   }
-  double h = 0.5 * spacing;
-  const double kMaxCells = d == 3 ? double(1 << 22) : double(1 << 22);
+  // cell edge: a quarter of the anchor spacing in 3D (about 2.2 candidates
+  // per surface cell on cfg5's square families, 6 at half the spacing),
+  // half of it in 2D
+  double h = (d == 3 ? 0.25 : 0.5) * spacing;
+  const double kMaxCells = d == 3 ? double(1 << 23) : double(1 << 22);
   for (;;) {
     double cells = 1.0;
     for (int j = 0; j < d; ++j) cells *= std::ceil((hi[j] - lo[j]) / h);
@@ -132,8 +136,20 @@ bool build_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G
   const double slack = 0.02 * h;
   G.cell.assign(n_cells, 255u);
   G.cand.clear();
+  // band cells are independent: threads take contiguous cell ranges, each
+  // writes its lists into a private buffer (cell word = local offset), and
+  // the buffers are concatenated in range order -- the same grid as a serial
+  // build, whatever the thread count
+  const int n_thr = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  constexpr int64_t kChunk = 2048;  // cells per work item (band cells cluster: interleave)
+  const int64_t n_items = (n_cells + kChunk - 1) / kChunk;
+  std::vector<std::vector<uint32_t>> part(n_items);
+  auto work = [&](int t) {
   std::vector<std::pair<double, int32_t>> found;
-  for (int64_t ci = 0; ci < n_cells; ++ci) {
+  for (int64_t it = t; it < n_items; it += n_thr) {
+  std::vector<uint32_t>& cand = part[it];
+  const int64_t c_lo = it * kChunk, c_hi = std::min<int64_t>(n_cells, c_lo + kChunk);
+  for (int64_t ci = c_lo; ci < c_hi; ++ci) {
     if (!band[ci]) continue;
     const int cx = (int)(ci % n[0]), cy = (int)((ci / n[0]) % n[1]), cz = (int)(ci / ((int64_t)n[0] * n[1]));
     double cc[3] = {lo[0] + (cx + 0.5) * h, lo[1] + (cy + 0.5) * h, d == 3 ? lo[2] + (cz + 0.5) * h : 0.0};
@@ -174,10 +190,30 @@ bool build_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G
         }
     if (found.empty() || found.size() > 254) continue;  // brute force
     std::sort(found.begin(), found.end());  // nearest first: early hits
-    const uint64_t off = G.cand.size();
+    const uint64_t off = cand.size();
     if (off >= (1u << 24)) continue;
-    for (auto& f : found) G.cand.push_back((uint32_t)f.second);
+    for (auto& f : found) cand.push_back((uint32_t)f.second);
     G.cell[ci] = ((uint32_t)off << 8) | (uint32_t)found.size();
+  }
+  }
+  };
+  {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < n_thr; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  // rebase each range's offsets; lists past 2^24 entries fall back to brute force
+  for (int64_t t = 0; t < n_items; ++t) {
+    const uint64_t base = G.cand.size();
+    const int64_t c_lo = t * kChunk, c_hi = std::min<int64_t>(n_cells, c_lo + kChunk);
+    for (int64_t ci = c_lo; ci < c_hi; ++ci) {
+      const uint32_t w = G.cell[ci];
+      if ((w & 255u) == 255u) continue;
+      const uint64_t off = base + (w >> 8);
+      G.cell[ci] = off + (w & 255u) <= (1u << 24) ? (uint32_t)((off << 8) | (w & 255u)) : 255u;
+    }
+    G.cand.insert(G.cand.end(), part[t].begin(), part[t].end());
   }
   if (G.cand.empty()) G.cand.push_back(0);
   for (int j = 0; j < 3; ++j) {

@@ -816,6 +816,9 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 #ifndef EM_MIN_BLOCKS
 #define EM_MIN_BLOCKS 0
 #endif
+#ifndef EM_TAB_WARP
+#define EM_TAB_WARP 0
+#endif
 #define EM_MINB(D) (EM_MIN_BLOCKS > 0 ? EM_MIN_BLOCKS : ((D) == 2 ? 5 : 4))
 // Per-warp exit queue in shared memory: exit point + pole (as int bits in
 // .w) and step count, binned 32 at a time.
@@ -858,6 +861,18 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
   constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
   constexpr bool SCALED = SHEAR || TANG;  // axes stored scaled (to_frame)
   // 3D tangent chain: the per-face constant rows, indexed per lane
+#if EM_TAB_WARP
+  // one copy per warp (warp-synchronous fill: no block barrier)
+  __shared__ __align__(16) float ttab_all[(TANG && D == 3) ? 72 * kWarps : 1];
+  float* ttab = ttab_all + ((TANG && D == 3) ? 72 * (threadIdx.x >> 5) : 0);
+  if (TANG && D == 3) {
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+      for (int k = 0; k < 72; ++k) ttab[k] = P.t3[k / 24][k % 24];
+    }
+    __syncwarp();
+  }
+#else
   __shared__ __align__(16) float ttab[(TANG && D == 3) ? 72 : 1];
   if (TANG && D == 3) {
     if (threadIdx.x == 0) {  // constant indices: no dynamic parameter-space indexing
@@ -866,6 +881,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
     }
     __syncthreads();
   }
+#endif
   // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
   // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
   constexpr int K = TANG ? 4 : Batch<D>::kSteps;
