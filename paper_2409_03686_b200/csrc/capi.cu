@@ -516,7 +516,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) id = false;
     const bool ok2 = d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0;
     const bool ok3 = d == 3 && g->gi[1] == 1 && nh == 0 && nn <= 1;
-    if (!((ok2 || ok3) && !id)) p->chain = EM_CHAIN_MAX;
+    const bool okb = d == 3 && g->gi[1] == 0 && nh == 0 && nn == 0;  // rolling balls
+    if (!((ok2 || ok3 || okb) && !id)) p->chain = EM_CHAIN_MAX;
   }
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
@@ -644,6 +645,19 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     P.shear = (g->gi[1] == 1 && nh == 0 && p->chain == EM_CHAIN_MAX && !ident && (d == 3 || nn == 0)) ? 1 : 0;
     P.tangent = p->chain == EM_CHAIN_TANGENT ? 1 : 0;
     if (P.rot) sym_eig(g->ksqrt, d, Adiag, Qd);
+    if (P.rot && P.tangent) {
+      // rolling-ball radius: the whitened ellipsoid {z : |diag(Ad) z| <= R}
+      // has semi-axes R / Ad_i and smallest curvature radius R min / max^2
+      double amin = Adiag[0], amax = Adiag[0];
+      for (int i = 1; i < d; ++i) {
+        amin = std::min(amin, Adiag[i]);
+        amax = std::max(amax, Adiag[i]);
+      }
+      const double rb = gf[d] * amin / (amax * amax) * (1.0 - 1e-6);
+      P.rho_b = (float)rb;
+      P.rho_b2 = (float)(rb * rb);
+      for (int i = 0; i < d; ++i) P.ia[i] = (float)(1.0 / Adiag[i]);
+    }
     for (int i = 0; i < 3; ++i) {
       P.Ad[i] = (float)Adiag[i];
       P.Kd[i] = (float)(Adiag[i] * Adiag[i]);
@@ -692,7 +706,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     }
     double tcd = 0.0;
     double tah[3][3] = {{0.0}};  // unit whitened face normals a_i (rows of A / R_i)
-    if (P.tangent) {
+    if (P.tangent && g->gi[1] == 1) {  // boxes (balls roll, see below)
       // xt_i = x_i / R_i: the whitened point's coordinate along face normal i
       const double* A = g->ksqrt;
       for (int i = 0; i < d; ++i) {
@@ -830,7 +844,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       std::frexp((double)sbmin, &ex);  // sb in [2^(ex-1), 2^ex), ulp = 2^(ex-24)
       P.ss_scale = std::ldexp(1.0f, 25 - ex + 1);
     }
-    if (P.tangent) {
+    if (P.tangent && g->gi[1] == 1) {  // boxes (balls roll, see below)
       // whitened half-widths and stop thresholds; the ball radius is shrunk
       // by keep and by a few ulps of the whitened box (coordinate rounding)
       float sbmin = 0.0f;

@@ -139,6 +139,11 @@ struct F32Params {
   // padded to 24 floats (six float4) per row
   float t3[3][24];
   float tn[2];      // L-box: notch planes in stored coordinates, notch_q / R_q
+  // 3D ball on the tangent chain (rolling balls, rotated frame A = diag(Ad)):
+  // whitened balls of radius rho_b (<= the smallest curvature radius of the
+  // whitened ellipsoid, R min(Ad) / max(Ad)^2) roll freely inside it
+  float rho_b, rho_b2;
+  float ia[3];      // 1 / Ad
   float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major
   float Kq[6];      // K = A^T A as (K00, K11, K22, 2 K01, 2 K02, 2 K12): |Av|^2 = v^T K v

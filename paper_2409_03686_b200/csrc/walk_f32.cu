@@ -759,6 +759,82 @@ __device__ __forceinline__ float tangent_step3(const F32Params& P, const float* 
   return wm;
 }
 
+// 3D ball on the tangent chain: walk on ROLLING balls.  In whitened
+// coordinates z (x = diag(Ad) z in the rotated frame) the domain is the
+// ellipsoid |diag(Ad) z| <= R, inside which every ball of radius rho_b (its
+// smallest curvature radius) rolls freely: the ball of that radius
+// internally tangent at any boundary point p lies in the domain (Blaschke).
+// p is the radial projection of x onto the sphere |x| = R; its inward
+// whitened normal is -diag(Ad) x / |Ax|, so with al = 1 - R / |x| and
+// be = rho_b / |Ax| the offset from the ball's centre is
+//   w = z - c = x (al / Ad + be Ad)          (per axis: one FFMA, one FMUL)
+// and z lies in the ball's near half (towards p) iff al |x|^2 + be |Ax|^2 > 0.
+// There the step samples the ball's harmonic measure from the off-centre
+// point z (distance d = |w| from the centre, axis w / d: the 3D Poisson
+// kernel, same depth formula as tangent_step3 with m = rho_b - d, on the
+// ball's own axis); elsewhere it is the max chain's centred ball (d = 0, the
+// same formula gives the uniform sphere).  Near the boundary z sits close to
+// p on the ball's axis, so the depth contracts quadratically (cfg4: 35.6 ->
+// ~7 steps per walk).  The orthonormal frame around the axis is Duff et
+// al.'s branch-free construction.
+__device__ __forceinline__ float rsq(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, unsigned word,
+                                            unsigned one_bits, float* nx) {
+  const float p0 = x[0] * x[0], p1 = x[1] * x[1], p2 = x[2] * x[2];
+  const float s2 = p0 + p1 + p2;
+  const float aa = fmaf(P.Kd[0], p0, fmaf(P.Kd[1], p1, P.Kd[2] * p2));
+  const float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
+  const float iaa = rsq(aa);
+  const float sa = aa * iaa;  // |Ax|
+  // max chain: the largest centred whitened ball, r = q / (|Ax| + sqrt(|Ax|^2 + q))
+  const float q = P.oR2 - s2;
+  const float rm = fmaf(fdiv(q, sa + fsqrt(fmaxf(aa + q, 0.0f))), P.keep, -P.shrink_abs);
+  // rolling ball tangent at the radial projection
+  const float al = fmaf(-P.oR, rsq(s2), 1.0f);
+  const float be = P.rho_b * iaa;
+  const float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
+  const float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
+  const float w2 = x[2] * fmaf(al, P.ia[2], be * P.Ad[2]);
+  const float d2 = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+  const bool roll = (d2 < P.rho_b2) & (fmaf(al, s2, be * aa) > 0.0f);
+  const float rho = roll ? P.rho_b : rm;
+  const float id = rsq(fmaxf(d2, 1e-30f));
+  const float d = roll ? d2 * id : 0.0f;
+  const float e0 = roll ? w0 * id : 0.0f, e1 = roll ? w1 * id : 0.0f, e2 = roll ? w2 * id : 1.0f;
+  const float m = rho - d;
+  // V2 = 2V from the high half-word, azimuth from the low one
+  const float fv = __uint_as_float(__byte_perm(word, one_bits, 0x7632u));
+  const float v2 = fmaf(fv, 256.0f, -256.0f) + 1.52587890625e-05f;
+  const float g = fdiv(m, fmaf(d, v2, m));
+  const float dep = (g * g) * ((2.0f - v2) * fmaf(0.5f * d, v2, rho));
+  const float tr = fsqrt(fmaxf(dep * fmaf(2.0f, rho, -dep), 0.0f));
+  float sn, cs;
+  __sincosf(angle_of(__byte_perm(word, one_bits, 0x7610u)), &sn, &cs);
+  const float tc = tr * cs, ts = tr * sn;
+  // Duff et al.: (b1, b2, e) orthonormal, branch-free
+  const float sg = copysignf(1.0f, e2);
+  const float A = -fdiv(1.0f, sg + e2);
+  const float B = e0 * e1 * A;
+  const float b10 = fmaf(sg * e0 * e0, A, 1.0f), b11 = sg * B, b12 = -sg * e0;
+  const float b20 = B, b21 = fmaf(e1 * e1, A, sg), b22 = -e1;
+  const float h = m - dep;
+  nx[0] = fmaf(P.Ad[0], fmaf(h, e0, fmaf(tc, b10, ts * b20)), x[0]);
+  nx[1] = fmaf(P.Ad[1], fmaf(h, e1, fmaf(tc, b11, ts * b21)), x[1]);
+  nx[2] = fmaf(P.Ad[2], fmaf(h, e2, fmaf(tc, b12, ts * b22)), x[2]);
+  return wm;
+}
+
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+struct Roll {
+  static constexpr bool value =
+      CHAIN == EM_CHAIN_TANGENT && D == 3 && OUTER == OUTER_BALL && NH == 0 && !IDENT;
+};
+
 constexpr int kWarps = 8;   // 256 threads per block
 constexpr int kQueue = 64;  // deferred exits per warp (binned 32 at a time)
 
@@ -859,6 +935,7 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
   acc_init(acc);
   if (MODE == 0) stats_smem_init<SMEM>(W);
   constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool ROLL = Roll<D, OUTER, NH, CHAIN, IDENT>::value;
   constexpr bool SCALED = SHEAR || TANG;  // axes stored scaled (to_frame)
   // 3D tangent chain: the per-face constant rows, indexed per lane
 #if EM_TAB_WARP
@@ -884,8 +961,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
 #endif
   // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
   // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
-  constexpr int K = TANG ? 4 : Batch<D>::kSteps;
-  constexpr int NB = TANG ? 1 : Batch<D>::kBlocks;
+  constexpr int K = (TANG || ROLL) ? 4 : Batch<D>::kSteps;
+  constexpr int NB = (TANG || ROLL) ? 1 : Batch<D>::kBlocks;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
@@ -980,9 +1057,10 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       float wm = 0.0f, sf = 0.0f;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        if (TANG) {
+        if (TANG || ROLL) {
           float nx[3];
-          if (D == 2) wm = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
+          if (ROLL) wm = roll_step3(P, x, wv[k], P.one_bits, nx);
+          else if (D == 2) wm = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
           else wm = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
           const bool go = wm != 0.0f;
 #pragma unroll
@@ -1003,14 +1081,15 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         float t, r, nx[3] = {0.0f, 0.0f, 0.0f};
-        if (TANG && D == 2) t = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
+        if (ROLL) t = roll_step3(P, x, wv[k], P.one_bits, nx);
+        else if (TANG && D == 2) t = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
         else if (TANG) t = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
         else dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         const int stop = walking & (t <= 0.0f);
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);
         failed |= over;
         walking &= (stop ^ 1) & (over ^ 1);
-        if (TANG) {
+        if (TANG || ROLL) {
 #pragma unroll
           for (int l = 0; l < D; ++l) x[l] = walking ? nx[l] : x[l];
         } else {
@@ -1108,6 +1187,15 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
     return nullptr;
   }
   if (outer == OUTER_BALL) {
+    if (nh_mode == 0 && chain == EM_CHAIN_TANGENT && !ident) {
+      // rolling balls (capi.cu resolves the chain)
+      if (mode != 0) return walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+      if (bink == BIN_GRID)
+        return smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
+                    : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
+      return smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                  : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+    }
     if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
     return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
   }

@@ -393,9 +393,10 @@ def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, c
 
 def test_fp32_tangent_chain_engages(B):
     """chain="tangent" runs the tangent-ball step on a 2D box (about 4 steps
-    per walk on cfg2 instead of ~16 for "max") and on the 3D L-box (about 6
-    instead of ~39 on cfg5), and resolves to "max" where the geometry has no
-    tangent-ball step (annulus, ball, K = I box)."""
+    per walk on cfg2 instead of ~16 for "max"), on the 3D L-box (about 6
+    instead of ~39 on cfg5) and on rolling balls in the 3D ball (about 7
+    instead of ~36 on cfg4), and resolves to "max" where the geometry has no
+    tangent-ball step (annulus, K = I box)."""
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(2).subset(16)
@@ -428,15 +429,20 @@ def test_fp32_tangent_chain_engages(B):
             r = plan.run(3, 20000)
         spw["5" + chain] = r.steps_sum.sum() / (8 * 20000)
     assert spw["5tangent"] < 10.0 < 25.0 < spw["5max"], spw
-    # the unit ball (cfg4) has no tangent-ball step
-    c4 = configs.get(4).subset(4)
-    with B.Plan(B.pack_geometry(c4.dom), c4.kt.k_sqrt, c4.poles, c4.eps, 10**6,
-                B.pack_side(c4.fam0, 3, c4.eps), B.pack_side(c4.fam1, 3, c4.eps),
-                precision="fp32", chain="tangent") as plan:
-        assert plan.chain == "max"
+    # the unit ball (cfg4) walks on rolling balls: ~7 steps instead of ~36
+    c4 = configs.get(4).subset(8)
+    g4 = B.pack_geometry(c4.dom)
+    b0, b1 = B.pack_side(c4.fam0, 3, c4.eps), B.pack_side(c4.fam1, 3, c4.eps)
+    for chain in ("tangent", "max"):
+        with B.Plan(g4, c4.kt.k_sqrt, c4.poles, c4.eps, 10**6, b0, b1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            r = plan.run(3, 20000)
+        spw["4" + chain] = r.steps_sum.sum() / (8 * 20000)
+    assert spw["4tangent"] < 12.0 < 25.0 < spw["4max"], spw
 
 
-@pytest.mark.parametrize("idx,n_poles", [(2, 16), (5, 16)])
+@pytest.mark.parametrize("idx,n_poles", [(2, 16), (4, 16), (5, 16)])
 def test_fp32_tangent_matches_max_chain_grouped(B, idx, n_poles):
     """High-power check of the tangent-ball chain against the max chain (both
     FP32, the max chain itself checked against the oracle above) at 10^6

@@ -60,6 +60,11 @@ s0 = B.pack_side(cfg.fam0, 3, cfg.eps)
 s1 = B.pack_side(cfg.fam1, 3, cfg.eps)
 compare("cfg5", cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, s0, s1, n, len(cfg.fam1))
 
+# cfg4 (ball, rolling balls)
+c4 = configs.get(4).subset(16)
+compare("cfg4", c4.dom, c4.kt.k_sqrt, c4.poles, c4.eps, B.pack_side(c4.fam0, 3, c4.eps),
+        B.pack_side(c4.fam1, 3, c4.eps), n, 1024)
+
 # off-centre anisotropic 3D box with generic anchors
 rng = np.random.default_rng(5)
 c, h = np.array([0.3, -0.2, 0.1]), 0.4
