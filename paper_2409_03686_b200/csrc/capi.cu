@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -55,6 +56,27 @@ struct GridHost {
   std::vector<uint32_t> cand;
 };
 bool build_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G);
+
+// A candidate grid resident on one device (cell words then candidate lists in
+// one allocation), shared by every plan over the same anchors: plans hold a
+// reference, so the cache may evict an entry while plans still use it.
+struct DeviceGrid {
+  double lo[3] = {0, 0, 0};
+  double h = 0.0;
+  int n[3] = {1, 1, 1};
+  int device = -1;
+  void* dev = nullptr;
+  const uint32_t* cell = nullptr;
+  const uint32_t* cand = nullptr;
+  ~DeviceGrid() {
+    if (!dev) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    cudaFree(dev);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  }
+};
 }  // namespace em
 
 using namespace em;
@@ -249,6 +271,7 @@ struct em_plan {
   int64_t last_walks = 0, last_steps = 0, last_launches = 0, last_n_rep = 0;
   bool last_timed = false;  // ev0 / ev1 bracket the last walk kernel
   cudaStream_t last_stream = nullptr;  // stream of the last run_device
+  std::vector<std::shared_ptr<DeviceGrid>> grids;  // device-resident candidate grids in use
   ~em_plan() {
     // buffers go back to the shared cache: nothing in flight may still use them
     if (stream) cudaStreamSynchronize(stream);
@@ -356,10 +379,12 @@ double sym_min_eig(const double* a_in, int d) {
   return m;
 }
 
-// Host-side cache of candidate grids: building one is a deterministic
-// function of (anchors, d, eps) and costs up to ~0.1-1 s for 8k anchors, so
-// repeated plans over the same bins (one per API call) reuse it.
-bool cached_grid(const double* anchors, int64_t m, int d, double eps, GridHost& G) {
+// Device-resident cache of candidate grids: a grid is a deterministic
+// function of (anchors, d, eps), costs up to ~1 s of host time for 8k
+// anchors and tens of MB, so repeated plans over the same bins (one per API
+// call) reuse the device copy instead of rebuilding and re-uploading it.
+std::shared_ptr<DeviceGrid> cached_device_grid(const double* anchors, int64_t m, int d, double eps,
+                                               int device) {
   uint64_t h = 1469598103934665603ULL;
   auto mix = [&](const void* p, size_t n) {
     const unsigned char* b = (const unsigned char*)p;
@@ -369,21 +394,38 @@ bool cached_grid(const double* anchors, int64_t m, int d, double eps, GridHost& 
   mix(&m, sizeof(m));
   mix(&d, sizeof(d));
   mix(&eps, sizeof(eps));
+  mix(&device, sizeof(device));
   static std::mutex mu;
-  static std::vector<std::pair<uint64_t, GridHost>> lru;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto& e : lru)
-      if (e.first == h) {
-        G = e.second;
-        return true;
-      }
-  }
-  if (!build_grid(anchors, m, d, eps, G)) return false;
+  static std::vector<std::pair<uint64_t, std::shared_ptr<DeviceGrid>>> lru;
   std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : lru)
+    if (e.first == h) return e.second;
+  GridHost G;
+  if (!build_grid(anchors, m, d, eps, G)) return nullptr;
+  auto D = std::make_shared<DeviceGrid>();
+  const size_t cb = G.cell.size() * 4, nb = G.cand.size() * 4;
+  D->device = device;
+  if (cudaMalloc(&D->dev, cb + nb) != cudaSuccess) {
+    D->dev = nullptr;
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemcpy(D->dev, G.cell.data(), cb, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(static_cast<char*>(D->dev) + cb, G.cand.data(), nb, cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  D->cell = static_cast<const uint32_t*>(D->dev);
+  D->cand = reinterpret_cast<const uint32_t*>(static_cast<char*>(D->dev) + cb);
+  for (int j = 0; j < 3; ++j) {
+    D->lo[j] = G.lo[j];
+    D->n[j] = G.n[j];
+  }
+  D->h = G.h;
   if (lru.size() >= 8) lru.erase(lru.begin());
-  lru.push_back({h, G});
-  return true;
+  lru.push_back({h, D});
+  return D;
 }
 
 int validate_geometry(const em_geometry* g) {
@@ -938,16 +980,16 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       put(af.data(), (size_t)S->n_anchors * 16, (void**)&D.anchors);
       // one generic block covering the family: accelerate with the grid
       if (D.n_blk == 1 && D.kind[0] == BLK_GENERIC && S->n_anchors > 8) {
-        GridHost G;
-        if (cached_grid(S->anchors, S->n_anchors, d, eps, G)) {
-          put(G.cell.data(), G.cell.size() * 4, (void**)&D.grid.cell);
-          put(G.cand.data(), G.cand.size() * 4, (void**)&D.grid.cand);
+        if (auto G = cached_device_grid(S->anchors, S->n_anchors, d, eps, o.device)) {
+          D.grid.cell = G->cell;
+          D.grid.cand = G->cand;
           D.has_grid = 1;
           for (int j = 0; j < 3; ++j) {
-            D.grid.lo[j] = (float)G.lo[j];
-            D.grid.n[j] = G.n[j];
+            D.grid.lo[j] = (float)G->lo[j];
+            D.grid.n[j] = G->n[j];
           }
-          D.grid.inv_h = (float)(1.0 / G.h);
+          D.grid.inv_h = (float)(1.0 / G->h);
+          p->grids.push_back(G);
         }
       }
     }
