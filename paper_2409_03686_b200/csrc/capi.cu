@@ -559,7 +559,11 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     const bool ok2 = d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0;
     const bool ok3 = d == 3 && g->gi[1] == 1 && nh == 0 && nn <= 1;
     const bool okb = d == 3 && g->gi[1] == 0 && nh == 0 && nn == 0;  // rolling balls
-    if (!((ok2 || ok3 || okb) && !id)) p->chain = EM_CHAIN_MAX;
+    // 2D: rolling disks in the ball, with at most one hole, concentric
+    bool conc = nh == 1;
+    for (int j = 0; conc && j < d; ++j) conc = g->gf[d + 1 + j] == g->gf[j];
+    const bool okd = d == 2 && g->gi[1] == 0 && nn == 0 && (nh == 0 || conc);
+    if (!((ok2 || ok3 || okb || okd) && !id)) p->chain = EM_CHAIN_MAX;
   }
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
@@ -695,7 +699,17 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         amin = std::min(amin, Adiag[i]);
         amax = std::max(amax, Adiag[i]);
       }
-      const double rb = gf[d] * amin / (amax * amax) * (1.0 - 1e-6);
+      double rb = gf[d] * amin / (amax * amax);
+      if (nh == 1) {
+        // annulus: every point y of a disk of radius r tangent at p has
+        // | |x_y| - |x_p| | <= 2 r max(Ad), so r = (R - rho) / (2 max Ad)
+        // keeps the outer disks off the hole and the hole's disks inside R
+        const double lim = (gf[d] - gf[d + 1 + d]) / (2.0 * amax);
+        rb = std::min(rb, lim);
+        P.rho_h = (float)(lim * (1.0 - 1e-6));
+        P.rho_h2 = (float)((double)P.rho_h * (double)P.rho_h);
+      }
+      rb *= 1.0 - 1e-6;
       P.rho_b = (float)rb;
       P.rho_b2 = (float)(rb * rb);
       for (int i = 0; i < d; ++i) P.ia[i] = (float)(1.0 / Adiag[i]);

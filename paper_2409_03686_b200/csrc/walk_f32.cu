@@ -829,10 +829,82 @@ __device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, 
   return wm;
 }
 
+// 2D ball / concentric annulus on the tangent chain: the same rolling disks
+// for the outer ellipse (radius rho_b, capped so the disk also clears the
+// hole), and for the hole the disk of radius rho_h externally tangent at the
+// radial projection onto the hole: it misses the (convex) hole whatever its
+// radius, and rho_h = (R - rho) / (2 max Ad) keeps it inside the outer
+// circle.  The exit from an off-centre point of a disk is the Moebius image
+// of a uniform angle (tangent_step's formula with m = radius - d on the
+// disk's own axis); the centred max-chain disk is the d = 0 case.
+template <int NH>
+__device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, unsigned word,
+                                            unsigned one_bits, float* nx) {
+  const float p0 = x[0] * x[0], p1 = x[1] * x[1];
+  const float s2 = p0 + p1;
+  const float aa = fmaf(P.Kd[0], p0, P.Kd[1] * p1);
+  float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
+  if (NH == 1) wm = fminf(wm, __saturatef(fmaf(s2, P.h2_scale, P.h2_bias)));
+  const float iaa = rsq(aa);
+  const float sa = aa * iaa;  // |Ax|
+  const float ir = rsq(s2);
+  // max chain: the largest centred whitened disk
+  float rm;
+  if (NH == 0) {
+    const float q = P.oR2 - s2;
+    rm = fmaf(fdiv(q, sa + fsqrt(fmaxf(aa + q, 0.0f))), P.keep, -P.shrink_abs);
+  } else {
+    const float qo = P.oR2 - s2;
+    const float Do = sa + fsqrt(fmaxf(aa + qo, 0.0f));
+    const float qh = s2 - P.hr2[0];
+    const float Dh = sa + fsqrt(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
+    const bool outer = qo * Dh <= qh * Do;
+    rm = fmaf(fdiv(outer ? qo : qh, outer ? Do : Dh), P.keep, -P.shrink_abs);
+  }
+  // rolling disk at the outer ellipse
+  const float al = fmaf(-P.oR, ir, 1.0f);
+  const float be = P.rho_b * iaa;
+  float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
+  float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
+  float d2 = fmaf(w0, w0, w1 * w1);
+  bool use = (d2 < P.rho_b2) & (fmaf(al, s2, be * aa) > 0.0f);
+  float rho = use ? P.rho_b : rm;
+  if (NH == 1) {
+    // disk tangent to the hole from outside, centre beyond the radial projection
+    const float ah = fmaf(-P.hr[0], ir, 1.0f);
+    const float bh = P.rho_h * iaa;
+    const float v0 = x[0] * fmaf(ah, P.ia[0], -bh * P.Ad[0]);
+    const float v1 = x[1] * fmaf(ah, P.ia[1], -bh * P.Ad[1]);
+    const float dh = fmaf(v0, v0, v1 * v1);
+    const bool uh = !use & (dh < P.rho_h2) & (fmaf(ah, s2, -bh * aa) < 0.0f);
+    w0 = uh ? v0 : w0;
+    w1 = uh ? v1 : w1;
+    d2 = uh ? dh : d2;
+    rho = uh ? P.rho_h : rho;
+    use |= uh;
+  }
+  const float id = rsq(fmaxf(d2, 1e-30f));
+  const float d = use ? d2 * id : 0.0f;
+  const float e0 = use ? w0 * id : 1.0f, e1 = use ? w1 * id : 0.0f;
+  const float m = rho - d;
+  // Moebius: psi uniform in [-pi/2, pi/2) from 23 bits
+  const float psi = fmaf(__uint_as_float(one_bits | (word >> 9)), kPi, -1.5f * kPi);
+  float sn, cs;
+  __sincosf(psi, &sn, &cs);
+  const float N = m * sn, Dd = fmaf(2.0f, rho, -m) * cs;
+  const float NN = N * N;
+  const float g = fdiv(rho + rho, fmaf(Dd, Dd, NN));
+  const float dep = g * NN, off = g * N * Dd;
+  const float h = m - dep;
+  nx[0] = fmaf(P.Ad[0], fmaf(h, e0, -off * e1), x[0]);
+  nx[1] = fmaf(P.Ad[1], fmaf(h, e1, off * e0), x[1]);
+  return wm;
+}
+
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
 struct Roll {
-  static constexpr bool value =
-      CHAIN == EM_CHAIN_TANGENT && D == 3 && OUTER == OUTER_BALL && NH == 0 && !IDENT;
+  static constexpr bool value = CHAIN == EM_CHAIN_TANGENT && OUTER == OUTER_BALL && !IDENT &&
+                                ((D == 3 && NH == 0) || (D == 2 && (NH == 0 || NH == 1)));
 };
 
 constexpr int kWarps = 8;   // 256 threads per block
@@ -896,6 +968,12 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
 #define EM_TAB_WARP 0
 #endif
 #define EM_MINB(D) (EM_MIN_BLOCKS > 0 ? EM_MIN_BLOCKS : ((D) == 2 ? 5 : 4))
+// 2D rolling disks carry more state per step: fewer resident blocks
+#ifndef EM_ROLL2_BLOCKS
+#define EM_ROLL2_BLOCKS 4
+#endif
+#define EM_MINB_K(D, OUTER, CHAIN) \
+  ((D) == 2 && (OUTER) == OUTER_BALL && (CHAIN) == EM_CHAIN_TANGENT ? EM_ROLL2_BLOCKS : EM_MINB(D))
 // Per-warp exit queue in shared memory: exit point + pole (as int bits in
 // .w) and step count, binned 32 at a time.
 struct ExitQueue {
@@ -904,7 +982,7 @@ struct ExitQueue {
 };
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT, int MODE, int BINK, int SMEM>
-__global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Params P) {
+__global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kernel(const F32Params P) {
   const WorkOut& W = P.w;
   constexpr bool SHEAR = Shear<D, OUTER, NH, CHAIN, IDENT>::value;
   __shared__ ExitQueue q_all[kWarps];
@@ -1059,7 +1137,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
       for (int k = 0; k < K; ++k) {
         if (TANG || ROLL) {
           float nx[3];
-          if (ROLL) wm = roll_step3(P, x, wv[k], P.one_bits, nx);
+          if (ROLL && D == 3) wm = roll_step3(P, x, wv[k], P.one_bits, nx);
+          else if (ROLL) wm = roll_step2<NH>(P, x, wv[k], P.one_bits, nx);
           else if (D == 2) wm = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
           else wm = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
           const bool go = wm != 0.0f;
@@ -1081,7 +1160,8 @@ __global__ void __launch_bounds__(256, EM_MINB(D)) walk_f32_kernel(const F32Para
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         float t, r, nx[3] = {0.0f, 0.0f, 0.0f};
-        if (ROLL) t = roll_step3(P, x, wv[k], P.one_bits, nx);
+        if (ROLL && D == 3) t = roll_step3(P, x, wv[k], P.one_bits, nx);
+        else if (ROLL) t = roll_step2<NH>(P, x, wv[k], P.one_bits, nx);
         else if (TANG && D == 2) t = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
         else if (TANG) t = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
         else dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
@@ -1162,6 +1242,23 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
                           int smem) {
   using namespace f32;
   if (d == 2) {
+    if (outer == OUTER_BALL && nh_mode <= 1 && chain == EM_CHAIN_TANGENT && !ident) {
+      // rolling disks (capi.cu resolves the chain: no hole or one concentric hole)
+      if (nh_mode == 0) {
+        if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+        if (bink == BIN_CIRCLE)
+          return smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 1>
+                      : walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 0>;
+        return smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+      }
+      if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
+      if (bink == BIN_CIRCLE)
+        return smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 1>
+                    : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 0>;
+      return smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                  : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+    }
     if (outer == OUTER_BALL) {
       if (nh_mode == 0) return pick_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
       if (nh_mode == 1) return pick_bin<2, OUTER_BALL, 1, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);

@@ -394,9 +394,10 @@ def test_fp32_frames_match_oracle_statistically(B, oracle, golden_cases, name, c
 def test_fp32_tangent_chain_engages(B):
     """chain="tangent" runs the tangent-ball step on a 2D box (about 4 steps
     per walk on cfg2 instead of ~16 for "max"), on the 3D L-box (about 6
-    instead of ~39 on cfg5) and on rolling balls in the 3D ball (about 7
-    instead of ~36 on cfg4), and resolves to "max" where the geometry has no
-    tangent-ball step (annulus, K = I box)."""
+    instead of ~39 on cfg5), on rolling balls in the 3D ball (about 7
+    instead of ~36 on cfg4) and on rolling / hole-tangent disks in the
+    annulus (cfg3), and resolves to "max" where the geometry has no
+    tangent-ball step (K = I box)."""
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(2).subset(16)
@@ -410,11 +411,18 @@ def test_fp32_tangent_chain_engages(B):
             r = plan.run(3, 20000)
         spw[chain] = r.steps_sum.sum() / (16 * 20000)
     assert spw["tangent"] < 6.0 < 12.0 < spw["max"], spw
-    c3 = configs.get(3).subset(4)
-    with B.Plan(B.pack_geometry(c3.dom), c3.kt.k_sqrt, c3.poles, c3.eps, 10**6,
-                B.pack_side(c3.fam0, 2, c3.eps), B.pack_side(c3.fam1, 2, c3.eps),
-                precision="fp32", chain="tangent") as plan:
-        assert plan.chain == "max"
+    # the annulus (cfg3) walks on rolling disks (outer ellipse) and disks
+    # tangent to the hole from outside
+    c3 = configs.get(3).subset(8)
+    g3 = B.pack_geometry(c3.dom)
+    a0, a1 = B.pack_side(c3.fam0, 2, c3.eps), B.pack_side(c3.fam1, 2, c3.eps)
+    for chain in ("tangent", "max"):
+        with B.Plan(g3, c3.kt.k_sqrt, c3.poles, c3.eps, 10**6, a0, a1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            r = plan.run(3, 20000)
+        spw["3" + chain] = r.steps_sum.sum() / (8 * 20000)
+    assert spw["3tangent"] < 0.6 * spw["3max"], spw
     with B.Plan(geom, np.eye(2), cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32",
                 chain="tangent") as plan:
         assert plan.chain == "max"
@@ -442,7 +450,7 @@ def test_fp32_tangent_chain_engages(B):
     assert spw["4tangent"] < 12.0 < 25.0 < spw["4max"], spw
 
 
-@pytest.mark.parametrize("idx,n_poles", [(2, 16), (4, 16), (5, 16)])
+@pytest.mark.parametrize("idx,n_poles", [(2, 16), (3, 16), (4, 16), (5, 16)])
 def test_fp32_tangent_matches_max_chain_grouped(B, idx, n_poles):
     """High-power check of the tangent-ball chain against the max chain (both
     FP32, the max chain itself checked against the oracle above) at 10^6

@@ -60,6 +60,11 @@ s0 = B.pack_side(cfg.fam0, 3, cfg.eps)
 s1 = B.pack_side(cfg.fam1, 3, cfg.eps)
 compare("cfg5", cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, s0, s1, n, len(cfg.fam1))
 
+# cfg3 (annulus: rolling disks, disks tangent to the hole)
+c3 = configs.get(3).subset(16)
+compare("cfg3", c3.dom, c3.kt.k_sqrt, c3.poles, c3.eps, B.pack_side(c3.fam0, 2, c3.eps),
+        B.pack_side(c3.fam1, 2, c3.eps), n, 512)
+
 # cfg4 (ball, rolling balls)
 c4 = configs.get(4).subset(16)
 compare("cfg4", c4.dom, c4.kt.k_sqrt, c4.poles, c4.eps, B.pack_side(c4.fam0, 3, c4.eps),
