@@ -50,6 +50,7 @@ F_STEP = {
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
     (2, "tangent"): (44, 3),                     # tangent balls: ~4x fewer, costlier steps
     (3, "woe"): (19, 4), (3, "max"): (31, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
+    (3, "tangent"): (91, 9),                     # rolling disks + disks tangent to the hole
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (4, "tangent"): (93, 10),                    # rolling balls (max-chain ball off the near side)
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
