@@ -1080,22 +1080,6 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
     w->rb = rb;
     w->n_chunks = (unsigned long long)p->n_poles * (unsigned long long)((n_rep + rb - 1) / rb);
-    w->c1 = w->n_chunks;
-    w->r1 = 0;
-    w->rb2 = rb;
-    if (p->precision == EM_PREC_FP32 && rb >= 256) {
-      // guided tail: the last ~1/8 of every pole's replicates in chunks of
-      // rb / 8, so warps finish within a short chunk of one another
-      const long long b1 = (n_rep - n_rep / 8) / rb;
-      if (b1 > 0 && b1 * rb < n_rep) {
-        const long long rb2 = rb / 8;
-        w->r1 = b1 * rb;
-        w->rb2 = rb2;
-        w->c1 = (unsigned long long)p->n_poles * (unsigned long long)b1;
-        w->n_chunks = w->c1 + (unsigned long long)p->n_poles *
-                                  (unsigned long long)((n_rep - w->r1 + rb2 - 1) / rb2);
-      }
-    }
     // minimum chunks (tiny jobs: ~1 walk per lane per chunk) mean a pole
     // change (a statistics flush) almost every walk: collect those flushes in
     // per-warp shared tables instead of global atomics (cfg1: 7x); bigger

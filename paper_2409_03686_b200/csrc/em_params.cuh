@@ -48,11 +48,7 @@ struct Side32 {
 struct WorkOut {
   long long n_poles, rep_start, n_rep, total;  // total = n_poles * n_rep
   long long rb;                                // replicates per chunk
-  unsigned long long n_chunks;                 // all chunks of the run
-  // guided tail (FP32 kernel): chunks c >= c1 cover replicates [r1, n_rep)
-  // in blocks of rb2 < rb, so the run winds down on short chunks
-  unsigned long long c1;                       // n_poles * (r1 / rb); = n_chunks: one phase
-  long long r1, rb2;
+  unsigned long long n_chunks;                 // n_poles * ceil(n_rep / rb)
   double inv_poles;                            // 1/n_poles for chunk -> (block, pole)
   const long long* pole_ids;                   // RNG pole index per row
   unsigned long long* ticket;                  // global chunk counter

@@ -120,13 +120,8 @@ __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask,
       if (c >= W.n_chunks) {
         wp.exhausted = 1;
       } else {
-        // phase 1: blocks of rb from replicate 0; phase 2 (c >= c1): blocks
-        // of rb2 from replicate r1 (guided tail)
-        const bool tail = c >= W.c1;
-        const unsigned long long cc = tail ? c - W.c1 : c;
-        const long long rbk = tail ? W.rb2 : W.rb;
-        long long b = (long long)((double)cc * W.inv_poles);
-        long long p = (long long)cc - b * W.n_poles;
+        long long b = (long long)((double)c * W.inv_poles);
+        long long p = (long long)c - b * W.n_poles;
         if (p < 0) {
           b -= 1;
           p += W.n_poles;
@@ -134,8 +129,8 @@ __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask,
           b += 1;
           p -= W.n_poles;
         }
-        const long long r0 = (tail ? W.r1 : 0) + b * rbk;
-        const int valid = (int)(W.n_rep - r0 < rbk ? W.n_rep - r0 : rbk);
+        const long long r0 = b * W.rb;
+        const int valid = (int)(W.n_rep - r0 < W.rb ? W.n_rep - r0 : W.rb);
         const int rem = n_need - avail;
         if (me && rank >= avail && rank - avail < valid) {
           np = (int)p;
