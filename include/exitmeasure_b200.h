@@ -66,16 +66,23 @@ extern "C" {
 #define EM_CHAIN_WOE 0
 #define EM_CHAIN_MAX 1
 /* EM_CHAIN_TANGENT: walk on tangent balls.  In whitened coordinates (where
- *   K-diffusion is Brownian motion) each step takes the largest ball inside
- *   the domain that is tangent to the nearest face at the foot of the
- *   current point and contains it, and jumps to an exact sample of that
- *   ball's harmonic measure seen from the point (a Cauchy variate through
- *   the Moebius map of the disk).  The centred ball is the special case of
- *   radius = distance, so every step is a valid walk-on-spheres step; near a
- *   face the distance contracts quadratically instead of geometrically
- *   (cfg2: 3.8 steps per walk instead of 15.7).  Same stopping rule
- *   sd <= eps, same exit law.  FP32, 2D boxes without holes; elsewhere the
- *   plan runs EM_CHAIN_MAX (em_plan_chain reports the chain in use). */
+ *   K-diffusion is Brownian motion) each step takes a ball inside the domain
+ *   that contains the current point and touches the boundary near it, and
+ *   jumps to an exact sample of that ball's harmonic measure seen from the
+ *   point (2D: the Moebius image of a uniform angle; 3D: the Poisson kernel,
+ *   uniform in 1/|z - y|).  Boxes and the L-box: the largest ball tangent to
+ *   the nearest face at the foot of the point.  Balls and the concentric
+ *   annulus: balls of the whitened ellipse's smallest curvature radius
+ *   tangent at the radial projection (they roll freely inside), disks
+ *   tangent to the hole from outside, else the max chain's centred ball.
+ *   The centred ball is the special case of a point at the centre, so every
+ *   step is a valid walk-on-spheres step; near the boundary the depth
+ *   contracts quadratically instead of geometrically (steps per walk cfg2
+ *   15.7 -> 3.7, cfg3 18.3 -> 5.8, cfg4 35.6 -> 7.0, cfg5 39.1 -> 6.0).
+ *   Same stopping rule sd <= eps, same exit law.  FP32 only, K != I; 2D / 3D
+ *   boxes and the 3D L-box without holes, the 2D ball with at most one
+ *   concentric hole, the 3D ball without holes; elsewhere the plan runs
+ *   EM_CHAIN_MAX (em_plan_chain reports the chain in use). */
 #define EM_CHAIN_TANGENT 2
 
 #define EM_MAX_HOLES 16

@@ -16,10 +16,13 @@ Two arithmetic paths (``precision``):
   binning); statistically identical exit law, not bit-identical.  With
   ``chain="max"`` each step uses the largest certified K^{1/2}-ellipsoid
   instead of the reference's sd-scaled one (fewer steps, same stopping shell
-  and exit law); ``chain="tangent"`` (default for fp32) walks on the largest
-  balls tangent to the nearest face in whitened coordinates where the
-  geometry has that step (2D boxes), sampling each ball's harmonic measure
-  exactly (quadratic approach to the boundary), and runs "max" elsewhere.
+  and exit law); ``chain="tangent"`` (default for fp32) walks on balls that
+  touch the boundary near the current point in whitened coordinates -- the
+  largest ball tangent to the nearest face (2D / 3D boxes, the L-box), balls
+  rolling inside the whitened ellipse / ellipsoid and disks tangent to a
+  concentric hole (ball, annulus) -- sampling each ball's harmonic measure
+  exactly (quadratic approach to the boundary), and runs "max" elsewhere
+  (K = I, non-concentric holes).
 
 ``EXITMEASURE_B200_PRECISION`` / ``EXITMEASURE_B200_CHAIN`` set the defaults
 process-wide (the analogue of the reference's ``EXITMEASURE_BACKEND``).
