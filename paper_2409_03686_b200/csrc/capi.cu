@@ -705,6 +705,10 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         // | |x_y| - |x_p| | <= 2 r max(Ad), so r = (R - rho) / (2 max Ad)
         // keeps the outer disks off the hole and the hole's disks inside R
         const double lim = (gf[d] - gf[d + 1 + d]) / (2.0 * amax);
+        P.rb_bl = (float)(gf[d] * amin / (amax * amax) * (1.0 - 1e-6));
+        P.gap = (float)((gf[d] - gf[d + 1 + d]) * (1.0 - 1e-6));
+        P.amax = (float)amax;
+        for (int i = 0; i < d; ++i) P.K4[i] = (float)(Adiag[i] * Adiag[i] * Adiag[i] * Adiag[i]);
         rb = std::min(rb, lim);
         P.rho_h = (float)(lim * (1.0 - 1e-6));
         P.rho_h2 = (float)((double)P.rho_h * (double)P.rho_h);

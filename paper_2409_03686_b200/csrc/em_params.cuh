@@ -144,6 +144,8 @@ struct F32Params {
   // whitened ellipsoid, R min(Ad) / max(Ad)^2) roll freely inside it
   float rho_b, rho_b2;
   float rho_h, rho_h2;  // 2D concentric annulus: disks tangent to the hole from outside
+  // EM_ROLL2_DYN: per-step radii (R - rho)(1 - 1e-6) / (max Ad + |diag(Ad) n|)
+  float rb_bl, gap, amax, K4[3];
   float ia[3];      // 1 / Ad
   float ss_scale;   // stop mask sat(min_i s_i * ss_scale) (power of two)
   float A[9];       // K^{1/2}, row-major

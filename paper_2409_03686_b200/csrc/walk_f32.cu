@@ -33,6 +33,10 @@
 #include "em_pool.cuh"
 #include "em_rng.cuh"
 
+#ifndef EM_ROLL2_DYN
+#define EM_ROLL2_DYN 0
+#endif
+
 namespace em {
 namespace f32 {
 
@@ -862,25 +866,34 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
     rm = fmaf(fdiv(outer ? qo : qh, outer ? Do : Dh), P.keep, -P.shrink_abs);
   }
   // rolling disk at the outer ellipse
+  float rb = P.rho_b, rb2 = P.rho_b2, rh = P.rho_h, rh2 = P.rho_h2;
+  if (NH == 1 && EM_ROLL2_DYN) {
+    // radii from the local normal: |diag(Ad) n| = |diag(Ad^2) x| / |Ax|
+    const float q4 = fmaf(P.K4[0], p0, P.K4[1] * p1);
+    rh = fdiv(P.gap, fmaf(q4 * rsq(q4), iaa, P.amax));
+    rb = fminf(P.rb_bl, rh);
+    rb2 = rb * rb;
+    rh2 = rh * rh;
+  }
   const float al = fmaf(-P.oR, ir, 1.0f);
-  const float be = P.rho_b * iaa;
+  const float be = rb * iaa;
   float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
   float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
   float d2 = fmaf(w0, w0, w1 * w1);
-  bool use = (d2 < P.rho_b2) & (fmaf(al, s2, be * aa) > 0.0f);
-  float rho = use ? P.rho_b : rm;
+  bool use = (d2 < rb2) & (fmaf(al, s2, be * aa) > 0.0f);
+  float rho = use ? rb : rm;
   if (NH == 1) {
     // disk tangent to the hole from outside, centre beyond the radial projection
     const float ah = fmaf(-P.hr[0], ir, 1.0f);
-    const float bh = P.rho_h * iaa;
+    const float bh = rh * iaa;
     const float v0 = x[0] * fmaf(ah, P.ia[0], -bh * P.Ad[0]);
     const float v1 = x[1] * fmaf(ah, P.ia[1], -bh * P.Ad[1]);
     const float dh = fmaf(v0, v0, v1 * v1);
-    const bool uh = !use & (dh < P.rho_h2) & (fmaf(ah, s2, -bh * aa) < 0.0f);
+    const bool uh = !use & (dh < rh2) & (fmaf(ah, s2, -bh * aa) < 0.0f);
     w0 = uh ? v0 : w0;
     w1 = uh ? v1 : w1;
     d2 = uh ? dh : d2;
-    rho = uh ? P.rho_h : rho;
+    rho = uh ? rh : rho;
     use |= uh;
   }
   const float id = rsq(fmaxf(d2, 1e-30f));
