@@ -206,6 +206,10 @@ int64_t em_plan_n_bins(const em_plan* p, int side);
 /* the walk chain the plan runs (EM_CHAIN_*): EM_CHAIN_TANGENT falls back to
  * EM_CHAIN_MAX where no tangent-ball step exists for the geometry */
 int em_plan_chain(const em_plan* p);
+/* the chain a plan over geometry g would run for (precision, chain), without
+ * a device: EM_CHAIN_TANGENT resolves to EM_CHAIN_MAX where no tangent-ball
+ * step exists; negative EM_ERR_* for an invalid geometry or pair */
+int em_resolve_chain(const em_geometry* g, int precision, int chain);
 
 /* Fractional rows (REF64 only; required for IDW weight families, valid for
  * Voronoi too): raw0 (n_poles, n0) and raw1 (n_poles, n1) doubles.  With

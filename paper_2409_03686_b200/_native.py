@@ -102,6 +102,8 @@ def lib():
         "em_plan_check": ([_p, _p, _p], ctypes.c_int),
         "em_plan_last_launches": ([_p, _p], ctypes.c_int),
         "em_plan_chain": ([_p], ctypes.c_int),
+        "em_resolve_chain": ([ctypes.POINTER(EmGeometry), ctypes.c_int, ctypes.c_int],
+                             ctypes.c_int),
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),
                                ctypes.POINTER(EmSide), _p, _p, _i64, _u64, _dbl, _i64, _i64,

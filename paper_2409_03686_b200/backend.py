@@ -67,6 +67,24 @@ def default_chain(precision: str) -> str:
     return "woe" if _PRECISIONS[precision] == N.EM_PREC_REF64 else "tangent"
 
 
+def resolve_chain(geom: "GeomPack", ksqrt, precision: str | None = None,
+                  chain: str | None = None) -> str:
+    """The chain a plan over ``geom`` runs for (precision, chain) -- "tangent"
+    becomes "max" where the geometry has no tangent-ball step (em_resolve_chain;
+    no device needed)."""
+    precision = (precision or default_precision()).lower()
+    chain = (chain or default_chain(precision)).lower()
+    if precision not in _PRECISIONS:
+        raise ValidationError(f"unknown precision {precision!r}")
+    if chain not in _CHAINS:
+        raise ValidationError(f"unknown chain {chain!r}")
+    m = _Marshal()
+    g = m.geometry(geom.gi, geom.gf, geom.comp_side, ksqrt)
+    rc = N.lib().em_resolve_chain(N.ctypes.byref(g), _PRECISIONS[precision], _CHAINS[chain])
+    N.check(rc, "em_resolve_chain")
+    return _CHAIN_NAMES[rc]
+
+
 def default_device() -> int:
     return int(os.environ.get("EXITMEASURE_B200_DEVICE", "0"))
 

@@ -428,6 +428,28 @@ std::shared_ptr<DeviceGrid> cached_device_grid(const double* anchors, int64_t m,
   return D;
 }
 
+// The chain a plan runs: EM_CHAIN_TANGENT exists (FP32, K != I) for 2D and
+// 3D boxes and the 3D L-box without holes, the 3D ball without holes (rolling
+// balls) and the 2D ball with at most one concentric hole (rolling disks,
+// hole-tangent disks); elsewhere it runs EM_CHAIN_MAX.  Expects a validated
+// geometry and a supported (precision, chain) pair.
+int resolve_chain(const em_geometry* g, int precision, int chain) {
+  if (precision != EM_PREC_FP32 || chain != EM_CHAIN_TANGENT) return chain;
+  const int d = (int)g->gi[0];
+  const int64_t nh = g->gi[2], nn = g->gi_len >= 4 ? g->gi[3] : 0;
+  bool id = true;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) id = false;
+  const bool ok2 = d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0;
+  const bool ok3 = d == 3 && g->gi[1] == 1 && nh == 0 && nn <= 1;
+  const bool okb = d == 3 && g->gi[1] == 0 && nh == 0 && nn == 0;
+  bool conc = nh == 1;
+  for (int j = 0; conc && j < d; ++j) conc = g->gf[d + 1 + j] == g->gf[j];
+  const bool okd = d == 2 && g->gi[1] == 0 && nn == 0 && (nh == 0 || conc);
+  return ((ok2 || ok3 || okb || okd) && !id) ? EM_CHAIN_TANGENT : EM_CHAIN_MAX;
+}
+
 int validate_geometry(const em_geometry* g) {
   if (!g || !g->gi || !g->gf || !g->comp_side || !g->ksqrt)
     return fail(EM_ERR_INVALID, "geometry: null pointer");
@@ -549,22 +571,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->device = o.device;
   p->precision = o.precision;
   p->chain = o.chain;
-  if (o.precision == EM_PREC_FP32 && o.chain == EM_CHAIN_TANGENT) {
-    // tangent-ball steps exist for boxes without holes and K != I: 2D boxes,
-    // 3D boxes and the 3D L-box
-    bool id = true;
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < d; ++j)
-        if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) id = false;
-    const bool ok2 = d == 2 && g->gi[1] == 1 && nh == 0 && nn == 0;
-    const bool ok3 = d == 3 && g->gi[1] == 1 && nh == 0 && nn <= 1;
-    const bool okb = d == 3 && g->gi[1] == 0 && nh == 0 && nn == 0;  // rolling balls
-    // 2D: rolling disks in the ball, with at most one hole, concentric
-    bool conc = nh == 1;
-    for (int j = 0; conc && j < d; ++j) conc = g->gf[d + 1 + j] == g->gf[j];
-    const bool okd = d == 2 && g->gi[1] == 0 && nn == 0 && (nh == 0 || conc);
-    if (!((ok2 || ok3 || okb || okd) && !id)) p->chain = EM_CHAIN_MAX;
-  }
+  p->chain = resolve_chain(g, o.precision, o.chain);
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
   p->n_holes = nh;
@@ -1331,6 +1338,18 @@ int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int6
 }
 
 int em_plan_chain(const em_plan* p) { return p ? p->chain : -1; }
+
+int em_resolve_chain(const em_geometry* g, int precision, int chain) {
+  int rc = validate_geometry(g);
+  if (rc) return rc;
+  if (precision != EM_PREC_REF64 && precision != EM_PREC_FP32)
+    return fail(EM_ERR_INVALID, "unknown precision");
+  if (chain != EM_CHAIN_WOE && chain != EM_CHAIN_MAX && chain != EM_CHAIN_TANGENT)
+    return fail(EM_ERR_INVALID, "unknown chain");
+  if (precision == EM_PREC_REF64 && chain != EM_CHAIN_WOE)
+    return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
+  return resolve_chain(g, precision, chain);
+}
 
 int em_plan_last_launches(const em_plan* p, int64_t* launches) {
   if (!p || !launches) return fail(EM_ERR_INVALID, "null");

@@ -258,3 +258,37 @@ def test_plan_cache_key_is_exact_content():
 
     r1 = RefSidePack(s1.anchors, s1.blk, s1.blkf, s1.weights_kind, s1.idw_radii, s1.idw_power)
     assert B._plan_key(*args[:6], r1, *args[7:]) != k  # no phase -> different plan
+
+
+def test_tangent_chain_resolution():
+    """Which geometries walk on tangent balls (em_resolve_chain, no device):
+    the BASELINE configs with K != I (cfg2 box, cfg3 concentric annulus, cfg4
+    ball, cfg5 L-box) resolve "tangent" to itself, cfg1 (K = I), an annulus
+    with an off-centre hole and a box with a hole to "max"; "max" / "woe"
+    are kept; REF64 runs the reference chain only."""
+    from paper_2409_03686_b200 import backend as B, configs
+    from paper_2409_03686_b200.errors import NativeError
+
+    for idx, want in ((1, "max"), (2, "tangent"), (3, "tangent"), (4, "tangent"),
+                      (5, "tangent")):
+        cfg = configs.get(idx)
+        geom = B.pack_geometry(cfg.dom)
+        assert B.resolve_chain(geom, cfg.kt.k_sqrt, "fp32", "tangent") == want, idx
+        assert B.resolve_chain(geom, cfg.kt.k_sqrt, "fp32", "max") == "max"
+        assert B.resolve_chain(geom, cfg.kt.k_sqrt, "fp32", "woe") == "woe"
+        assert B.resolve_chain(geom, cfg.kt.k_sqrt, "ref64", "woe") == "woe"
+        with pytest.raises(NativeError):
+            B.resolve_chain(geom, cfg.kt.k_sqrt, "ref64", "tangent")
+    k2 = configs.get(2).kt.k_sqrt
+    off = B.GeomPack(np.array([2, 0, 1]), np.array([0.0, 0.0, 1.0, 0.1, 0.0, 0.4]),
+                     np.array([0, 1], dtype=np.int8))
+    assert B.resolve_chain(off, k2, "fp32", "tangent") == "max"
+    conc = B.GeomPack(np.array([2, 0, 1]), np.array([0.0, 0.0, 1.0, 0.0, 0.0, 0.4]),
+                      np.array([0, 1], dtype=np.int8))
+    assert B.resolve_chain(conc, k2, "fp32", "tangent") == "tangent"
+    holed_box = B.GeomPack(np.array([2, 1, 1]), np.array([0.0, 0.0, 1.0, 0.2, 0.0, 0.3]),
+                           np.array([0, 1], dtype=np.int8))
+    assert B.resolve_chain(holed_box, k2, "fp32", "tangent") == "max"
+    with pytest.raises(NativeError):  # invalid geometry: dimension 4
+        B.resolve_chain(B.GeomPack(np.array([4, 1, 0]), np.zeros(5), np.zeros(1, np.int8)),
+                        np.eye(4), "fp32", "tangent")
