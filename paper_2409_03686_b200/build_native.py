@@ -39,8 +39,7 @@ UNITS = [
                      f"-DEM_Z_BITS={os.environ.get('EM_Z_BITS', '16')}",
                      f"-DEM_TAB_WARP={os.environ.get('EM_TAB_WARP', '0')}",
                      f"-DEM_ROLL2_BLOCKS={os.environ.get('EM_ROLL2_BLOCKS', '4')}",
-                     f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}",
-                     f"-DEM_GRID_SHORT={os.environ.get('EM_GRID_SHORT', '4')}"]),
+                     f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}"]),
     ("capi.cu", []),
     ("kat_curand.cu", []),
 ]

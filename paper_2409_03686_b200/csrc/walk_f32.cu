@@ -33,11 +33,6 @@
 #include "em_pool.cuh"
 #include "em_rng.cuh"
 
-// candidate-grid binner: candidates each lane scans alone before the warp
-// scans the rest of long lists together
-#ifndef EM_GRID_SHORT
-#define EM_GRID_SHORT 4
-#endif
 #ifndef EM_ROLL2_DYN
 #define EM_ROLL2_DYN 0
 #endif
@@ -455,58 +450,12 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
     const int n = brute ? na : (int)cnt;
     float best = kInf;
     int bi = 0;
-    // (t, index)-lexicographic minimum, as the reference's scan (S/_kernel.pyx:315-319)
-    const int n1 = n < EM_GRID_SHORT ? n : EM_GRID_SHORT;
-    for (int j = 0; j < n1; ++j) {
+    for (int j = 0; j < n; ++j) {
       const int a = brute ? j : (int)__ldg(&cand[off + j]);
       const float t = d2_to<D>(__ldg(&anchors[a]), x);
       if (t < best || (t == best && a < bi)) {
         best = t;
         bi = a;
-      }
-    }
-    // the rest of the long lists (cells near Voronoi vertices and face
-    // edges, brute-force cells): the whole warp scans each such list
-    // together and reduces, instead of every lane waiting for the warp's
-    // longest list (mean ~2 candidates, warp maximum ~16).  Every lane of the
-    // warp is here (retire is called warp-wide).
-    unsigned longm = __ballot_sync(kFull, n > EM_GRID_SHORT);
-    const int lane = threadIdx.x & 31;
-    while (longm) {
-      const int src = __ffs(longm) - 1;
-      longm &= longm - 1u;
-      const int s_side = __shfl_sync(kFull, side, src);
-      const int s_n = __shfl_sync(kFull, n, src);
-      const unsigned s_off = __shfl_sync(kFull, off, src);
-      const int s_brute = __shfl_sync(kFull, (int)brute, src);
-      float sx[3];
-      sx[0] = __shfl_sync(kFull, x[0], src);
-      sx[1] = __shfl_sync(kFull, x[1], src);
-      sx[2] = D == 3 ? __shfl_sync(kFull, x[2], src) : 0.0f;
-      const float4* s_anch = pick(s_side, S0.anchors, S1.anchors);
-      const unsigned* s_cand = pick(s_side, S0.grid.cand, S1.grid.cand);
-      float tb = kInf;
-      int ib = 0x7fffffff;
-      for (int j = EM_GRID_SHORT + lane; j < s_n; j += 32) {
-        const int a = s_brute ? j : (int)__ldg(&s_cand[s_off + j]);
-        const float t = d2_to<D>(__ldg(&s_anch[a]), sx);
-        if (t < tb || (t == tb && a < ib)) {
-          tb = t;
-          ib = a;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float t2 = __shfl_xor_sync(kFull, tb, o);
-        const int i2 = __shfl_xor_sync(kFull, ib, o);
-        if (t2 < tb || (t2 == tb && i2 < ib)) {
-          tb = t2;
-          ib = i2;
-        }
-      }
-      if (lane == src && (tb < best || (tb == best && ib < bi))) {
-        best = tb;
-        bi = ib;
       }
     }
     return bi;
@@ -1006,7 +955,7 @@ __device__ __forceinline__ void frame_to_world(const F32Params& P, const float* 
 
 template <int D, int OUTER, int NH, int BINK, int SMEM, bool SHEAR>
 __device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
-                                       StepAcc& acc, bool valid = true) {
+                                       StepAcc& acc) {
   const WorkOut& W = P.w;
   float xf[3], xw[3];
   to_frame<D, OUTER, SHEAR>(P, x, xf);
@@ -1016,10 +965,8 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
   frame_to_world<D, OUTER>(P, xf, xw);
   const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
-  if (valid) {
-    atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
-    acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
-  }
+  atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+  acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
 
 // MODE 0: bin exits into the count rows + per-pole step statistics
@@ -1259,12 +1206,11 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
   }
   if (MODE == 0) {
     __syncwarp();
-    if (qn > 0) {  // drain the queue, warp-wide (lanes past qn re-bin slot 0, uncounted)
+    if (lane < qn) {  // drain the queue
       const ExitQueue& q = q_all[threadIdx.x >> 5];
-      const int sl = lane < qn ? lane : 0;
-      const float4 e = q.x[sl];
+      const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, __float_as_int(e.w), q.s[sl], acc, lane < qn);
+      retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
     acc_flush<SMEM>(acc, W);
     stats_smem_flush<SMEM>(W);
