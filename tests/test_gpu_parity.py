@@ -490,3 +490,41 @@ def test_fp32_tangent_matches_max_chain_grouped(B, idx, n_poles):
     pv = np.array(pv)
     assert pv.min() > 1e-4 / n_poles, pv
     assert stats.combine_pvalues(pv)[1] > 1e-4, pv
+
+
+def test_fp32_rolling_disk_without_hole_matches_max_chain(B):
+    """The 2D rolling-disk chain on a hole-free ball (cfg1's disk and bins
+    with cfg2's anisotropic K -- no BASELINE config runs it): far fewer steps
+    than the max chain and the same exit law (per-pole upper-half mass within
+    4.5 binomial standard errors, two-sample chi^2 over 32 bin groups with
+    Bonferroni and Fisher levels 1e-4)."""
+    from scipy import stats
+
+    from paper_2409_03686_b200 import configs
+
+    c1, c2 = configs.get(1), configs.get(2)
+    geom = B.pack_geometry(c1.dom)
+    s0, s1 = B.pack_side(c1.fam0, 2, c1.eps), B.pack_side(c1.fam1, 2, c1.eps)
+    k = c2.kt.k_sqrt
+    n = 10**6
+    res, spw = {}, {}
+    for chain, seed in (("max", 31), ("tangent", 32)):
+        with B.Plan(geom, k, c1.poles[::4], c1.eps, 10**6, s0, s1, precision="fp32",
+                    chain=chain) as plan:
+            assert plan.chain == chain
+            r = plan.run(seed, n)
+        res[chain] = r.counts.astype(np.float64)
+        spw[chain] = r.steps_sum.sum() / (r.counts.shape[0] * n)
+    assert spw["tangent"] < 0.6 * spw["max"], spw
+    a, b = res["max"], res["tangent"]
+    assert (a.sum(1) == n).all() and (b.sum(1) == n).all()
+    half = a.shape[1] // 2
+    fa, fb = a[:, :half].sum(1) / n, b[:, :half].sum(1) / n
+    p = (fa + fb) / 2
+    z = (fb - fa) / np.sqrt(2 * p * (1 - p) / n)
+    assert np.abs(z).max() < 4.5, z
+    edges = np.arange(0, a.shape[1], a.shape[1] // 32)
+    ga, gb = np.add.reduceat(a, edges, axis=1), np.add.reduceat(b, edges, axis=1)
+    pv = np.array([stats.chi2_contingency(np.vstack([ga[i], gb[i]]))[1] for i in range(len(a))])
+    assert pv.min() > 1e-4 / len(pv), pv
+    assert stats.combine_pvalues(pv)[1] > 1e-4, pv
