@@ -793,13 +793,14 @@ __device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, 
   const float s2 = p0 + p1 + p2;
   const float aa = fmaf(P.Kd[0], p0, fmaf(P.Kd[1], p1, P.Kd[2] * p2));
   const float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
-  const float iaa = rsq(aa);
+  // clamped: a walk at the exact centre (x = 0) keeps finite terms
+  const float iaa = rsq(fmaxf(aa, 1e-30f));
   const float sa = aa * iaa;  // |Ax|
   // max chain: the largest centred whitened ball, r = q / (|Ax| + sqrt(|Ax|^2 + q))
   const float q = P.oR2 - s2;
   const float rm = fmaf(fdiv(q, sa + fsqrt(fmaxf(aa + q, 0.0f))), P.keep, -P.shrink_abs);
   // rolling ball tangent at the radial projection
-  const float al = fmaf(-P.oR, rsq(s2), 1.0f);
+  const float al = fmaf(-P.oR, rsq(fmaxf(s2, 1e-30f)), 1.0f);
   const float be = P.rho_b * iaa;
   const float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
   const float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
@@ -849,9 +850,10 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
   const float aa = fmaf(P.Kd[0], p0, P.Kd[1] * p1);
   float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
   if (NH == 1) wm = fminf(wm, __saturatef(fmaf(s2, P.h2_scale, P.h2_bias)));
-  const float iaa = rsq(aa);
+  // clamped: a walk at the exact centre (x = 0) keeps finite terms
+  const float iaa = rsq(fmaxf(aa, 1e-30f));
   const float sa = aa * iaa;  // |Ax|
-  const float ir = rsq(s2);
+  const float ir = rsq(fmaxf(s2, 1e-30f));
   // max chain: the largest centred whitened disk
   float rm;
   if (NH == 0) {

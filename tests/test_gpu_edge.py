@@ -183,3 +183,27 @@ def test_plan_cache_reuse_is_exact(B, cfg2, precision):
     assert np.array_equal(e.counts, a.counts) and len(B._PLAN_CACHE) == 2
     B.clear_plan_cache()
     assert len(B._PLAN_CACHE) == 0
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_fp32_rolling_chain_pole_at_the_centre(B, d):
+    """A pole at the exact centre of a ball (x = 0: |x| and |Ax| vanish in the
+    rolling-ball construction) still walks and bins every walk into a valid
+    column: exact row sums, and by the symmetry x -> -x of the ellipse /
+    ellipsoid the two halves of the boundary get equal mass.  3D: cfg4; 2D:
+    cfg1's disk with cfg2's anisotropic K."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(4 if d == 3 else 1)
+    k = cfg.kt.k_sqrt if d == 3 else configs.get(2).kt.k_sqrt
+    geom = B.pack_geometry(cfg.dom)
+    s0, s1 = B.pack_side(cfg.fam0, d, cfg.eps), B.pack_side(cfg.fam1, d, cfg.eps)
+    n = 200_000
+    with B.Plan(geom, k, np.zeros((1, d)), cfg.eps, 10**6, s0, s1, precision="fp32",
+                chain="tangent") as plan:
+        assert plan.chain == "tangent"
+        r = plan.run(5, n)
+    assert int(r.counts.sum()) == n
+    half = r.counts.shape[1] // 2
+    lower = r.counts[0, half:].sum() / n
+    assert abs(lower - 0.5) < 0.01, lower
