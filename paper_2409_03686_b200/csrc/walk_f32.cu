@@ -28,6 +28,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "em_params.cuh"
 #include "em_pool.cuh"
@@ -1350,7 +1353,26 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
                               int* nb) {
   F32Kernel k = pick_f32(d, outer, nh_mode, 0, chain, ident, bink, 0);
   if (!k) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
+  // per (kernel, device): the query costs microseconds on every plan otherwise
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<const void*, int> key{(const void*)k, dev};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+      if (e.first == key) {
+        *nb = e.second;
+        return cudaSuccess;
+      }
+  }
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back({key, *nb});
+  }
+  return e;
 }
 
 // ---- FP32 point binning (same owner/binner as the walk kernel) ----

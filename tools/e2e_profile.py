@@ -53,3 +53,17 @@ for _ in range(5):
                          B.pack_side(cfg.fam0, cfg.d, cfg.eps), B.pack_side(cfg.fam1, cfg.d, cfg.eps),
                          precision="fp32")
 print(f"run_accumulate: {1e3*(time.perf_counter()-t0)/5:.3f} ms per call (kernel {r.kernel_ms:.3f})")
+
+if len(sys.argv) > 2 and sys.argv[2] == "prof":
+    import cProfile
+    import pstats
+
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(50):
+        B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, cfg.n_rep,
+                         s0, s1, precision="fp32", cache=False)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
