@@ -39,7 +39,8 @@ UNITS = [
                      f"-DEM_Z_BITS={os.environ.get('EM_Z_BITS', '16')}",
                      f"-DEM_TAB_WARP={os.environ.get('EM_TAB_WARP', '0')}",
                      f"-DEM_ROLL2_BLOCKS={os.environ.get('EM_ROLL2_BLOCKS', '4')}",
-                     f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}"]),
+                     f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}",
+                     f"-DEM_POST_STOP={os.environ.get('EM_POST_STOP', '1')}"]),
     ("capi.cu", []),
     ("kat_curand.cu", []),
 ]

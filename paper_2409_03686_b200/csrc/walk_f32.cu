@@ -36,6 +36,10 @@
 #include "em_pool.cuh"
 #include "em_rng.cuh"
 
+// test the landing point of a batch's last move before the service pass
+#ifndef EM_POST_STOP
+#define EM_POST_STOP 1
+#endif
 #ifndef EM_ROLL2_DYN
 #define EM_ROLL2_DYN 0
 #endif
@@ -1173,6 +1177,26 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
       }
       walking = wm != 0.0f;
       steps += (int)sf;
+      if (EM_POST_STOP) {
+        // the stop test of the point the last move landed on (the next
+        // batch's first test, evaluated now): a walk that reached the shell
+        // on a batch's last step retires at this service pass instead of
+        // idling through one more batch.  Only the stop mask of the step
+        // functions is live here (the rest is dead code); results are
+        // unchanged (same moves, same draws).
+        float t2;
+        if (TANG || ROLL) {
+          float nx[3];
+          if (ROLL && D == 3) t2 = roll_step3(P, x, 0u, P.one_bits, nx);
+          else if (ROLL) t2 = roll_step2<NH>(P, x, 0u, P.one_bits, nx);
+          else if (D == 2) t2 = tangent_step(P, x, 0u, P.one_bits, nx[0], nx[1]);
+          else t2 = tangent_step3<OUTER>(P, ttab, x, 0u, P.one_bits, nx);
+        } else {
+          float r2;
+          dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t2, r2);
+        }
+        walking &= t2 != 0.0f;
+      }
     } else {
       int failed = 0;
 #pragma unroll
