@@ -1130,6 +1130,12 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
         rep_hi = (unsigned)(rep >> 32);
         steps = 0;
         walking = 1;
+      } else if (EM_POST_STOP && !walking) {
+        // park a lane left without work: its exit point is already queued,
+        // and the batch's own stop test need not agree with the post-batch
+        // one to the last rounding (separately scheduled FMA chains), so an
+        // idle lane must not sit on a borderline point it could walk from
+        x[0] = x[1] = x[2] = kFar;
       }
       live = __ballot_sync(kFull, walking);
       if (wp.exhausted && live == 0) break;
@@ -1181,9 +1187,12 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
         // the stop test of the point the last move landed on (the next
         // batch's first test, evaluated now): a walk that reached the shell
         // on a batch's last step retires at this service pass instead of
-        // idling through one more batch.  Only the stop mask of the step
-        // functions is live here (the rest is dead code); results are
-        // unchanged (same moves, same draws).
+        // idling through one more batch (cfg2-cfg5 +9-12%).  Only the stop
+        // mask of the step functions is live here (the rest is dead code).
+        // Same criterion, same moves and draws; the two evaluations of the
+        // test may round apart on a point at the shell's edge (separately
+        // scheduled FMA chains), so such a walk can end one step earlier --
+        // and a lane left without work is parked far outside (service).
         float t2;
         if (TANG || ROLL) {
           float nx[3];
