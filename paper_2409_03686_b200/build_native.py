@@ -40,7 +40,8 @@ UNITS = [
                      f"-DEM_TAB_WARP={os.environ.get('EM_TAB_WARP', '0')}",
                      f"-DEM_ROLL2_BLOCKS={os.environ.get('EM_ROLL2_BLOCKS', '4')}",
                      f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}",
-                     f"-DEM_POST_STOP={os.environ.get('EM_POST_STOP', '1')}"]),
+                     f"-DEM_POST_STOP={os.environ.get('EM_POST_STOP', '1')}",
+                     f"-DEM_TANG_K={os.environ.get('EM_TANG_K', '4')}"]),
     ("capi.cu", []),
     ("kat_curand.cu", []),
 ]

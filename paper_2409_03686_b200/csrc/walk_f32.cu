@@ -36,6 +36,10 @@
 #include "em_pool.cuh"
 #include "em_rng.cuh"
 
+// steps per batch on the tangent chains (one Philox block: <= 4)
+#ifndef EM_TANG_K
+#define EM_TANG_K 4
+#endif
 // test the landing point of a batch's last move before the service pass
 #ifndef EM_POST_STOP
 #define EM_POST_STOP 1
@@ -1061,7 +1065,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
 #endif
   // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
   // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
-  constexpr int K = (TANG || ROLL) ? 4 : Batch<D>::kSteps;
+  constexpr int K = (TANG || ROLL) ? EM_TANG_K : Batch<D>::kSteps;
   constexpr int NB = (TANG || ROLL) ? 1 : Batch<D>::kBlocks;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
