@@ -36,7 +36,8 @@
 #include "em_pool.cuh"
 #include "em_rng.cuh"
 
-// steps per batch on the tangent chains (one Philox block: <= 4)
+// steps per batch on the tangent chains (one 32-bit word per step, one
+// Philox block per 4 steps)
 #ifndef EM_TANG_K
 #define EM_TANG_K 4
 #endif
@@ -1066,7 +1067,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
   // tangent chain: ~4 steps per walk, so 4-step batches (one Philox block,
   // one 32-bit word per step); elsewhere 8-step batches of 16-bit angles
   constexpr int K = (TANG || ROLL) ? EM_TANG_K : Batch<D>::kSteps;
-  constexpr int NB = (TANG || ROLL) ? 1 : Batch<D>::kBlocks;
+  constexpr int NB = (TANG || ROLL) ? (EM_TANG_K + 3) / 4 : Batch<D>::kBlocks;
   for (;;) {
     // ---- service: retire finished walks, refill idle lanes ----
     const unsigned need = __ballot_sync(kFull, !walking);
