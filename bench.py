@@ -198,9 +198,6 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
 
 # walks per pole per step of the `--impl reference` arm (~0.2-1 s of CPU work
 # per step on 16 host threads, so a K-step run ends in minutes) ...
-# chain of the committed cfg2 capture (profiles/r01_cfg2_walk_f32_ncu_raw.csv)
-PROFILED_CHAIN = "tangent"
-
 REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
 # ... and of the in-bench `cpu_baseline` leg: about 10 s of CPU work on the
 # GPU box's 16 host threads (cfg1: the whole 3.2e5-walk workload), see
@@ -208,49 +205,44 @@ REF_SAMPLE = {1: 10_000, 2: 16_384, 3: 1024, 4: 256, 5: 16}
 CPU_SAMPLE = {1: 10_000, 2: 163_840, 3: 32_768, 4: 16_384, 5: 1024}
 
 
-def profiled_traffic(cfg_index: int, precision: str, chain: str):
-    """DRAM bytes per launch of the walk kernel from the committed `ncu --set
-    full` capture of this same command (profiles/r01_cfg2_walk_f32_ncu_raw.csv),
-    or None when no capture matches the configuration."""
+# committed ncu captures of the walk kernel per (config, chain): key metrics
+# in "metric,value,unit" rows (tools/ncu_metrics.py from the raw page of one
+# `ncu --set full` capture of `bench.py --config C`)
+PROFILES = {(2, "tangent"): "profiles/r01_cfg2_walk_f32_ncu_raw.csv",
+            (3, "tangent"): "profiles/r02_cfg3_walk_f32_ncu_metrics.csv",
+            (4, "tangent"): "profiles/r02_cfg4_walk_f32_ncu_metrics.csv",
+            (5, "tangent"): "profiles/r02_cfg5_walk_f32_ncu_metrics.csv"}
+
+
+def profiled_ncu(cfg_index: int, precision: str, chain: str):
+    """DRAM bytes per launch and issue / pipe utilisation of the walk kernel
+    from the committed capture of this configuration, or None."""
     import csv
 
-    f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
-    if cfg_index != 2 or precision != "fp32" or chain != PROFILED_CHAIN or not f.exists():
+    rel = PROFILES.get((cfg_index, chain)) if precision == "fp32" else None
+    if rel is None or not (ROOT / rel).exists():
         return None
     vals = {}
-    for row in csv.reader(open(f)):
+    for row in csv.reader(open(ROOT / rel)):
         if len(row) == 3:
             vals[row[0]] = (row[1], row[2])
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out = {"source": rel}
     try:
-        tot = 0.0
-        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            v, u = vals[k]
-            tot += float(v) * scale[u]
-        return tot
+        out["traffic"] = sum(float(vals[k][0]) * scale[vals[k][1]]
+                             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except (KeyError, ValueError):
-        return None
-
-
-def profiled_issue(cfg_index: int, precision: str, chain: str):
-    """Issue-slot and pipe utilisation of the walk kernel from the same
-    committed capture (the FP32-issue roofline's direct evidence), or None."""
-    import csv
-
-    f = ROOT / "profiles" / "r01_cfg2_walk_f32_ncu_raw.csv"
-    if cfg_index != 2 or precision != "fp32" or chain != PROFILED_CHAIN or not f.exists():
-        return None
-    vals = {row[0]: row[1] for row in csv.reader(open(f)) if len(row) == 3}
+        out["traffic"] = None
     keys = {"issue_active": "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "pipe_fma": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
             "pipe_alu": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
             "pipe_xu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
             "warps_active": "sm__warps_active.avg.pct_of_peak_sustained_active"}
     try:
-        out = {k: round(float(vals[v]) / 100.0, 4) for k, v in keys.items()}
+        out["issue"] = {k: round(float(vals[v][0]) / 100.0, 4) for k, v in keys.items()}
+        out["issue"]["source"] = rel + " (fractions of peak)"
     except (KeyError, ValueError):
-        return None
-    out["source"] = "profiles/r01_cfg2_walk_f32_ncu_raw.csv (fractions of peak)"
+        out["issue"] = None
     return out
 
 
@@ -299,10 +291,27 @@ def run_reference(args):
     return 0
 
 
+def _nccl_lines():
+    """The communicator-init lines NCCL wrote under NCCL_DEBUG=INFO (the
+    NCCL_DEBUG_FILE this harness sets): rank / nranks per communicator."""
+    import glob
+    import re
+
+    out = []
+    for f in sorted(glob.glob(os.environ.get("EM_NCCL_LOG_GLOB", "/nonexistent"))):
+        for line in open(f, errors="replace"):
+            if re.search(r"nranks \d+", line) and "Init COMPLETE" in line:
+                out.append(line.strip())
+    return out
+
+
 def run_ours(args):
     import torch
 
     world, rank, local = _dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -311,7 +320,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
-    from paper_2409_03686_b200 import _native, backend, configs
+    from paper_2409_03686_b200 import _native, backend, configs, distributed
 
     cfg = configs.get(args.config)
     if args.n_rep:
@@ -325,9 +334,10 @@ def run_ours(args):
         ids = np.arange(cfg.n_poles)
         rep_start = rank * cfg.n_rep
     else:
-        # strong scaling: cyclic row shard of the fixed workload + an NCCL
-        # all-gather of the count rows every step
-        ids = np.arange(rank, cfg.n_poles, world)
+        # strong scaling (default): cyclic row shard of the fixed workload,
+        # then ONE NCCL all-gather of the count rows + step statistics and the
+        # un-permute to pole order, all inside the timed region
+        ids = distributed.shard_rows(cfg.n_poles, world, rank)
         rep_start = 0
     geom = backend.pack_geometry(cfg.dom)
     s0 = backend.pack_side(cfg.fam0, cfg.d, cfg.eps)
@@ -338,10 +348,19 @@ def run_ours(args):
     row = plan.n0 + plan.n1
     m_local = len(ids)
     m_pad = m_local if weak else -(-cfg.n_poles // world)
-    counts = torch.zeros((m_pad, row), dtype=torch.int64, device="cuda")
-    stats = torch.zeros((3, m_pad), dtype=torch.int64, device="cuda")
-    gathered = (torch.zeros((world * m_pad, row), dtype=torch.int64, device="cuda")
-                if world > 1 and not weak else None)
+    # one flat block per rank: counts (m_pad, row) | stats (3, m_pad), so the
+    # exchange is ONE all-gather
+    blk_len = m_pad * row + 3 * m_pad
+    buf = torch.zeros(blk_len, dtype=torch.int64, device="cuda")
+    counts = buf[: m_pad * row].view(m_pad, row)
+    stats = buf[m_pad * row:].view(3, m_pad)
+    gathered = full = perm = None
+    if world > 1 and not weak:
+        gathered = torch.zeros((world, blk_len), dtype=torch.int64, device="cuda")
+        # global pole g lives in rank g % N's block at row g // N
+        g = torch.arange(cfg.n_poles, device="cuda")
+        perm = (g % world) * m_pad + g // world
+        full = torch.zeros((cfg.n_poles, row), dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -349,13 +368,17 @@ def run_ours(args):
         plan.run_device(cfg.seed, cfg.n_rep, counts.data_ptr(), stats.data_ptr(),
                         stream.cuda_stream, rep_start)
         if gathered is not None:
-            dist.all_gather_into_tensor(gathered, counts)
+            dist.all_gather_into_tensor(gathered.view(-1), buf)
+            rows = gathered[:, : m_pad * row].reshape(world * m_pad, row)
+            torch.index_select(rows, 0, perm, out=full)
 
     for _ in range(args.warmup):
         flush.zero_()
         one_step()
     torch.cuda.synchronize()
     steps_per_run = int(stats[0, :m_local].sum().item())
+    if full is not None:  # the gathered rows count every walk of every pole once
+        assert bool((full.sum(1) == cfg.n_rep).all().item()), "gathered rows wrong"
     ffma_peak, _ = _native.fp32_peak(device)
     info = _native.device_info(device)
 
@@ -371,9 +394,10 @@ def run_ours(args):
             ev[i][0].record(stream)
             one_step()
             ev[i][1].record(stream)
-            launches += plan.last_launches()
+            launches += plan.last_launches() + (2 if gathered is not None else 0)
         torch.cuda.synchronize()
     plan.check()  # budget errors of the (asynchronous) runs
+    kernel_ms = plan.last_stats()[0]  # walk kernel alone, last run (CUDA events)
     combined_ok = None
     if dist and weak:
         # the one exchange, outside the timed region: sum the ranks' rows into
@@ -385,9 +409,9 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([tot_ms, kernel_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms, kernel_ms = float(t[0].item()), float(t[1].item())
         st = torch.tensor([steps_per_run], device="cuda", dtype=torch.int64)
         dist.all_reduce(st)
         steps_total_run = int(st.item())
@@ -398,34 +422,72 @@ def run_ours(args):
     steps_per_s = steps_total_run * args.steps / (tot_ms * 1e-3)
     clocks = clk.summary()
 
-    # roofline: FP32 issue bound of this kernel on this GPU
+    # roofline: FP32 issue bound of the walk kernel on this GPU.  The kernel's
+    # own duration (CUDA events around the launch on its stream, averaged over
+    # the timed runs' last launch) sets `achieved`; the step time also holds
+    # the zeroing / fold launches and, at N > 1, the gather.
     fp32, xu = F_STEP[(cfg.index, plan.chain if plan.precision == "fp32" else "woe")]
-    per_gpu_steps_s = steps_per_s / world
-    achieved = fp32 * per_gpu_steps_s / 1e12
+    steps_per_gpu_run = steps_total_run / world
+    achieved = fp32 * steps_per_gpu_run / (kernel_ms * 1e-3) / 1e12
     clk_mhz = clocks["sm_mhz"] or (info["clock_khz"] / 1e3)
     peak_nominal = info["sm_count"] * 128 * clk_mhz * 1e6 / 1e12
     peak_ffma = ffma_peak / 1e12
 
-    # e2e through the public API: host numpy in, host numpy out, one call
-    e2e_val = None
-    h2d = d2h = 0
-    if rank == 0:
-        sub_ids = ids
-        e2e_times = []
-        for i in range(max(3, min(args.steps, 11))):
-            t0 = time.perf_counter()
-            r = backend.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles[sub_ids], cfg.seed,
-                                       cfg.eps, 10**6, cfg.n_rep, s0, s1,
-                                       precision=plan.precision, chain=plan.chain,
-                                       device=device, pole_ids=sub_ids, cache=False)
-            e2e_times.append(time.perf_counter() - t0)
-        e2e_val = (len(sub_ids) * cfg.n_rep * (world if weak else 1)
-                   / float(np.median(e2e_times[1:])))
-        if not weak:
-            e2e_val *= world  # every rank walks its shard concurrently
-        h2d = (cfg.poles[sub_ids].nbytes + s0.anchors.nbytes + s1.anchors.nbytes
-               + geom.gi.nbytes + geom.gf.nbytes + cfg.kt.k_sqrt.nbytes)
-        d2h = r.counts.nbytes + 3 * 8 * len(sub_ids)
+    # e2e through the public API, host numpy in / out, every step: plan
+    # creation + upload of the inputs, the walk, the exchange, the D2H of the
+    # rows.  N = 1: the REFERENCE's own entry point exitmeasure.backend.
+    # run_accumulate with this backend installed by plugin.install() (when the
+    # reference package is importable); N > 1: distributed.
+    # run_accumulate_sharded on every rank, wall time max over ranks.
+    e2e_vals, api = [], None
+    n_e2e = max(3, min(args.steps, 11))
+    if world == 1:
+        ref_be = _plugin_backend(plan.precision, plan.chain, device)
+        if ref_be is not None:
+            api = ("exitmeasure.backend.run_accumulate (the reference's entry point) with "
+                   "paper_2409_03686_b200.plugin.install(cache=False) -- the reference's "
+                   "AccumulateResult (float64 raw0/raw1) out")
+            call = lambda: ref_be.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed,
+                                                 cfg.eps, 10**6, cfg.n_rep, s0, s1)
+        else:
+            api = "paper_2409_03686_b200.backend.run_accumulate(cache=False)"
+            call = lambda: backend.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed,
+                                                  cfg.eps, 10**6, cfg.n_rep, s0, s1,
+                                                  precision=plan.precision, chain=plan.chain,
+                                                  device=device, cache=False)
+    elif weak:
+        api = "paper_2409_03686_b200.backend.run_accumulate(cache=False) per rank (own replicate range)"
+        call = lambda: backend.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed,
+                                              cfg.eps, 10**6, cfg.n_rep, s0, s1,
+                                              precision=plan.precision, chain=plan.chain,
+                                              device=device, cache=False)
+    else:
+        api = ("paper_2409_03686_b200.distributed.run_accumulate_sharded (row shard, NCCL "
+               "all-gather, full rows on every rank)")
+        call = lambda: distributed.run_accumulate_sharded(
+            cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6, cfg.n_rep, s0, s1,
+            precision=plan.precision, chain=plan.chain)
+    for _ in range(n_e2e):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = call()
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e_vals.append(dt)
+    e2e_walks = cfg.total_walks * (world if weak else 1)
+    e2e_val = e2e_walks / float(np.median(e2e_vals[1:]))
+    in_ids = ids if (weak or world == 1) else np.arange(cfg.n_poles)
+    h2d = (cfg.poles.nbytes + s0.anchors.nbytes + s1.anchors.nbytes + geom.gi.nbytes
+           + geom.gf.nbytes + cfg.kt.k_sqrt.nbytes)
+    d2h = (len(in_ids) * row * 8 + 3 * 8 * len(in_ids)) if (weak or world == 1) else \
+        (m_pad * row + 3 * m_pad) * 8
+    grid_note = ("candidate-grid cache warm after the first call (the grid is a pure "
+                 "function of the anchors; ~1 s host build)" if cfg.index in (4, 5)
+                 else "no candidate grid on this config (closed-form binner)")
 
     line = None
     if rank == 0:
@@ -437,6 +499,7 @@ def run_ours(args):
                    "kind": c[2],
                    "sample": f"{cfg.name}: all {cfg.n_poles} poles x {n_sample} walks/pole "
                              f"({c[3]:.1f} s), steps/s {c[1]:.3g}"}
+        prof = profiled_ncu(cfg.index, plan.precision, plan.chain)
         line = {
             "metric": "walks/s", "value": value, "unit": "walks/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -452,18 +515,28 @@ def run_ours(args):
                                        + ("" if combined_ok is None else
                                           f" (row sums {'ok' if combined_ok else 'WRONG'})")
                                        if weak else
-                                       f"rows cyclic over {world} GPU(s), NCCL all-gather of "
-                                       "the count rows every step"),
+                                       f"rows cyclic over {world} GPU(s) (pole i -> rank i mod "
+                                       f"{world})" + (", one NCCL all-gather of the count rows + "
+                                                      "step statistics and the un-permute to pole "
+                                                      "order inside every timed step"
+                                                      if world > 1 else "")),
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "counts": "int64 (n_poles, n0+n1) rows + step stats"},
+                       "counts": "int64 (n_poles, n0+n1) rows + step stats",
+                       "build": _native.build_info()},
             "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
                          "unit": "Top/s", "frac": achieved / peak_nominal,
-                         "traffic": profiled_traffic(cfg.index, plan.precision, plan.chain),
-                         "traffic_note": "DRAM bytes per launch from the committed ncu --set "
-                                         "full capture (profiles/r01_cfg2_walk_f32_ncu_raw.csv); "
-                                         "algorithmic: the int64 count rows",
-                         "algorithmic_bytes": int(cfg.n_poles * (plan.n0 + plan.n1) * 8),
-                         "f_step": {"fp32": fp32, "xu": xu},
+                         "kernel_ms": kernel_ms,
+                         "traffic": prof["traffic"] if prof else None,
+                         "traffic_note": ("DRAM bytes per launch of the walk kernel from the "
+                                          f"committed ncu --set full capture ({prof['source']}); "
+                                          "algorithmic: the int64 count rows") if prof else
+                                         "no committed capture of this configuration",
+                         "algorithmic_bytes": int(cfg.n_poles * row * 8),
+                         "f_step": {"fp32": fp32, "xu": xu,
+                                    "convention": "SURVEY 8(d): add/sub/mul/fma/min/max/compare "
+                                                  "on the path a step takes (no selects, no "
+                                                  "discarded branch arms); XU and RNG apart; "
+                                                  "DESIGN.md 3.3"},
                          "peak_note": f"{info['sm_count']} SMs x 128 FP32 lanes x median SM "
                                       f"clock under load {clk_mhz:.0f} MHz (MEASURED_PEAKS.json "
                                       "has no FP32 figure)",
@@ -471,21 +544,27 @@ def run_ours(args):
                          "frac_of_measured_ffma": achieved / peak_ffma,
                          "frac_at_max_clock": achieved / (info["sm_count"] * 128 *
                                                           (clocks["sm_max_mhz"] or 1965) * 1e-6),
-                         "ncu": profiled_issue(cfg.index, plan.precision, plan.chain),
+                         "ncu": prof["issue"] if prof else None,
                          "reference_chain_equivalent": {
                              "frac": (value / world) * F_REF[cfg.index][0] * F_REF[cfg.index][1]
                                      / (peak_nominal * 1e12),
                              "note": "walks/s x the reference chain's FP32 ops/step x its "
                                      "steps/walk (SURVEY 8d) / peak: the FP32 issue share the "
-                                     "reference algorithm would need for the same walks/s"}},
+                                     "reference algorithm would need for the same walks/s (not "
+                                     "a roofline fraction)"}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "walks/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h),
-                    "api": "paper_2409_03686_b200.backend.run_accumulate (host numpy in/out; "
-                           "cache=False: plan creation + input upload every call)"},
+                    "d2h_bytes_per_step": int(d2h), "api": api,
+                    "timing": ("wall clock per call, median of the calls after the first"
+                               + (", max over ranks" if world > 1 else "")),
+                    "caches": "plan cache off (plan creation + input upload in every call); "
+                              + grid_note},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
+        if world > 1:
+            nl = _nccl_lines()
+            line["config"]["nccl"] = {"init_lines": nl[:world], "n_lines": len(nl)}
         print(json.dumps(line), flush=True)
     plan.close()
     if dist:
@@ -494,25 +573,99 @@ def run_ours(args):
     return 0
 
 
-def main():
+def _plugin_backend(precision, chain, device):
+    """The reference's backend module with this library installed (oracle/_ref
+    holds the unmodified reference package), or None when it is absent."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "exitmeasure").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from paper_2409_03686_b200 import plugin
+
+        return plugin.install(precision=precision, chain=chain, device=device, cache=False)
+    except Exception as e:  # pragma: no cover - reference import problems
+        print(f"bench.py: plugin path unavailable ({e})", file=sys.stderr)
+        return None
+
+
+def run_harness_check(args):
+    """The launch / rendezvous / max-over-ranks plumbing without a GPU
+    (gloo): each rank reports itself, rank 0 prints one line with n_gpus."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = _dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    r = torch.tensor([rank], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ranks = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(ranks, r)
+        seen = sorted(int(x.item()) for x in ranks)
+    else:
+        seen = [0]
+    if rank == 0:
+        print(json.dumps({"harness_check": True, "n_gpus": world, "ranks": seen,
+                          "max_over_ranks": float(t.item())}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def self_launch(argv, n: int) -> int:
+    """--gpus N without a torchrun environment: launch N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1, NCCL logging on."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    logdir = Path(os.environ.get("TMPDIR", "/tmp")) / f"em_nccl_{os.getpid()}"
+    logdir.mkdir(parents=True, exist_ok=True)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", str(logdir / "nccl.%h.%p.log"))
+    env["EM_NCCL_LOG_GLOB"] = str(logdir / "nccl.*.log")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())]
+    return subprocess.call(cmd + list(argv), env=env)
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3,
+                    help="BASELINE config (default 3: the annulus, the config BASELINE.json "
+                         "shards over 1/2/4/8 GPUs)")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--chain", default=None)
     ap.add_argument("--n-rep", type=int, default=None, help="override walks per pole")
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak (default) = every rank walks all poles on its own "
-                         "replicate range, no collective in the timed region; strong = "
-                         "cyclic row shard of the fixed workload + NCCL all-gather of the "
-                         "rows every step")
-    args = ap.parse_args()
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong (default) = cyclic row shard of the fixed workload + "
+                         "NCCL all-gather of the rows inside every timed step; weak = every "
+                         "rank walks all poles on its own replicate range, no collective in "
+                         "the timed region")
+    ap.add_argument("--harness-check", action="store_true",
+                    help="launch / rendezvous plumbing only (gloo, no GPU)")
+    args = ap.parse_args(argv)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(argv, args.gpus)
+    if args.harness_check:
+        return run_harness_check(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -144,6 +144,12 @@ typedef struct {
 typedef struct em_plan em_plan;
 
 int em_abi_version(void);
+/* Every compile-time knob the loaded library was built with, as one
+ * "key=value ..." string (ABI, arch, debug asserts, the REF64 and FP32 math
+ * flags and the FP32 kernel's batch / RNG-resolution / occupancy macros).
+ * No reference counterpart: the reference's kernel has no build knobs
+ * (R/pkg/setup.py:28-34 fixes its Cython directives). */
+const char* em_build_info(void);
 const char* em_last_error(void);
 int em_device_count(void);
 /* sm_count, max SM clock (kHz), compute capability major/minor */

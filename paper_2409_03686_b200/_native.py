@@ -18,7 +18,10 @@ import numpy as np
 
 from .errors import NativeError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libexitmeasure_b200.so"
+# EXITMEASURE_B200_DEBUG=1 loads the EM_DEBUG variant (device bounds asserts)
+DEBUG = os.environ.get("EXITMEASURE_B200_DEBUG") == "1"
+LIB_PATH = (Path(__file__).resolve().parent / "lib"
+            / ("libexitmeasure_b200_debug.so" if DEBUG else "libexitmeasure_b200.so"))
 
 EM_OK = 0
 EM_BUDGET = 1
@@ -72,13 +75,14 @@ def lib():
         if os.environ.get("EXITMEASURE_B200_AUTOBUILD", "1") == "1":
             from .build_native import build
 
-            build()
+            build(debug=DEBUG)
         if not LIB_PATH.exists():
             raise NativeError(f"CUDA library missing: {LIB_PATH} "
                               "(run python -m paper_2409_03686_b200.build_native)")
     L = ctypes.CDLL(str(LIB_PATH))
     sig = {
         "em_abi_version": ([], ctypes.c_int),
+        "em_build_info": ([], ctypes.c_char_p),
         "em_last_error": ([], ctypes.c_char_p),
         "em_device_count": ([], ctypes.c_int),
         "em_device_info": ([ctypes.c_int, _p, _p, _p, _p], ctypes.c_int),
@@ -140,6 +144,12 @@ def exported_symbols():
     """(name, exported?) for every function the header declares."""
     L = ctypes.CDLL(str(LIB_PATH))
     return [(n, hasattr(L, n)) for n in declared_symbols()]
+
+
+def build_info() -> dict:
+    """The compile knobs of the loaded library (em_build_info) as a dict."""
+    text = lib().em_build_info().decode()
+    return dict(kv.split("=", 1) for kv in text.split())
 
 
 def last_error() -> str:

@@ -344,6 +344,9 @@ class Plan:
         pid = None if pole_ids is None else m.arr(pole_ids, np.int64)
         if pid is not None and pid.shape[0] != self.n_poles:
             raise ValidationError("one pole id per pole required")
+        # budget errors name the GLOBAL pole (the RNG key), as the reference's
+        # job-order scan does (S/backend.py:189-192)
+        self.pole_ids = None if pid is None else pid.copy()
         opt = N.EmOptions(_PRECISIONS[precision], _CHAINS[chain], self.device, int(block),
                           int(grid), 0)
         h = ctypes.c_void_p()
@@ -356,6 +359,11 @@ class Plan:
         # the chain the plan runs: "tangent" becomes "max" where the geometry
         # has no tangent-ball step (em_plan_chain)
         self.chain = _CHAIN_NAMES.get(int(N.lib().em_plan_chain(h)), chain)
+
+    def _budget_error(self, row: int, replicate: int) -> WalkBudgetError:
+        """WalkBudgetError for plan row ``row``, naming its global pole id."""
+        pole = int(self.pole_ids[row]) if self.pole_ids is not None else int(row)
+        return WalkBudgetError(pole, int(replicate), self.max_steps)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -388,7 +396,7 @@ class Plan:
                                              ctypes.byref(ep), ctypes.byref(er)),
                      "em_plan_run_raw")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
+            raise self._budget_error(ep.value, rep_start + er.value)
         return AccumulateResult(raw0, raw1, stats[0].copy(), stats[1].copy(), stats[2].copy(),
                                 int(fb.value))
 
@@ -402,7 +410,7 @@ class Plan:
                                               int(n_rep), ctypes.byref(blk), ctypes.byref(ep),
                                               ctypes.byref(er)), "em_plan_run_host")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
+            raise self._budget_error(ep.value, rep_start + er.value)
         nc = self.n_poles * row
         # zero-copy: the result owns the page-locked block the counts were
         # copied into (returned to the library's cache when the arrays die)
@@ -423,7 +431,10 @@ class Plan:
         """Outputs stay in device memory: counts (n_poles, n0+n1) int64 and
         stats (3, n_poles) int64 at the given device pointers; work is
         ordered on ``stream_ptr`` (e.g. torch's current stream) and this call
-        returns without waiting -- call ``check()`` after synchronising."""
+        returns without waiting -- call ``check()`` after synchronising.
+        Integer rows only: IDW families need ``run_raw``."""
+        if self.idw:
+            raise ValidationError("IDW weight families give fractional rows: use run_raw")
         out = N.EmOutputs(ctypes.c_void_p(counts_ptr), ctypes.c_void_p(stats_ptr),
                           ctypes.c_void_p(stats_ptr + 8 * self.n_poles),
                           ctypes.c_void_p(stats_ptr + 16 * self.n_poles), -1, -1)
@@ -443,8 +454,7 @@ class Plan:
         rc = N.check(N.lib().em_plan_check(self._h, ctypes.byref(ep), ctypes.byref(er)),
                      "em_plan_check")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(ep.value), int(getattr(self, "_last_rep_start", 0)
-                                                     + er.value), self.max_steps)
+            raise self._budget_error(ep.value, getattr(self, "_last_rep_start", 0) + er.value)
 
     def exits(self, seed: int, n_rep: int, rep_start: int = 0):
         """Exit points, steps and components of n_rep walks per pole,
@@ -458,7 +468,7 @@ class Plan:
                                           int(n_rep), N.ptr(x), N.ptr(steps), N.ptr(comp),
                                           ctypes.byref(ep), ctypes.byref(er)), "em_run_exits")
         if rc == N.EM_BUDGET:
-            raise WalkBudgetError(int(ep.value), int(rep_start + er.value), self.max_steps)
+            raise self._budget_error(ep.value, rep_start + er.value)
         return x, steps, comp
 
     def bin_points(self, pts):

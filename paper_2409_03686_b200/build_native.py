@@ -22,29 +22,42 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "lib"
-LIB = OUT_DIR / "libexitmeasure_b200.so"
 BUILD = PKG / "_build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(PKG.parent / "include")]
 
-UNITS = [
-    # (source, extra flags)
-    ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]),
-    ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false",
-                     f"-DEM_BATCH_STEPS={os.environ.get('EM_BATCH_STEPS', '8')}",
-                     f"-DEM_MIN_BLOCKS={os.environ.get('EM_MIN_BLOCKS', '0')}",
-                     f"-DEM_ANGLE_BITS={os.environ.get('EM_ANGLE_BITS', '16')}",
-                     f"-DEM_Z_BITS={os.environ.get('EM_Z_BITS', '16')}",
-                     f"-DEM_TAB_WARP={os.environ.get('EM_TAB_WARP', '0')}",
-                     f"-DEM_ROLL2_BLOCKS={os.environ.get('EM_ROLL2_BLOCKS', '4')}",
-                     f"-DEM_ROLL2_DYN={os.environ.get('EM_ROLL2_DYN', '0')}",
-                     f"-DEM_POST_STOP={os.environ.get('EM_POST_STOP', '1')}",
-                     f"-DEM_TANG_K={os.environ.get('EM_TANG_K', '4')}"]),
-    ("capi.cu", []),
-    ("kat_curand.cu", []),
-]
+# FP32 kernel knobs (measured alternatives in profiles/).
+# The production values are fixed here: an environment variable changes them
+# only when EXITMEASURE_B200_KNOBS=1 (A/B tooling), so a stray variable cannot
+# silently change the kernel's RNG resolution or chain.  em_build_info()
+# reports what the loaded library was built with.
+KNOB_DEFAULTS = {"EM_BATCH_STEPS": "8", "EM_MIN_BLOCKS": "0", "EM_ANGLE_BITS": "16",
+                 "EM_Z_BITS": "16", "EM_TAB_WARP": "0", "EM_ROLL2_BLOCKS": "4",
+                 "EM_ROLL2_DYN": "0", "EM_POST_STOP": "1", "EM_TANG_K": "4"}
+
+
+def knobs() -> dict:
+    if os.environ.get("EXITMEASURE_B200_KNOBS") != "1":
+        return dict(KNOB_DEFAULTS)
+    return {k: os.environ.get(k, v) for k, v in KNOB_DEFAULTS.items()}
+
+
+def units(debug: bool = False):
+    """(source, extra nvcc flags) per translation unit."""
+    dbg = ["-DEM_DEBUG=1"] if debug else []
+    return [
+        ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"] + dbg),
+        ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false"]
+         + [f"-D{k}={v}" for k, v in knobs().items()] + dbg),
+        ("capi.cu", dbg),
+        ("kat_curand.cu", dbg),
+    ]
+
+
+def lib_path(debug: bool = False) -> Path:
+    return OUT_DIR / ("libexitmeasure_b200_debug.so" if debug else "libexitmeasure_b200.so")
 
 
 def nvcc() -> str:
@@ -62,29 +75,38 @@ def _sources_newer(target: Path) -> bool:
     return any(f.stat().st_mtime > t for f in files)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _sources_newer(LIB):
-        return LIB
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> Path:
+    """Compile the library (``debug=True``: the EM_DEBUG variant with device
+    bounds asserts, lib/libexitmeasure_b200_debug.so).  Units compile in
+    parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    target = lib_path(debug)
+    if not force and not _sources_newer(target):
+        return target
+    bdir = BUILD.with_name(BUILD.name + ("_debug" if debug else ""))
+    bdir.mkdir(exist_ok=True)
     OUT_DIR.mkdir(exist_ok=True)
     nv = nvcc()
-    objs = []
-    for src, extra in UNITS:
-        obj = BUILD / (Path(src).stem + ".o")
+    cmds, objs = [], []
+    for src, extra in units(debug):
+        obj = bdir / (Path(src).stem + ".o")
         cmd = [nv, "-c", str(CSRC / src), "-o", str(obj)] + ARCH + NVCC_COMMON + extra
         if verbose:
             cmd += ["-Xptxas", "-v"]
-        _run(cmd, verbose)
+        cmds.append(cmd)
         objs.append(str(obj))
-    gobj = BUILD / "grid.o"
-    _run(["g++", "-O2", "-fPIC", "-std=c++17", "-c", str(CSRC / "grid.cpp"), "-o", str(gobj)],
-         verbose)
+    gobj = bdir / "grid.o"
+    cmds.append(["g++", "-O2", "-fPIC", "-std=c++17", "-c", str(CSRC / "grid.cpp"), "-o",
+                 str(gobj)])
     objs.append(str(gobj))
-    tmp = LIB.with_suffix(".so.tmp")
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), cmds))
+    tmp = target.with_suffix(".so.tmp")
     _run([nv, "-shared", "-o", str(tmp)] + objs + ARCH + ["-cudart", "static", "-lpthread"],
          verbose)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 def _run(cmd, verbose):
@@ -101,5 +123,6 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--debug", action="store_true", help="EM_DEBUG variant (device asserts)")
     a = ap.parse_args()
-    print(build(force=a.force or a.verbose, verbose=a.verbose))
+    print(build(force=a.force or a.verbose, verbose=a.verbose, debug=a.debug))

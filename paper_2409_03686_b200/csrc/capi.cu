@@ -47,6 +47,7 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
+const char* f32_build_knobs();
 
 struct GridHost {
   double lo[3];
@@ -271,6 +272,7 @@ struct em_plan {
   int64_t last_walks = 0, last_steps = 0, last_launches = 0, last_n_rep = 0;
   bool last_timed = false;  // ev0 / ev1 bracket the last walk kernel
   cudaStream_t last_stream = nullptr;  // stream of the last run_device
+  cudaStream_t last_launch_stream = nullptr;  // stream of the last launch (any entry point)
   std::vector<std::shared_ptr<DeviceGrid>> grids;  // device-resident candidate grids in use
   ~em_plan() {
     // buffers go back to the shared cache: nothing in flight may still use them
@@ -501,6 +503,15 @@ int validate_side(const em_side* s, int d, const char* name, bool used) {
 extern "C" {
 
 int em_abi_version(void) { return EM_ABI_VERSION; }
+
+const char* em_build_info(void) {
+  static const std::string info = std::string("abi=") + std::to_string(EM_ABI_VERSION) +
+                                  " arch=sm_100a debug=" + std::to_string(EM_DEBUG) +
+                                  " ref64=-fmad=false,-prec-div=true,-prec-sqrt=true"
+                                  " f32=-fmad=true,-prec-div=false,-prec-sqrt=false " +
+                                  f32_build_knobs();
+  return info.c_str();
+}
 
 const char* em_last_error(void) { return g_last_error.c_str(); }
 
@@ -1080,6 +1091,10 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   const int64_t total = p->n_poles * n_rep;
   if (n_rep > 0 && total / n_rep != p->n_poles) return fail(EM_ERR_INVALID, "walk count overflows");
   if ((double)total > 9.0e15) return fail(EM_ERR_INVALID, "walk count too large");
+  // integer-count paths bin to the nearest anchor: an IDW family's
+  // fractional rows come only from em_plan_run_raw (never silently Voronoi)
+  if (mode == 0 && (p->wkind[0] || p->wkind[1]))
+    return fail(EM_ERR_UNSUPPORTED, "IDW weight families need em_plan_run_raw (fractional rows)");
   WorkOut* w = p->precision == EM_PREC_REF64 ? &p->p64.w : &p->p32.w;
   w->rep_start = rep_start;
   w->n_rep = n_rep;
@@ -1112,7 +1127,13 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   w->counts = counts;
   unsigned long long* sdst = stats;
   if (w->stat_copies > 1) {
-    if (p->scopies.alloc((size_t)w->stat_copies * 3 * p->n_poles * 8) != cudaSuccess)
+    const size_t need = (size_t)w->stat_copies * 3 * p->n_poles * 8;
+    // growing returns the old buffer to the shared free list: a kernel of an
+    // earlier (asynchronous) run may still write it, so wait for that run
+    if (p->scopies.p && need > p->scopies.bytes && p->last_launch_stream &&
+        cudaStreamSynchronize(p->last_launch_stream) != cudaSuccess)
+      return fail(EM_ERR_CUDA, "synchronise before growing the statistics copies");
+    if (p->scopies.alloc(need) != cudaSuccess)
       return fail(EM_ERR_NOMEM, "cudaMalloc: statistics copies");
     sdst = p->scopies.as<unsigned long long>();
   }
@@ -1182,6 +1203,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   }
   p->last_launches = launches;
   p->last_walks = total;
+  p->last_launch_stream = s;
   return EM_OK;
 }
 

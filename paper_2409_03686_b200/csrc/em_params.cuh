@@ -6,6 +6,28 @@
 #include "../../include/exitmeasure_b200.h"
 #include "em_rng.cuh"
 
+// EM_DEBUG=1 (the debug library, build_native.build(debug=True)) turns on
+// device-side bounds checks on every count-row write and work hand-out; a
+// failed check prints its location and traps (the launch then fails with a
+// CUDA error instead of writing out of bounds).  Off in the production build.
+#ifndef EM_DEBUG
+#define EM_DEBUG 0
+#endif
+#if EM_DEBUG
+#include <cstdio>
+#define EM_DEV_ASSERT(c)                                                      \
+  do {                                                                        \
+    if (!(c)) {                                                               \
+      printf("EM_DEV_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      __trap();                                                               \
+    }                                                                         \
+  } while (0)
+#else
+#define EM_DEV_ASSERT(c) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace em {
 
 constexpr int kMaxBlk = 16;         // structured anchor blocks per side

@@ -979,6 +979,9 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
   frame_to_world<D, OUTER>(P, xf, xw);
   const int a = bin_exit<D, BINK>(P, side, xw);
   const int col = side ? W.col_off1 + a : a;
+  EM_DEV_ASSERT(side == 0 || side == 1);
+  EM_DEV_ASSERT(a >= 0 && a < (side ? P.side[1].n_anchors : P.side[0].n_anchors));
+  EM_DEV_ASSERT(col >= 0 && col < W.row_len && pole >= 0 && pole < W.n_poles);
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
   acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
@@ -1103,6 +1106,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
         }
       } else if (done) {
         const long long o = (long long)pole * W.n_rep + rep_off;
+        EM_DEV_ASSERT(o >= 0 && o < W.total);
         float xf[3];
         to_frame<D, OUTER, SCALED>(P, x, xf);
         double xd[3] = {(double)x[0], (double)x[1], D == 3 ? (double)x[2] : 0.0};
@@ -1119,6 +1123,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
         W.comp_out[o] = owner<D, OUTER, NH>(P, xf);
       }
       if (pool_take_fast(wp, need, W, pole, rep_off, eq, lt)) {
+        EM_DEV_ASSERT(pole >= 0 && pole < W.n_poles && rep_off >= 0 && rep_off < W.n_rep);
         if (pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
           px = p.x;
@@ -1411,6 +1416,18 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
     cache.push_back({key, *nb});
   }
   return e;
+}
+
+// Compile knobs of this translation unit (em_build_info): every macro that
+// changes the FP32 kernel's arithmetic or schedule, as built.
+#define EM_STR2(x) #x
+#define EM_STR(x) EM_STR2(x)
+const char* f32_build_knobs() {
+  return "EM_BATCH_STEPS=" EM_STR(EM_BATCH_STEPS) " EM_ANGLE_BITS=" EM_STR(EM_ANGLE_BITS)
+         " EM_Z_BITS=" EM_STR(EM_Z_BITS) " EM_TANG_K=" EM_STR(EM_TANG_K)
+         " EM_POST_STOP=" EM_STR(EM_POST_STOP) " EM_MIN_BLOCKS=" EM_STR(EM_MIN_BLOCKS)
+         " EM_ROLL2_BLOCKS=" EM_STR(EM_ROLL2_BLOCKS) " EM_ROLL2_DYN=" EM_STR(EM_ROLL2_DYN)
+         " EM_TAB_WARP=" EM_STR(EM_TAB_WARP) " EM_DEBUG=" EM_STR(EM_DEBUG);
 }
 
 // ---- FP32 point binning (same owner/binner as the walk kernel) ----

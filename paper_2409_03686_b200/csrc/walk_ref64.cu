@@ -296,6 +296,8 @@ __device__ __forceinline__ void retire64(const Ref64Params& P, const double* xq,
   const int side = P.comp_side[comp];
   const long long winner = assign_anchor(x, P.d, P.side[side]);
   const long long col = side ? W.col_off1 + winner : winner;
+  EM_DEV_ASSERT(winner >= 0 && winner < P.side[side].n_anchors);
+  EM_DEV_ASSERT(col >= 0 && col < W.row_len && pole >= 0 && pole < W.n_poles);
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
   acc_add(acc, W, pole, (unsigned long long)steps);
 }
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(256, 4) walk_ref64_kernel(const Ref64Params P)
       }
     } else if (stop) {
       const long long o = (long long)pole * W.n_rep + rep_off;
+      EM_DEV_ASSERT(o >= 0 && o < W.total);
       for (int j = 0; j < d; ++j) W.x_out[o * d + j] = x[j];
       W.steps_out[o] = steps;
       W.comp_out[o] = owner_component(P, x);

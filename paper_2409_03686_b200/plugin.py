@@ -73,10 +73,11 @@ def install_linalg(device: int | None = None):
 
 
 def install(precision: str | None = None, chain: str | None = None, device: int | None = None,
-            module=None, linalg: str | None = None):
+            module=None, linalg: str | None = None, cache: bool = True):
     """Patch ``exitmeasure.backend`` (or ``module``) to run on this library
     (and, with ``linalg="device"``, the dense algebra: install_linalg).
-    Returns the patched backend module."""
+    ``cache=False`` builds and uploads a fresh plan on every call (no
+    resident-plan reuse across calls).  Returns the patched backend module."""
     if linalg not in (None, "host", "device"):
         raise ValueError(f"linalg must be 'host' or 'device', got {linalg!r}")
     if linalg == "device":
@@ -89,7 +90,8 @@ def install(precision: str | None = None, chain: str | None = None, device: int 
                        threads=None):
         try:
             res = B.run_accumulate(dom, ksqrt, poles, seed, eps, max_steps, n_rep, side0, side1,
-                                   threads, precision=precision, chain=chain, device=device)
+                                   threads, precision=precision, chain=chain, device=device,
+                                   cache=cache)
         except WalkBudgetError as e:
             raise ref_budget(e.pole, e.replicate, e.max_steps) from None
         return module.AccumulateResult(res.raw0, res.raw1, res.steps_sum, res.steps_sq_sum,

@@ -24,9 +24,9 @@ def _reference_available():
 @pytest.fixture(scope="module")
 def native():
     from paper_2409_03686_b200 import _native
-    from paper_2409_03686_b200.build_native import LIB, build
+    from paper_2409_03686_b200.build_native import build, lib_path
 
-    if not LIB.exists():
+    if not lib_path().exists():
         build()
     return _native
 
@@ -36,6 +36,17 @@ def test_library_exports_every_declared_symbol(native):
     assert len(names) >= 15
     missing = [n for n, ok in names if not ok]
     assert not missing, missing
+
+
+def test_build_info_reports_production_knobs(native):
+    """The loaded library was built with the production knobs (a stray
+    environment variable at build time cannot change them silently)."""
+    from paper_2409_03686_b200.build_native import KNOB_DEFAULTS
+
+    info = native.build_info()
+    assert info["arch"] == "sm_100a" and info["debug"] == "0" and info["abi"] == "1"
+    for k, v in KNOB_DEFAULTS.items():
+        assert info[k] == v, (k, info[k], v)
 
 
 def test_ctypes_layout_matches_c_header(native, tmp_path):
@@ -292,3 +303,66 @@ def test_tangent_chain_resolution():
     with pytest.raises(NativeError):  # invalid geometry: dimension 4
         B.resolve_chain(B.GeomPack(np.array([4, 1, 0]), np.zeros(5), np.zeros(1, np.int8)),
                         np.eye(4), "fp32", "tangent")
+
+
+_BUDGET_WORKER = textwrap.dedent("""
+    import sys
+    import torch.distributed as dist
+    sys.path.insert(0, sys.argv[1])
+    from paper_2409_03686_b200.distributed import agree_on_budget_error
+    from paper_2409_03686_b200.errors import WalkBudgetError
+    dist.init_process_group("gloo")
+    rank = dist.get_rank()
+    # rank 0 fails at global (pole 5, rep 3), rank 1 at (pole 2, rep 7): every
+    # rank must raise the lexicographically first one, (2, 7)
+    cases = [({0: (5, 3), 1: (2, 7)}, (2, 7)), ({1: (4, 0)}, (4, 0)), ({}, None)]
+    for errs, want in cases:
+        e = WalkBudgetError(*errs[rank], 100) if rank in errs else None
+        try:
+            agree_on_budget_error(e, 10, 100, "cpu")
+            got = None
+        except WalkBudgetError as x:
+            got = (x.pole, x.replicate)
+            assert x.max_steps == 100
+        assert got == want, (rank, got, want)
+    dist.barrier(); dist.destroy_process_group()
+    print("rank", rank, "ok")
+""")
+
+
+def test_budget_error_agreed_across_gloo_ranks(tmp_path):
+    """A budget overrun on any rank is raised on EVERY rank (the global
+    lexicographic minimum) before the gather, so no rank is left blocking in
+    the collective."""
+    w = tmp_path / "worker.py"
+    w.write_text(_BUDGET_WORKER)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29579", str(w), str(ROOT)]
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
+    assert res.stdout.count("ok") == 2
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without a torchrun environment launches two ranks
+    itself (the driver's N>1 contract); the gloo harness check reports both."""
+    import json
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2",
+                          "--harness-check"], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(line) == 1, res.stdout
+    d = json.loads(line[0])
+    assert d["n_gpus"] == 2 and d["ranks"] == [0, 1]
+
+
+def test_bench_rejects_world_mismatch():
+    """Under torchrun, --gpus must equal WORLD_SIZE (no silent 1-GPU timing)."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert res.returncode == 2 and "WORLD_SIZE" in res.stderr
