@@ -151,6 +151,10 @@ def cpu_reference_walks_per_s(cfg, n_sample: int, threads: int):
         from exitmeasure import backend as rb
         from exitmeasure.geometry import Ball, Box, BoundaryPointSet, make_domain
 
+        # the reference's OWN CPU path, never this library installed over it
+        assert not hasattr(rb, "_em_b200_original"), "plugin installed over the reference"
+        assert rb.BACKEND == "compiled", rb.BACKEND
+
         from paper_2409_03686_b200 import backend as B
 
         geom = B.pack_geometry(sub.dom)
@@ -439,7 +443,7 @@ def run_ours(args):
     # run_accumulate with this backend installed by plugin.install() (when the
     # reference package is importable); N > 1: distributed.
     # run_accumulate_sharded on every rank, wall time max over ranks.
-    e2e_vals, api = [], None
+    e2e_vals, api, ref_be = [], None, None
     n_e2e = max(3, min(args.steps, 11))
     if world == 1:
         ref_be = _plugin_backend(plan.precision, plan.chain, device)
@@ -478,6 +482,10 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e_vals.append(dt)
+    if world == 1 and ref_be is not None:
+        from paper_2409_03686_b200 import plugin
+
+        plugin.uninstall(ref_be)  # the cpu_baseline leg below times the reference itself
     e2e_walks = cfg.total_walks * (world if weak else 1)
     e2e_val = e2e_walks / float(np.median(e2e_vals[1:]))
     in_ids = ids if (weak or world == 1) else np.arange(cfg.n_poles)

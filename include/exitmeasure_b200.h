@@ -126,8 +126,14 @@ typedef struct {
   int32_t device;    /* CUDA ordinal */
   int32_t block;     /* threads per block, 0 = library default */
   int32_t grid;      /* persistent blocks, 0 = library default (SMs x occupancy) */
-  int32_t reserved;
+  int32_t flags;     /* EM_FLAG_* bits, 0 = none */
 } em_options;
+
+/* Run EM_CHAIN_TANGENT even when K = I (where it is normally resolved to
+ * EM_CHAIN_MAX).  Then the rolling ball of a ball domain is the domain
+ * itself, so one step samples the domain's Poisson kernel exactly: the
+ * closed-form test of the production samplers (tests/test_gpu_closed_form.py). */
+#define EM_FLAG_TANGENT_ON_IDENTITY 1
 
 /* Per-run outputs.  Host pointers for em_plan_run / em_run_accumulate,
  * device pointers for em_plan_run_device.  counts is (n_poles, n0 + n1)
@@ -248,6 +254,17 @@ int em_run_accumulate(const em_geometry* g, const em_side* s0, const em_side* s1
 int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                  double* x_out, int64_t* steps_out, int64_t* comp_out, int64_t* err_pole,
                  int64_t* err_rep);
+
+/* Test hook: ONE step of the plan's FP32 walk chain from each of n world
+ * points x (n, d) with the random words (n, 2) (the tangent / rolling steps
+ * use word 0; the woe / max steps take the azimuth from word 0 -- 3D: z
+ * from word 0, azimuth from word 1), through the same device functions as
+ * the walk kernel.  y (n, d): the candidate next point in world coordinates;
+ * mask (n,): the walk's 0/1 stop mask at x (0 = inside the eps-shell).  No
+ * reference counterpart (the reference's step is inline in S/_kernel.pyx:
+ * 185-196); it exposes the samplers to closed-form checks. */
+int em_debug_step(em_plan* p, const double* x, const uint32_t* words, int64_t n, double* y,
+                  float* mask);
 
 /* Micro-benchmark used for the roofline denominator: achieved FP32 FFMA
  * lane-ops/s of an issue-bound kernel on `device` (its own CUDA events). */

@@ -34,6 +34,7 @@ EM_PREC_FP32 = 1
 EM_CHAIN_WOE = 0
 EM_CHAIN_MAX = 1
 EM_CHAIN_TANGENT = 2
+EM_FLAG_TANGENT_ON_IDENTITY = 1
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
@@ -55,7 +56,7 @@ class EmSide(ctypes.Structure):
 
 class EmOptions(ctypes.Structure):
     _fields_ = [("precision", _i32), ("chain", _i32), ("device", _i32), ("block", _i32),
-                ("grid", _i32), ("reserved", _i32)]
+                ("grid", _i32), ("flags", _i32)]
 
 
 class EmOutputs(ctypes.Structure):
@@ -117,6 +118,7 @@ def lib():
         "em_plan_run_raw": ([_p, _u64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p],
                             ctypes.c_int),
         "em_bin_points": ([_p, _p, _i64, _p, _p, _p], ctypes.c_int),
+        "em_debug_step": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
         "em_fp32_peak": ([ctypes.c_int, _p, _p], ctypes.c_int),
         "em_philox4x64_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "em_philox4x32_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),

@@ -319,7 +319,8 @@ class Plan:
 
     def __init__(self, geom: GeomPack, ksqrt, poles, eps: float, max_steps: int,
                  side0, side1, precision: str | None = None, chain: str | None = None,
-                 device: int | None = None, pole_ids=None, block: int = 0, grid: int = 0):
+                 device: int | None = None, pole_ids=None, block: int = 0, grid: int = 0,
+                 flags: int = 0):
         precision = (precision or default_precision()).lower()
         if precision not in _PRECISIONS:
             raise ValidationError(f"unknown precision {precision!r}")
@@ -348,7 +349,7 @@ class Plan:
         # job-order scan does (S/backend.py:189-192)
         self.pole_ids = None if pid is None else pid.copy()
         opt = N.EmOptions(_PRECISIONS[precision], _CHAINS[chain], self.device, int(block),
-                          int(grid), 0)
+                          int(grid), int(flags))
         h = ctypes.c_void_p()
         N.check(N.lib().em_plan_create(ctypes.byref(g), ctypes.byref(s0), ctypes.byref(s1),
                                        N.ptr(pl), N.ptr(pid) if pid is not None else None,
@@ -482,6 +483,20 @@ class Plan:
         N.check(N.lib().em_bin_points(self._h, N.ptr(pts), n, N.ptr(comp), N.ptr(side),
                                       N.ptr(bins)), "em_bin_points")
         return comp, side, bins
+
+    def debug_step(self, x, words):
+        """ONE step of the plan's FP32 chain from each world point x (n, d)
+        with random words (n, 2) uint32 (em_debug_step): (candidate next
+        points (n, d), 0/1 stop masks at x)."""
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, self.d)
+        w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1, 2)
+        if w.shape[0] != x.shape[0]:
+            raise ValidationError("one word pair per point")
+        y = np.empty_like(x)
+        mask = np.empty(x.shape[0], dtype=np.float32)
+        N.check(N.lib().em_debug_step(self._h, N.ptr(x), N.ptr(w), x.shape[0], N.ptr(y),
+                                      N.ptr(mask)), "em_debug_step")
+        return y, mask
 
     def last_stats(self):
         ms = ctypes.c_double(0)

@@ -48,6 +48,9 @@ cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
 const char* f32_build_knobs();
+cudaError_t launch_debug_step(const F32Params& P, int d, int outer, int nh_mode, int chain,
+                              bool ident, const double* x, const unsigned* words, long long n,
+                              double* y, float* mask, cudaStream_t s);
 
 struct GridHost {
   double lo[3];
@@ -435,7 +438,7 @@ std::shared_ptr<DeviceGrid> cached_device_grid(const double* anchors, int64_t m,
 // balls) and the 2D ball with at most one concentric hole (rolling disks,
 // hole-tangent disks); elsewhere it runs EM_CHAIN_MAX.  Expects a validated
 // geometry and a supported (precision, chain) pair.
-int resolve_chain(const em_geometry* g, int precision, int chain) {
+int resolve_chain(const em_geometry* g, int precision, int chain, bool on_identity = false) {
   if (precision != EM_PREC_FP32 || chain != EM_CHAIN_TANGENT) return chain;
   const int d = (int)g->gi[0];
   const int64_t nh = g->gi[2], nn = g->gi_len >= 4 ? g->gi[3] : 0;
@@ -449,7 +452,7 @@ int resolve_chain(const em_geometry* g, int precision, int chain) {
   bool conc = nh == 1;
   for (int j = 0; conc && j < d; ++j) conc = g->gf[d + 1 + j] == g->gf[j];
   const bool okd = d == 2 && g->gi[1] == 0 && nn == 0 && (nh == 0 || conc);
-  return ((ok2 || ok3 || okb || okd) && !id) ? EM_CHAIN_TANGENT : EM_CHAIN_MAX;
+  return ((ok2 || ok3 || okb || okd) && (!id || on_identity)) ? EM_CHAIN_TANGENT : EM_CHAIN_MAX;
 }
 
 int validate_geometry(const em_geometry* g) {
@@ -582,7 +585,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->device = o.device;
   p->precision = o.precision;
   p->chain = o.chain;
-  p->chain = resolve_chain(g, o.precision, o.chain);
+  const bool on_identity = (o.flags & EM_FLAG_TANGENT_ON_IDENTITY) != 0;
+  p->chain = resolve_chain(g, o.precision, o.chain, on_identity);
   p->d = d;
   p->outer = nn ? OUTER_LBOX : (int)g->gi[1];
   p->n_holes = nh;
@@ -606,6 +610,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   for (int i = 0; i < d; ++i)
     for (int j = 0; j < d; ++j)
       if (g->ksqrt[i * d + j] != (i == j ? 1.0 : 0.0)) ident = false;
+  // the forced tangent chain runs its general (K != I) kernels on K = I
+  if (on_identity && p->chain == EM_CHAIN_TANGENT) ident = false;
   p->ident = ident;
 
   const int64_t row = p->n0 + p->n1;
@@ -1530,6 +1536,30 @@ int em_bin_points(em_plan* p, const double* pts, int64_t n, int64_t* comp, int64
   EM_CUDA(cudaMemcpyAsync(comp, dc.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
   EM_CUDA(cudaMemcpyAsync(side, ds.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
   EM_CUDA(cudaMemcpyAsync(bin, db.p, (size_t)n * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaStreamSynchronize(p->stream));
+  return EM_OK;
+}
+
+int em_debug_step(em_plan* p, const double* x, const uint32_t* words, int64_t n, double* y,
+                  float* mask) {
+  if (!p || (n > 0 && (!x || !words || !y || !mask))) return fail(EM_ERR_INVALID, "null");
+  if (p->precision != EM_PREC_FP32) return fail(EM_ERR_UNSUPPORTED, "em_debug_step: FP32 plans only");
+  if (n <= 0) return EM_OK;
+  DeviceGuard dg(p->device);
+  DevBuf dx, dw, dy, dm;
+  cudaError_t ce;
+  if ((ce = dx.alloc((size_t)n * p->d * 8)) != cudaSuccess || (ce = dw.alloc((size_t)n * 8)) != cudaSuccess ||
+      (ce = dy.alloc((size_t)n * p->d * 8)) != cudaSuccess || (ce = dm.alloc((size_t)n * 4)) != cudaSuccess)
+    return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+  EM_CUDA(cudaMemcpyAsync(dx.p, x, (size_t)n * p->d * 8, cudaMemcpyHostToDevice, p->stream));
+  EM_CUDA(cudaMemcpyAsync(dw.p, words, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream));
+  cudaError_t e = launch_debug_step(p->p32, p->d, p->outer, p->nh_mode, p->chain, p->ident,
+                                    dx.as<double>(), dw.as<unsigned>(), n, dy.as<double>(),
+                                    dm.as<float>(), p->stream);
+  if (e == cudaErrorInvalidValue) return fail(EM_ERR_UNSUPPORTED, "em_debug_step: no such kernel family");
+  if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("debug step: ") + cudaGetErrorString(e));
+  EM_CUDA(cudaMemcpyAsync(y, dy.p, (size_t)n * p->d * 8, cudaMemcpyDeviceToHost, p->stream));
+  EM_CUDA(cudaMemcpyAsync(mask, dm.p, (size_t)n * 4, cudaMemcpyDeviceToHost, p->stream));
   EM_CUDA(cudaStreamSynchronize(p->stream));
   return EM_OK;
 }

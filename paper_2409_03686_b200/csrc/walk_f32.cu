@@ -1265,7 +1265,118 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
   }
 }
 
+// One step of the walk chain from world points (em_debug_step): the same
+// device functions as walk_f32_kernel, exposed so tests can check each
+// sampler against closed forms (every landing point of a step lies on one
+// whitened sphere and follows its Poisson kernel seen from the start point).
+template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
+__global__ void __launch_bounds__(128) debug_step_kernel(const F32Params P, const double* xin,
+                                                         const unsigned* words, long long n,
+                                                         double* yout, float* mout) {
+  constexpr bool SHEAR = Shear<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool ROLL = Roll<D, OUTER, NH, CHAIN, IDENT>::value;
+  constexpr bool SCALED = SHEAR || TANG;
+  __shared__ __align__(16) float ttab[72];
+  if (TANG && D == 3) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 72; ++k) ttab[k] = P.t3[k / 24][k % 24];
+    }
+    __syncthreads();
+  }
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  // world -> kernel coordinates (capi.cu's to_kernel on the device)
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < D; ++k) v[k] = xin[j * D + k] - (double)P.frame[k];
+  float x[3] = {0.0f, 0.0f, 0.0f};
+  for (int k = 0; k < D; ++k) {
+    double t = 0.0;
+    if (OUTER == OUTER_BALL && P.rot) {
+      for (int i = 0; i < D; ++i) t += (double)P.Q[3 * i + k] * v[i];
+    } else if (SCALED) {
+      t = v[k] / (double)P.ax[k];
+    } else {
+      t = v[k];
+    }
+    x[k] = (float)t;
+  }
+  const unsigned w0 = words[2 * j], w1 = words[2 * j + 1];
+  float nx[3] = {x[0], x[1], x[2]}, m = 0.0f;
+  if (ROLL && D == 3) {
+    m = roll_step3(P, x, w0, P.one_bits, nx);
+  } else if (ROLL) {
+    m = roll_step2<NH>(P, x, w0, P.one_bits, nx);
+  } else if (TANG && D == 2) {
+    m = tangent_step(P, x, w0, P.one_bits, nx[0], nx[1]);
+  } else if (TANG) {
+    m = tangent_step3<OUTER>(P, ttab, x, w0, P.one_bits, nx);
+  } else {
+    // the batch layout of the woe / max chains: z words, then azimuth words
+    const unsigned wv[8] = {w0, w0, w0, w0, D == 3 ? w1 : w0, w1, w1, w1};
+    float t, r;
+    dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
+    m = t;
+    step<D, OUTER, IDENT, SHEAR>(P, nx, r, D == 3 ? z_of<D>(wv, 0, P.one_bits) : 0.0f,
+                                 angle_bits<D>(wv, 0, P.one_bits));
+  }
+  // kernel -> world in double (the exits mode's conversion)
+  double xd[3] = {(double)nx[0], (double)nx[1], D == 3 ? (double)nx[2] : 0.0};
+  if (OUTER == OUTER_BALL && P.rot) {
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < D; ++i)
+      for (int k = 0; k < D; ++k) t[i] += (double)P.Q[3 * i + k] * xd[k];
+    for (int i = 0; i < D; ++i) xd[i] = t[i];
+  } else if (SCALED) {
+    for (int i = 0; i < D; ++i) xd[i] *= (double)P.ax[i];
+  }
+  for (int k = 0; k < D; ++k) yout[j * D + k] = xd[k] + (double)P.frame[k];
+  mout[j] = m;
+}
+
 }  // namespace f32
+
+cudaError_t launch_debug_step(const F32Params& P, int d, int outer, int nh_mode, int chain,
+                              bool ident, const double* x, const unsigned* words, long long n,
+                              double* y, float* mask, cudaStream_t s) {
+  using namespace f32;
+  using K = void (*)(F32Params, const double*, const unsigned*, long long, double*, float*);
+  K k = nullptr;
+  const int nh = nh_mode;  // 0: none, 1: one hole (2D ball), 2: runtime count
+#define EM_DBG(D_, O_, NH_, C_, I_) \
+  if (d == D_ && outer == O_ && nh == (NH_ < 0 ? 2 : NH_) && chain == C_ && ident == I_) \
+    k = debug_step_kernel<D_, O_, NH_, C_, I_>;
+  if (ident) {
+    EM_DBG(2, OUTER_BALL, 0, EM_CHAIN_WOE, true)
+    EM_DBG(3, OUTER_BALL, 0, EM_CHAIN_WOE, true)
+    EM_DBG(2, OUTER_BOX, 0, EM_CHAIN_WOE, true)
+  } else if (chain == EM_CHAIN_TANGENT) {
+    EM_DBG(2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false)
+    EM_DBG(3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false)
+    EM_DBG(3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false)
+    EM_DBG(3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false)
+    EM_DBG(2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false)
+    EM_DBG(2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false)
+  } else if (chain == EM_CHAIN_MAX) {
+    EM_DBG(2, OUTER_BOX, 0, EM_CHAIN_MAX, false)
+    EM_DBG(3, OUTER_BOX, 0, EM_CHAIN_MAX, false)
+    EM_DBG(3, OUTER_LBOX, 0, EM_CHAIN_MAX, false)
+    EM_DBG(3, OUTER_BALL, 0, EM_CHAIN_MAX, false)
+    EM_DBG(2, OUTER_BALL, 0, EM_CHAIN_MAX, false)
+    EM_DBG(2, OUTER_BALL, 1, EM_CHAIN_MAX, false)
+  } else {
+    EM_DBG(2, OUTER_BOX, 0, EM_CHAIN_WOE, false)
+    EM_DBG(3, OUTER_BOX, 0, EM_CHAIN_WOE, false)
+    EM_DBG(3, OUTER_BALL, 0, EM_CHAIN_WOE, false)
+    EM_DBG(2, OUTER_BALL, 0, EM_CHAIN_WOE, false)
+    EM_DBG(2, OUTER_BALL, 1, EM_CHAIN_WOE, false)
+  }
+#undef EM_DBG
+  if (!k) return cudaErrorInvalidValue;
+  k<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, x, words, n, y, mask);
+  return cudaGetLastError();
+}
 
 // Host dispatch over the instantiated (dimension, outer, holes, chain, K=I,
 // binner) combinations.  nh_mode: 0 = no holes, 1 = exactly one hole, 2 =

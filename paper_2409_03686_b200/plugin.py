@@ -107,10 +107,25 @@ def install(precision: str | None = None, chain: str | None = None, device: int 
     impl = types.ModuleType("exitmeasure_b200_impl")
     impl.walk_exits_chunk = B.walk_exits_chunk
     impl.accumulate_chunk = B.accumulate_chunk
+    if not hasattr(module, "_em_b200_original"):  # keep the reference's own entry points
+        module._em_b200_original = {k: getattr(module, k) for k in
+                                    ("run_accumulate", "run_exits", "_impl", "BACKEND")}
     module.run_accumulate = run_accumulate
     module.run_exits = run_exits
     module._impl = impl
     module.BACKEND = "cuda-" + (precision or B.default_precision())
+    return module
+
+
+def uninstall(module=None):
+    """Restore the reference's own backend entry points (after install)."""
+    if module is None:
+        import exitmeasure.backend as module
+    orig = getattr(module, "_em_b200_original", None)
+    if orig:
+        for k, v in orig.items():
+            setattr(module, k, v)
+        del module._em_b200_original
     return module
 
 
