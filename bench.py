@@ -348,7 +348,8 @@ def run_ours(args):
     s1 = backend.pack_side(cfg.fam1, cfg.d, cfg.eps)
     plan = backend.Plan(geom, cfg.kt.k_sqrt, cfg.poles[ids], cfg.eps, 10**6, s0, s1,
                         precision=args.precision, chain=args.chain, device=device,
-                        pole_ids=ids, grid=args.grid)
+                        pole_ids=ids, grid=args.grid,
+                        flags=_native.EM_FLAG_PERSISTENT if args.sched == "persistent" else 0)
     row = plan.n0 + plan.n1
     m_local = len(ids)
     m_pad = m_local if weak else -(-cfg.n_poles // world)
@@ -530,6 +531,7 @@ def run_ours(args):
                                                       if world > 1 else "")),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "counts": "int64 (n_poles, n0+n1) rows + step stats",
+                       "scheduler": plan.last_scheduler(),
                        "build": _native.build_info()},
             "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
                          "unit": "Top/s", "frac": achieved / peak_nominal,
@@ -662,6 +664,9 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
+    ap.add_argument("--sched", default="auto", choices=["auto", "persistent"],
+                    help="auto: pole-block histograms for long rows; persistent: force the "
+                         "pole-cycling persistent scheduler (A/B)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: strong (default) = cyclic row shard of the fixed workload + "
                          "NCCL all-gather of the rows inside every timed step; weak = every "

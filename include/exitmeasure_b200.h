@@ -134,6 +134,14 @@ typedef struct {
  * itself, so one step samples the domain's Poisson kernel exactly: the
  * closed-form test of the production samplers (tests/test_gpu_closed_form.py). */
 #define EM_FLAG_TANGENT_ON_IDENTITY 1
+/* Keep the persistent pole-cycling scheduler (per-exit int64 atomics) even
+ * where the pole-block scheduler would run: one block per (pole, replicate
+ * range), the row's histogram in shared memory with warp-aggregated
+ * (__match_any_sync) adds, flushed once per block -- the default for long
+ * rows (>= 1024 bins) on the tangent chains.  Counts are identical either
+ * way (every walk's stream is keyed by (seed, pole, replicate)); the flag
+ * exists for A/B measurements. */
+#define EM_FLAG_PERSISTENT 2
 
 /* Per-run outputs.  Host pointers for em_plan_run / em_run_accumulate,
  * device pointers for em_plan_run_device.  counts is (n_poles, n0 + n1)
@@ -215,6 +223,10 @@ int em_plan_last_stats(const em_plan* p, double* kernel_ms, int64_t* walks, int6
  * any zeroing/packing kernels) */
 int em_plan_last_launches(const em_plan* p, int64_t* launches);
 int64_t em_plan_n_bins(const em_plan* p, int side);
+/* scheduler of the last integer-count run: 0 persistent pole-cycling warps,
+ * 1 the same with per-warp shared step-statistics tables (tiny jobs), 2 the
+ * pole-block scheduler with per-block shared-memory histograms; -1 none */
+int em_plan_last_scheduler(const em_plan* p);
 /* the walk chain the plan runs (EM_CHAIN_*): EM_CHAIN_TANGENT falls back to
  * EM_CHAIN_MAX where no tangent-ball step exists for the geometry */
 int em_plan_chain(const em_plan* p);

@@ -35,6 +35,7 @@ EM_CHAIN_WOE = 0
 EM_CHAIN_MAX = 1
 EM_CHAIN_TANGENT = 2
 EM_FLAG_TANGENT_ON_IDENTITY = 1
+EM_FLAG_PERSISTENT = 2
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
@@ -110,6 +111,7 @@ def lib():
         "em_resolve_chain": ([ctypes.POINTER(EmGeometry), ctypes.c_int, ctypes.c_int],
                              ctypes.c_int),
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
+        "em_plan_last_scheduler": ([_p], ctypes.c_int),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),
                                ctypes.POINTER(EmSide), _p, _p, _i64, _u64, _dbl, _i64, _i64,
                                ctypes.POINTER(EmOptions), ctypes.POINTER(EmOutputs)],

@@ -505,6 +505,11 @@ class Plan:
         N.lib().em_plan_last_stats(self._h, ctypes.byref(ms), ctypes.byref(w), ctypes.byref(s))
         return ms.value, w.value, s.value
 
+    def last_scheduler(self) -> str:
+        """Scheduler of the last integer-count run (em_plan_last_scheduler)."""
+        return {0: "persistent", 1: "persistent+smem-stats", 2: "pole-blocks"}.get(
+            int(N.lib().em_plan_last_scheduler(self._h)), "none")
+
     def last_launches(self) -> int:
         v = ctypes.c_int64(0)
         N.lib().em_plan_last_launches(self._h, ctypes.byref(v))

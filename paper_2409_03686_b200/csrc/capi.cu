@@ -44,6 +44,7 @@ cudaError_t launch_zero_ranges(unsigned long long* const* ptrs, const long long*
 cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, long long n_poles,
                               unsigned long long* stats, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
+bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
@@ -269,6 +270,9 @@ struct em_plan {
   DevBuf xo, so, co;           // exits
   DevBuf ikind, iidx, itot, iside, iraw0, iraw1, iinit0, iinit1;
   int wkind[2] = {0, 0}, idw_power[2] = {2, 2};
+  int flags = 0;  // em_options.flags
+  bool pole_blocks = false;  // the FP32 kernel family has the pole-block scheduler
+  int last_sched = -1;       // scheduler of the last integer-count launch
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
@@ -595,6 +599,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   p->n0 = s0->n_anchors;
   p->n1 = s1->n_anchors;
   p->block = o.block > 0 ? o.block : 256;
+  p->flags = o.flags;
   auto bail = [&](int code) {
     delete p;
     return code;
@@ -1085,6 +1090,8 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       per_sm = nb;
   }
   p->grid = o.grid > 0 ? o.grid : sm_count_of(o.device) * per_sm * (256 / p->block > 0 ? 256 / p->block : 1);
+  if (p->precision == EM_PREC_FP32)
+    p->pole_blocks = f32_has_pole_blocks(p->d, p->outer, p->nh_mode, p->chain, p->ident, p->bink);
   *out = p;
   return EM_OK;
 }
@@ -1123,6 +1130,29 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     // (few rows, e.g. a row shard, or few walks per row) the flushes
     // serialise on the 3 n_poles addresses in L2: spread them over copies
     // (folded by a second kernel) so every address sees <= 32 / 2^17 per walk
+    // pole-block scheduler for long rows: one block per (pole, replicate
+    // range) in pole-major order, the row's histogram in shared memory, one
+    // flush per block (north_star's exit binning).  Concurrent blocks then
+    // share a handful of rows, which stay L2-resident, instead of every
+    // warp adding straight into rows spread over all poles (cfg5's 256 MiB
+    // of rows exceed the 126 MB L2).  Blocks hold ~1/24 of a resident wave's
+    // share of the walks, so the last wave's tail stays short.
+    w->bc = 0;
+    w->splits = 0;
+    const int64_t row_len = p->n0 + p->n1;
+    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats && p->pole_blocks &&
+        !(p->flags & EM_FLAG_PERSISTENT) && row_len >= 1024 && row_len * 4 <= 160 * 1024 &&
+        n_rep >= 4096) {
+      long long bc = 1024;
+      while (bc < 65536 && (double)total / ((double)p->grid * 24.0) >= (double)(bc * 2)) bc *= 2;
+      if (bc > n_rep) bc = n_rep;
+      const long long splits = (n_rep + bc - 1) / bc;
+      if ((double)p->n_poles * (double)splits < 2147483647.0) {
+        w->bc = bc;
+        w->splits = splits;
+        w->smem_stats = 2;
+      }
+    }
     w->stat_copies = 1;
     if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats) {
       int c = 1;
@@ -1209,6 +1239,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   }
   p->last_launches = launches;
   p->last_walks = total;
+  if (mode == 0) p->last_sched = w->smem_stats;
   p->last_launch_stream = s;
   return EM_OK;
 }
@@ -1384,6 +1415,8 @@ int em_plan_last_launches(const em_plan* p, int64_t* launches) {
   *launches = p->last_launches;
   return EM_OK;
 }
+
+int em_plan_last_scheduler(const em_plan* p) { return p ? p->last_sched : -1; }
 
 int64_t em_plan_n_bins(const em_plan* p, int side) {
   if (!p) return -1;

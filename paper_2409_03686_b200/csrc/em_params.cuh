@@ -81,6 +81,10 @@ struct WorkOut {
   // warp flushes into copy (warp + lane) mod stat_copies, and a second kernel
   // folds the copies (spreads the flush atomics when many warps share a pole)
   int stat_copies;
+  // pole-block scheduler (walk_f32_kernel SMEM == 2): block b walks pole
+  // b / splits, replicates [(b % splits) * bc, + bc), into a shared-memory
+  // histogram of the row flushed once per block
+  long long bc, splits;
   unsigned long long *ssum, *ssq, *smax;
   // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
   // output block means "no failure" and the smallest key wins

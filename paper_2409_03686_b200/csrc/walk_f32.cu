@@ -967,7 +967,13 @@ __device__ __forceinline__ void frame_to_world(const F32Params& P, const float* 
   xw[2] = D == 3 ? xf[2] + P.frame[2] : 0.0f;
 }
 
-template <int D, int OUTER, int NH, int BINK, int SMEM, bool SHEAR>
+// Pole-block scheduler (SMEM == 2): the block's shared-memory histogram of
+// its one pole's count row (dynamic shared memory, row_len u32 words).
+__device__ __forceinline__ unsigned* block_hist() {
+  return reinterpret_cast<unsigned*>(s_stats);
+}
+
+template <int D, int OUTER, int NH, int BINK, int SMEM, bool SHEAR, bool FULL = true>
 __device__ __forceinline__ void retire(const F32Params& P, const float* x, int pole, int steps,
                                        StepAcc& acc) {
   const WorkOut& W = P.w;
@@ -982,6 +988,22 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
   EM_DEV_ASSERT(side == 0 || side == 1);
   EM_DEV_ASSERT(a >= 0 && a < (side ? P.side[1].n_anchors : P.side[0].n_anchors));
   EM_DEV_ASSERT(col >= 0 && col < W.row_len && pole >= 0 && pole < W.n_poles);
+  if (SMEM == 2) {
+    // one pole per block: warp-aggregated shared-memory histogram (all 32
+    // lanes bin together in the deferred pass: __match_any_sync groups equal
+    // bins, the lowest lane of each group adds the group's count)
+    unsigned* hist = block_hist();
+    if (FULL) {
+      const unsigned peers = __match_any_sync(kFull, col);
+      if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u) atomicAdd(&hist[col], __popc(peers));
+    } else {
+      atomicAdd(&hist[col], 1u);
+    }
+    acc.sum += (unsigned long long)steps;
+    acc.sq += (unsigned long long)steps * (unsigned long long)steps;
+    acc.mx = (unsigned long long)steps > acc.mx ? (unsigned long long)steps : acc.mx;
+    return;
+  }
   atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
   acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
@@ -1041,7 +1063,34 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
   pool_init(wp);
   StepAcc acc;
   acc_init(acc);
-  if (MODE == 0) stats_smem_init<SMEM>(W);
+  if (MODE == 0 && SMEM != 2) stats_smem_init<SMEM>(W);
+  // pole-block scheduler: this block walks replicates [r0, r0 + cnt) of one
+  // pole (pole-major block order: concurrent blocks share few rows, which
+  // stay L2-resident) into a shared histogram, flushed once at the end
+  __shared__ unsigned s_next, s_done;
+  __shared__ unsigned long long s_st[3];
+  long long bpole = 0, br0 = 0;
+  unsigned bcnt = 0;
+  if (SMEM == 2) {
+    bpole = (long long)blockIdx.x / W.splits;
+    br0 = ((long long)blockIdx.x - bpole * W.splits) * W.bc;
+    bcnt = (unsigned)(W.n_rep - br0 < W.bc ? W.n_rep - br0 : W.bc);
+    unsigned* hist = block_hist();
+    for (int i = threadIdx.x; i < W.row_len; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x == 0) {
+      s_next = 0u;
+      s_done = 0u;
+      s_st[0] = s_st[1] = s_st[2] = 0ULL;
+    }
+    __syncthreads();
+    const float4 p = __ldg(&P.poles[bpole]);
+    px = p.x;
+    py = p.y;
+    pz = p.z;
+    cpid = W.pole_ids ? (unsigned)W.pole_ids[bpole] : (unsigned)bpole;
+    cpole = (int)bpole;
+    acc.pole = (int)bpole;
+  }
   constexpr bool TANG = Tangent<D, OUTER, NH, CHAIN, IDENT>::value;
   constexpr bool ROLL = Roll<D, OUTER, NH, CHAIN, IDENT>::value;
   constexpr bool SCALED = SHEAR || TANG;  // axes stored scaled (to_frame)
@@ -1122,9 +1171,29 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
         W.steps_out[o] = steps;
         W.comp_out[o] = owner<D, OUTER, NH>(P, xf);
       }
-      if (pool_take_fast(wp, need, W, pole, rep_off, eq, lt)) {
+      bool took;
+      if (SMEM == 2) {
+        // claim replicates from the block's cursor (one shared atomic per warp)
+        took = false;
+        if (!wp.exhausted) {
+          const unsigned n_need = __popc(need);
+          unsigned base = 0u;
+          if (eq == 1u) base = atomicAdd(&s_next, n_need);
+          base = __shfl_sync(kFull, base, 0);
+          if (base + n_need >= bcnt) wp.exhausted = 1;
+          const unsigned k = base + __popc(need & lt);
+          if ((need & eq) && k < bcnt) {
+            pole = (int)bpole;
+            rep_off = (int)(br0 + k);
+            took = true;
+          }
+        }
+      } else {
+        took = pool_take_fast(wp, need, W, pole, rep_off, eq, lt);
+      }
+      if (took) {
         EM_DEV_ASSERT(pole >= 0 && pole < W.n_poles && rep_off >= 0 && rep_off < W.n_rep);
-        if (pole != cpole) {
+        if (SMEM != 2 && pole != cpole) {
           const float4 p = __ldg(&P.poles[pole]);
           px = p.x;
           py = p.y;
@@ -1258,10 +1327,47 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
       const ExitQueue& q = q_all[threadIdx.x >> 5];
       const float4 e = q.x[lane];
       const float ex[3] = {e.x, e.y, e.z};
-      retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, __float_as_int(e.w), q.s[lane], acc);
+      retire<D, OUTER, NH, BINK, SMEM, SCALED, false>(P, ex, __float_as_int(e.w), q.s[lane], acc);
     }
-    acc_flush<SMEM>(acc, W);
-    stats_smem_flush<SMEM>(W);
+    if (SMEM == 2) {
+      // step statistics: warp reduction, then the block's shared totals
+      unsigned long long sm = acc.sum, sq = acc.sq, mx = acc.mx;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sm += __shfl_xor_sync(kFull, sm, o);
+        sq += __shfl_xor_sync(kFull, sq, o);
+        const unsigned long long t = __shfl_xor_sync(kFull, mx, o);
+        mx = t > mx ? t : mx;
+      }
+      unsigned last = 0u;
+      if (eq == 1u) {
+        atomicAdd(&s_st[0], sm);
+        atomicAdd(&s_st[1], sq);
+        atomicMax(&s_st[2], mx);
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1u) == (unsigned)(blockDim.x / 32 - 1);
+      }
+      last = __shfl_sync(kFull, last, 0);
+      if (last) {
+        // the block's last warp flushes the row: one int64 atomic per
+        // touched bin, then the pole's statistics
+        __threadfence_block();
+        const unsigned* hist = block_hist();
+        unsigned long long* row = W.counts + bpole * W.row_len;
+        for (int i = lane; i < W.row_len; i += 32) {
+          const unsigned v = hist[i];
+          if (v) atomicAdd(&row[i], (unsigned long long)v);
+        }
+        if (eq == 1u) {
+          atomicAdd(&W.ssum[bpole], s_st[0]);
+          atomicAdd(&W.ssq[bpole], s_st[1]);
+          atomicMax(&W.smax[bpole], s_st[2]);
+        }
+      }
+    } else {
+      acc_flush<SMEM>(acc, W);
+      stats_smem_flush<SMEM>(W);
+    }
   }
 }
 
@@ -1384,6 +1490,16 @@ cudaError_t launch_debug_step(const F32Params& P, int d, int outer, int nh_mode,
 // them; everything else takes BIN_ANY.
 using F32Kernel = void (*)(F32Params);
 
+// smem: 0 = persistent pole-cycling warps, 1 = the same with per-warp shared
+// step-statistics tables (tiny jobs), 2 = the pole-block scheduler with a
+// shared-memory histogram per block (capi.cu picks it for long rows; only
+// the closed-form / grid binners are instantiated with it)
+#define EM_SCHED3(ARGS, BK)                                                          \
+  (smem == 2 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 2>                              \
+             : (smem ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 1>                      \
+                     : walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 0>))
+#define EM_UNPAREN(...) __VA_ARGS__
+
 template <int D, int OUTER, int NH, int BINK, int SM>
 static F32Kernel pick_chain_sm(int mode, int chain, bool ident) {
   using namespace f32;
@@ -1399,6 +1515,7 @@ static F32Kernel pick_chain_sm(int mode, int chain, bool ident) {
 
 template <int D, int OUTER, int NH, int BINK>
 static F32Kernel pick_chain(int mode, int chain, bool ident, int smem) {
+  if (smem == 2) return nullptr;  // the pole-block scheduler: tangent chains only
   return smem ? pick_chain_sm<D, OUTER, NH, BINK, 1>(mode, chain, ident)
               : pick_chain_sm<D, OUTER, NH, BINK, 0>(mode, chain, ident);
 }
@@ -1419,17 +1536,15 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
       if (nh_mode == 0) {
         if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
         if (bink == BIN_CIRCLE)
-          return smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 1>
-                      : walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 0>;
-        return smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+          return EM_SCHED3((2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false), BIN_CIRCLE);
+        return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
       }
       if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_CIRCLE)
-        return smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 1>
-                    : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_CIRCLE, 0>;
-      return smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
-                  : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+        return EM_SCHED3((2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false), BIN_CIRCLE);
+      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (outer == OUTER_BALL) {
       if (nh_mode == 0) return pick_bin<2, OUTER_BALL, 0, BIN_CIRCLE, BIN_ANY>(mode, chain, ident, bink, smem);
@@ -1442,12 +1557,10 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
         // resolves EM_CHAIN_TANGENT to EM_CHAIN_MAX everywhere else)
         if (mode != 0) return walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
         if (bink == BIN_SQUARE)
-          return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_SQUARE, 1>
-                      : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_SQUARE, 0>;
+          return EM_SCHED3((2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_SQUARE);
         if (bink == BIN_GRID)
-          return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
-                      : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
-        return smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+          return EM_SCHED3((2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
+        return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
       }
       if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink, smem);
@@ -1460,10 +1573,9 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
       // rolling balls (capi.cu resolves the chain)
       if (mode != 0) return walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_GRID)
-        return smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
-                    : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
-      return smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
-                  : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+        return EM_SCHED3((3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
+      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
     return pick_bin<3, OUTER_BALL, -1, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
@@ -1473,17 +1585,15 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
     if (outer == OUTER_BOX) {
       if (mode != 0) return walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_GRID)
-        return smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
-                    : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
-      return smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
-                  : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+        return EM_SCHED3((3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
+      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (mode != 0) return walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
     if (bink == BIN_GRID)
-      return smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 1>
-                  : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_GRID, 0>;
-    return smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
-                : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
+      return EM_SCHED3((3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
+    return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+                    : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
   }
   if (outer == OUTER_BOX) {
     if (nh_mode == 0) return pick_bin<3, OUTER_BOX, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
@@ -1496,11 +1606,34 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
                        bool ident, int bink, int grid, int block, cudaStream_t s) {
   if (block != 32 * f32::kWarps) return cudaErrorInvalidConfiguration;
-  F32Kernel k = pick_f32(d, outer, nh_mode, mode, chain, ident, bink, P.w.smem_stats);
+  const int sched = mode == 0 ? P.w.smem_stats : 0;
+  F32Kernel k = pick_f32(d, outer, nh_mode, mode, chain, ident, bink, sched);
   if (!k) return cudaErrorInvalidValue;
-  const size_t smem = (mode == 0 && P.w.smem_stats) ? (size_t)f32::kWarps * 3 * P.w.n_poles * 8 : 0;
+  size_t smem = 0;
+  if (sched == 1) smem = (size_t)f32::kWarps * 3 * P.w.n_poles * 8;
+  if (sched == 2) {
+    // one block per (pole, replicate range), the row's histogram in shared
+    smem = ((size_t)P.w.row_len * 4 + 15) & ~(size_t)15;
+    grid = (int)(P.w.n_poles * P.w.splits);
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> set;
+    std::lock_guard<std::mutex> lk(mu);
+    bool done = false;
+    for (auto& e : set)
+      if (e.first == (const void*)k && e.second >= smem) done = true;
+    if (!done) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      set.push_back({(const void*)k, smem});
+    }
+  }
   k<<<grid, block, smem, s>>>(P);
   return cudaGetLastError();
+}
+
+// the pole-block scheduler exists for this plan's kernel family
+bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink) {
+  return pick_f32(d, outer, nh_mode, 0, chain, ident, bink, 2) != nullptr;
 }
 
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink,
