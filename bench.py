@@ -349,7 +349,8 @@ def run_ours(args):
     plan = backend.Plan(geom, cfg.kt.k_sqrt, cfg.poles[ids], cfg.eps, 10**6, s0, s1,
                         precision=args.precision, chain=args.chain, device=device,
                         pole_ids=ids, grid=args.grid,
-                        flags=_native.EM_FLAG_PERSISTENT if args.sched == "persistent" else 0)
+                        flags={"auto": 0, "persistent": _native.EM_FLAG_PERSISTENT,
+                               "pole-blocks": _native.EM_FLAG_POLE_BLOCKS}[args.sched])
     row = plan.n0 + plan.n1
     m_local = len(ids)
     m_pad = m_local if weak else -(-cfg.n_poles // world)
@@ -664,9 +665,10 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
-    ap.add_argument("--sched", default="auto", choices=["auto", "persistent"],
-                    help="auto: pole-block histograms for long rows; persistent: force the "
-                         "pole-cycling persistent scheduler (A/B)")
+    ap.add_argument("--sched", default="auto", choices=["auto", "persistent", "pole-blocks"],
+                    help="long rows: auto = pole-major persistent warps with warp-aggregated "
+                         "atomics; pole-blocks = per-block shared-memory histograms; "
+                         "persistent = pole-cycling warps, one atomic per exit (A/B)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: strong (default) = cyclic row shard of the fixed workload + "
                          "NCCL all-gather of the rows inside every timed step; weak = every "

@@ -11,12 +11,26 @@
 # - CFLAGS pin -O2 -ffp-contract=off so the reference's FP64 arithmetic is not
 #   FMA-contracted (the SURVEY's F1 bit-reproducibility condition).
 # - This is test infrastructure: nothing on the product path imports it.
+# - The reference's own test suite is copied beside it (oracle/_ref/ref_tests,
+#   same git-ignore / travel rules) so tests/test_gpu_refsuite.py can run it
+#   on the GPU box against this backend (the box has no /root/reference).
+#   `build_ref.sh --tests-only` refreshes just that copy.
 set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
 REF="${REFERENCE_ROOT:-/root/reference}/pkg"
 OUT="$HERE/_ref"
 if [ ! -d "$REF" ]; then
   echo "build_ref: $REF absent (GPU box?) - keeping prebuilt $OUT" >&2
+  exit 0
+fi
+copy_tests() {
+  rm -rf "$OUT/ref_tests"
+  cp -r "$REF/tests" "$OUT/ref_tests"
+  # the reference's pytest settings (R/pkg/pyproject.toml [tool.pytest.ini_options])
+  printf '[pytest]\naddopts = -m "not nightly"\nmarkers =\n    nightly: long-running checks\n    slow: heavier statistical tests\n' > "$OUT/ref_tests/pytest.ini"
+}
+if [ "${1:-}" = "--tests-only" ]; then
+  copy_tests
   exit 0
 fi
 TMP="$(mktemp -d /tmp/emref.XXXXXX)"
@@ -27,6 +41,7 @@ mkdir -p "$OUT"
 CFLAGS="-O2 -ffp-contract=off" python -m pip install --quiet --no-index \
   --no-build-isolation --no-deps --find-links /opt/wheelhouse \
   --target "$OUT" "$TMP/pkg"
+copy_tests
 python - "$OUT" <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])

@@ -36,6 +36,7 @@ EM_CHAIN_MAX = 1
 EM_CHAIN_TANGENT = 2
 EM_FLAG_TANGENT_ON_IDENTITY = 1
 EM_FLAG_PERSISTENT = 2
+EM_FLAG_POLE_BLOCKS = 4
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64

@@ -741,6 +741,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         rb = std::min(rb, lim);
         P.rho_h = (float)(lim * (1.0 - 1e-6));
         P.rho_h2 = (float)((double)P.rho_h * (double)P.rho_h);
+        P.mid2 = (float)(0.25 * (gf[d] + gf[d + 1 + d]) * (gf[d] + gf[d + 1 + d]));
       }
       rb *= 1.0 - 1e-6;
       P.rho_b = (float)rb;
@@ -1139,10 +1140,12 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     // share of the walks, so the last wave's tail stays short.
     w->bc = 0;
     w->splits = 0;
+    w->nbp = (n_rep + rb - 1) / rb;
+    w->inv_nbp = 1.0 / (double)std::max<long long>(w->nbp, 1);
     const int64_t row_len = p->n0 + p->n1;
-    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats && p->pole_blocks &&
-        !(p->flags & EM_FLAG_PERSISTENT) && row_len >= 1024 && row_len * 4 <= 160 * 1024 &&
-        n_rep >= 4096) {
+    const bool long_rows = p->precision == EM_PREC_FP32 && mode == 0 && p->pole_blocks &&
+                           !(p->flags & EM_FLAG_PERSISTENT) && row_len >= 1024 && n_rep >= 4096;
+    if (long_rows && (p->flags & EM_FLAG_POLE_BLOCKS) && row_len * 4 <= 160 * 1024) {
       long long bc = 1024;
       while (bc < 65536 && (double)total / ((double)p->grid * 24.0) >= (double)(bc * 2)) bc *= 2;
       if (bc > n_rep) bc = n_rep;
@@ -1152,10 +1155,14 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
         w->splits = splits;
         w->smem_stats = 2;
       }
+    } else if (long_rows) {
+      w->smem_stats = 3;  // persistent, pole-major, warp-aggregated atomics
     }
     w->stat_copies = 1;
-    if (p->precision == EM_PREC_FP32 && mode == 0 && !w->smem_stats) {
-      int c = 1;
+    if (p->precision == EM_PREC_FP32 && mode == 0 && (w->smem_stats == 0 || w->smem_stats == 3)) {
+      // pole-major chunks put every warp on the same few poles: spread the
+      // statistics flushes over at least 8 copies
+      int c = w->smem_stats == 3 ? 8 : 1;
       while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 131072.0) c *= 2;
       w->stat_copies = c;
     }

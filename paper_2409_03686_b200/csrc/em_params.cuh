@@ -85,6 +85,10 @@ struct WorkOut {
   // b / splits, replicates [(b % splits) * bc, + bc), into a shared-memory
   // histogram of the row flushed once per block
   long long bc, splits;
+  // pole-major chunk order (walk_f32_kernel SMEM == 3): chunk c -> pole
+  // c / nbp, replicate block c % nbp (nbp = chunks per pole)
+  long long nbp;
+  double inv_nbp;
   unsigned long long *ssum, *ssq, *smax;
   // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
   // output block means "no failure" and the smallest key wins
@@ -170,6 +174,7 @@ struct F32Params {
   // whitened ellipsoid, R min(Ad) / max(Ad)^2) roll freely inside it
   float rho_b, rho_b2;
   float rho_h, rho_h2;  // 2D concentric annulus: disks tangent to the hole from outside
+  float mid2;           // ((R + rho) / 2)^2: which boundary's disk a step tries (EM_ROLL2_ONE)
   // EM_ROLL2_DYN: per-step radii (R - rho)(1 - 1e-6) / (max Ad + |diag(Ad) n|)
   float rb_bl, gap, amax, K4[3];
   float ia[3];      // 1 / Ad

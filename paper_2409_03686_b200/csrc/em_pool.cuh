@@ -101,7 +101,10 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
 // (the current chunk covers every idle lane) is straight-line predicated
 // code; only a chunk claim branches.  eq / lt are this lane's bit and the
 // bits below it, kept in registers by the caller.
-template <class RepT>
+// PM (pole-major): chunk c -> (pole c / nbp, replicate block c % nbp), so the
+// warps in flight share a handful of rows (L2-resident even when all rows
+// are not) -- the persistent scheduler's order for long rows.
+template <class RepT, bool PM = false>
 __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask, const WorkOut& W,
                                                int& pole, RepT& rep_off, unsigned eq, unsigned lt) {
   const int n_need = __popc(need_mask);
@@ -120,14 +123,27 @@ __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask,
       if (c >= W.n_chunks) {
         wp.exhausted = 1;
       } else {
-        long long b = (long long)((double)c * W.inv_poles);
-        long long p = (long long)c - b * W.n_poles;
-        if (p < 0) {
-          b -= 1;
-          p += W.n_poles;
-        } else if (p >= W.n_poles) {
-          b += 1;
-          p -= W.n_poles;
+        long long b, p;
+        if (PM) {
+          p = (long long)((double)c * W.inv_nbp);
+          b = (long long)c - p * W.nbp;
+          if (b < 0) {
+            p -= 1;
+            b += W.nbp;
+          } else if (b >= W.nbp) {
+            p += 1;
+            b -= W.nbp;
+          }
+        } else {
+          b = (long long)((double)c * W.inv_poles);
+          p = (long long)c - b * W.n_poles;
+          if (p < 0) {
+            b -= 1;
+            p += W.n_poles;
+          } else if (p >= W.n_poles) {
+            b += 1;
+            p -= W.n_poles;
+          }
         }
         const long long r0 = b * W.rb;
         const int valid = (int)(W.n_rep - r0 < W.rb ? W.n_rep - r0 : W.rb);
@@ -182,7 +198,7 @@ __device__ __forceinline__ unsigned long long* warp_stats(const WorkOut& W) {
 template <int SMEM = -1>
 __device__ __forceinline__ void acc_flush(StepAcc& a, const WorkOut& W) {
   if (a.pole >= 0 && a.sum + a.mx > 0) {
-    if (SMEM == 1 || (SMEM < 0 && W.smem_stats)) {
+    if (SMEM == 1 || (SMEM < 0 && W.smem_stats == 1)) {
       unsigned long long* t = warp_stats(W);
       atomicAdd(&t[a.pole], a.sum);
       atomicAdd(&t[W.n_poles + a.pole], a.sq);
@@ -202,7 +218,7 @@ __device__ __forceinline__ void acc_flush(StepAcc& a, const WorkOut& W) {
 
 template <int SMEM = -1>
 __device__ __forceinline__ void stats_smem_init(const WorkOut& W) {
-  if (SMEM == 0 || (SMEM < 0 && !W.smem_stats)) return;
+  if ((SMEM >= 0 && SMEM != 1) || (SMEM < 0 && W.smem_stats != 1)) return;
   unsigned long long* t = warp_stats(W);
   for (int i = threadIdx.x & 31; i < 3 * W.n_poles; i += 32) t[i] = 0;
   __syncwarp();
@@ -210,7 +226,7 @@ __device__ __forceinline__ void stats_smem_init(const WorkOut& W) {
 
 template <int SMEM = -1>
 __device__ __forceinline__ void stats_smem_flush(const WorkOut& W) {
-  if (SMEM == 0 || (SMEM < 0 && !W.smem_stats)) return;
+  if ((SMEM >= 0 && SMEM != 1) || (SMEM < 0 && W.smem_stats != 1)) return;
   __syncwarp();
   const unsigned long long* t = warp_stats(W);
   const int n = (int)W.n_poles;

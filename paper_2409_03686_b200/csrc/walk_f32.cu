@@ -48,6 +48,10 @@
 #ifndef EM_ROLL2_DYN
 #define EM_ROLL2_DYN 0
 #endif
+// 2D annulus rolling chain: one candidate disk per step (mid-radius choice)
+#ifndef EM_ROLL2_ONE
+#define EM_ROLL2_ONE 1
+#endif
 
 namespace em {
 namespace f32 {
@@ -889,13 +893,34 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
     rb2 = rb * rb;
     rh2 = rh * rh;
   }
+  float w0, w1, d2, rho;
+  bool use;
+  if (NH == 1 && EM_ROLL2_ONE && !EM_ROLL2_DYN) {
+    // ONE candidate disk per step: the outer rolling disk when |x| lies
+    // beyond the annulus' mid radius, else the hole-tangent disk (same
+    // offset algebra with the hole's radius and a negative signed radius);
+    // z must lie inside it and on its near side, else the centred disk.
+    // Any disk containing z inside the domain is a valid step; this choice
+    // matches trying the outer disk first and then the hole's (same steps
+    // per walk on cfg3), at one disk's cost instead of two.
+    const bool outer = s2 > P.mid2;
+    const float rc = outer ? rb : rh, rc2 = outer ? rb2 : rh2;
+    const float bs = outer ? rb : -rh;  // signed radius: inward from the outer circle
+    const float al = fmaf(outer ? -P.oR : -P.hr[0], ir, 1.0f);
+    const float be = bs * iaa;
+    w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
+    w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
+    d2 = fmaf(w0, w0, w1 * w1);
+    use = (d2 < rc2) & (fmaf(al, s2, be * aa) * bs > 0.0f);
+    rho = use ? rc : rm;
+  } else {
   const float al = fmaf(-P.oR, ir, 1.0f);
   const float be = rb * iaa;
-  float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
-  float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
-  float d2 = fmaf(w0, w0, w1 * w1);
-  bool use = (d2 < rb2) & (fmaf(al, s2, be * aa) > 0.0f);
-  float rho = use ? rb : rm;
+  w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
+  w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
+  d2 = fmaf(w0, w0, w1 * w1);
+  use = (d2 < rb2) & (fmaf(al, s2, be * aa) > 0.0f);
+  rho = use ? rb : rm;
   if (NH == 1) {
     // disk tangent to the hole from outside, centre beyond the radial projection
     const float ah = fmaf(-P.hr[0], ir, 1.0f);
@@ -909,6 +934,7 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
     d2 = uh ? dh : d2;
     rho = uh ? rh : rho;
     use |= uh;
+  }
   }
   const float id = rsq(fmaxf(d2, 1e-30f));
   const float d = use ? d2 * id : 0.0f;
@@ -1004,7 +1030,17 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
     acc.mx = (unsigned long long)steps > acc.mx ? (unsigned long long)steps : acc.mx;
     return;
   }
-  atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
+  unsigned long long* cell = &W.counts[(long long)pole * W.row_len + col];
+  if (SMEM == 3 && FULL) {
+    // pole-major chunks: the 32 exits of a binning pass mostly share a row,
+    // and near-pole bins are hot -- one RED per distinct address, adding the
+    // group's count (__match_any_sync over the 64-bit address)
+    const unsigned peers = __match_any_sync(kFull, (unsigned long long)cell);
+    if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u)
+      atomicAdd(cell, (unsigned long long)__popc(peers));
+  } else {
+    atomicAdd(cell, 1ULL);
+  }
   acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
 
@@ -1189,7 +1225,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
           }
         }
       } else {
-        took = pool_take_fast(wp, need, W, pole, rep_off, eq, lt);
+        took = pool_take_fast<int, SMEM == 3>(wp, need, W, pole, rep_off, eq, lt);
       }
       if (took) {
         EM_DEV_ASSERT(pole >= 0 && pole < W.n_poles && rep_off >= 0 && rep_off < W.n_rep);
@@ -1495,7 +1531,8 @@ using F32Kernel = void (*)(F32Params);
 // shared-memory histogram per block (capi.cu picks it for long rows; only
 // the closed-form / grid binners are instantiated with it)
 #define EM_SCHED3(ARGS, BK)                                                          \
-  (smem == 2 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 2>                              \
+  (smem == 3 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 3> :                            \
+   smem == 2 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 2>                              \
              : (smem ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 1>                      \
                      : walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 0>))
 #define EM_UNPAREN(...) __VA_ARGS__
@@ -1515,7 +1552,7 @@ static F32Kernel pick_chain_sm(int mode, int chain, bool ident) {
 
 template <int D, int OUTER, int NH, int BINK>
 static F32Kernel pick_chain(int mode, int chain, bool ident, int smem) {
-  if (smem == 2) return nullptr;  // the pole-block scheduler: tangent chains only
+  if (smem >= 2) return nullptr;  // pole-block / pole-major schedulers: tangent chains only
   return smem ? pick_chain_sm<D, OUTER, NH, BINK, 1>(mode, chain, ident)
               : pick_chain_sm<D, OUTER, NH, BINK, 0>(mode, chain, ident);
 }
@@ -1537,13 +1574,13 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
         if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
         if (bink == BIN_CIRCLE)
           return EM_SCHED3((2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false), BIN_CIRCLE);
-        return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+        return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<2, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
       }
       if (mode != 0) return walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_CIRCLE)
         return EM_SCHED3((2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false), BIN_CIRCLE);
-      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+      return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<2, OUTER_BALL, 1, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (outer == OUTER_BALL) {
@@ -1560,7 +1597,7 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
           return EM_SCHED3((2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_SQUARE);
         if (bink == BIN_GRID)
           return EM_SCHED3((2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
-        return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+        return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<2, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
       }
       if (nh_mode == 0) return pick_bin<2, OUTER_BOX, 0, BIN_SQUARE, BIN_GRID>(mode, chain, ident, bink, smem);
@@ -1574,7 +1611,7 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
       if (mode != 0) return walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_GRID)
         return EM_SCHED3((3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
-      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+      return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<3, OUTER_BALL, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (nh_mode == 0) return pick_bin<3, OUTER_BALL, 0, BIN_GRID, BIN_ANY>(mode, chain, ident, bink, smem);
@@ -1586,13 +1623,13 @@ static F32Kernel pick_f32(int d, int outer, int nh_mode, int mode, int chain, bo
       if (mode != 0) return walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
       if (bink == BIN_GRID)
         return EM_SCHED3((3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
-      return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+      return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<3, OUTER_BOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
     }
     if (mode != 0) return walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 1, BIN_ANY, 0>;
     if (bink == BIN_GRID)
       return EM_SCHED3((3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false), BIN_GRID);
-    return smem == 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
+    return smem >= 2 ? (F32Kernel) nullptr : smem ? walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 1>
                     : walk_f32_kernel<3, OUTER_LBOX, 0, EM_CHAIN_TANGENT, false, 0, BIN_ANY, 0>;
   }
   if (outer == OUTER_BOX) {
@@ -1631,7 +1668,7 @@ cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mo
   return cudaGetLastError();
 }
 
-// the pole-block scheduler exists for this plan's kernel family
+// the pole-block / pole-major schedulers exist for this plan's kernel family
 bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink) {
   return pick_f32(d, outer, nh_mode, 0, chain, ident, bink, 2) != nullptr;
 }
@@ -1671,7 +1708,8 @@ const char* f32_build_knobs() {
          " EM_Z_BITS=" EM_STR(EM_Z_BITS) " EM_TANG_K=" EM_STR(EM_TANG_K)
          " EM_POST_STOP=" EM_STR(EM_POST_STOP) " EM_MIN_BLOCKS=" EM_STR(EM_MIN_BLOCKS)
          " EM_ROLL2_BLOCKS=" EM_STR(EM_ROLL2_BLOCKS) " EM_ROLL2_DYN=" EM_STR(EM_ROLL2_DYN)
-         " EM_TAB_WARP=" EM_STR(EM_TAB_WARP) " EM_DEBUG=" EM_STR(EM_DEBUG);
+         " EM_TAB_WARP=" EM_STR(EM_TAB_WARP) " EM_ROLL2_ONE=" EM_STR(EM_ROLL2_ONE)
+         " EM_DEBUG=" EM_STR(EM_DEBUG);
 }
 
 // ---- FP32 point binning (same owner/binner as the walk kernel) ----

@@ -1,13 +1,14 @@
-"""The two FP32 schedulers give identical results.
+"""The three FP32 schedulers give identical results.
 
-Long rows (>= 1024 bins: cfg3, cfg4, cfg5) run on the pole-block scheduler
--- one block per (pole, replicate range), the row's histogram in shared
-memory with warp-aggregated (__match_any_sync) adds, one int64 flush per
-block, north_star's exit binning -- instead of the persistent pole-cycling
-warps that add every exit straight into the int64 rows.  Every walk's random
-stream is keyed by (seed, pole, replicate) and all accumulation is integer,
-so counts and step statistics must agree EXACTLY (the reference's own
-chunking-invariance contract, T/test_backend.py:118-137)."""
+Long rows (>= 1024 bins: cfg3, cfg4, cfg5) run by default on persistent
+warps claiming chunks in pole-major order with warp-aggregated
+(__match_any_sync) int64 atomics; EM_FLAG_POLE_BLOCKS selects north_star's
+per-block shared-memory histograms (one block per (pole, replicate range),
+one flush per block); EM_FLAG_PERSISTENT the pole-cycling warps with one
+atomic per exit.  Every walk's random stream is keyed by (seed, pole,
+replicate) and all accumulation is integer, so counts and step statistics
+must agree EXACTLY (the reference's own chunking-invariance contract,
+T/test_backend.py:118-137)."""
 
 import numpy as np
 import pytest
@@ -23,14 +24,15 @@ def B():
     return backend
 
 
-def _pair(B, cfg, n_rep, pole_ids=None, rep_start=0, max_steps=10**6):
+def _all(B, cfg, n_rep, pole_ids=None, rep_start=0, max_steps=10**6):
     from paper_2409_03686_b200 import _native
 
     geom = B.pack_geometry(cfg.dom)
     s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
     s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
     out = {}
-    for name, flags in (("blocks", 0), ("persistent", _native.EM_FLAG_PERSISTENT)):
+    for name, flags in (("major", 0), ("blocks", _native.EM_FLAG_POLE_BLOCKS),
+                        ("persistent", _native.EM_FLAG_PERSISTENT)):
         with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, max_steps, s0, s1,
                     precision="fp32", pole_ids=pole_ids, flags=flags) as plan:
             try:
@@ -46,14 +48,17 @@ def test_pole_block_scheduler_equals_persistent(B, idx, n_poles, n_rep):
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(idx).subset(n_poles)
-    out = _pair(B, cfg, n_rep)
-    (rb, sb), (rp, sp) = out["blocks"], out["persistent"]
-    assert sb == "pole-blocks" and sp == "persistent", (sb, sp)
-    assert np.array_equal(rb.counts.sum(1), np.full(cfg.n_poles, n_rep))
-    assert np.array_equal(rb.counts, rp.counts)
-    assert np.array_equal(rb.steps_sum, rp.steps_sum)
-    assert np.array_equal(rb.steps_sq_sum, rp.steps_sq_sum)
-    assert np.array_equal(rb.steps_max, rp.steps_max)
+    out = _all(B, cfg, n_rep)
+    (rp, sp) = out["persistent"]
+    assert sp == "persistent"
+    assert np.array_equal(rp.counts.sum(1), np.full(cfg.n_poles, n_rep))
+    for name, want in (("major", "pole-major"), ("blocks", "pole-blocks")):
+        rb, sb = out[name]
+        assert sb == want, (name, sb)
+        assert np.array_equal(rb.counts, rp.counts), name
+        assert np.array_equal(rb.steps_sum, rp.steps_sum), name
+        assert np.array_equal(rb.steps_sq_sum, rp.steps_sq_sum), name
+        assert np.array_equal(rb.steps_max, rp.steps_max), name
 
 
 def test_pole_block_scheduler_shards_and_offsets(B):
@@ -63,11 +68,12 @@ def test_pole_block_scheduler_shards_and_offsets(B):
 
     cfg = configs.get(3).subset(16)
     ids = np.arange(1, 32, 2)
-    out = _pair(B, cfg, 30_000, pole_ids=ids, rep_start=123_457)
-    (rb, sb), (rp, _) = out["blocks"], out["persistent"]
-    assert sb == "pole-blocks"
-    assert np.array_equal(rb.counts, rp.counts)
-    assert np.array_equal(rb.steps_sum, rp.steps_sum)
+    out = _all(B, cfg, 30_000, pole_ids=ids, rep_start=123_457)
+    rp, _ = out["persistent"]
+    for name in ("major", "blocks"):
+        rb, _ = out[name]
+        assert np.array_equal(rb.counts, rp.counts), name
+        assert np.array_equal(rb.steps_sum, rp.steps_sum), name
 
 
 def test_pole_block_scheduler_budget_error(B):
@@ -78,10 +84,10 @@ def test_pole_block_scheduler_budget_error(B):
 
     cfg = configs.get(4).subset(5)
     ids = np.array([7, 3, 11, 2, 40])
-    out = _pair(B, cfg, 8192, pole_ids=ids, max_steps=3)
-    eb, sb = out["blocks"]
+    out = _all(B, cfg, 8192, pole_ids=ids, max_steps=3)
     ep, _ = out["persistent"]
-    assert sb == "pole-blocks"
-    assert isinstance(eb, WalkBudgetError) and isinstance(ep, WalkBudgetError)
-    assert (eb.pole, eb.replicate) == (ep.pole, ep.replicate)
-    assert eb.pole == 7  # first row of the plan
+    assert isinstance(ep, WalkBudgetError) and ep.pole == 7  # first row of the plan
+    for name in ("major", "blocks"):
+        eb, _ = out[name]
+        assert isinstance(eb, WalkBudgetError), name
+        assert (eb.pole, eb.replicate) == (ep.pole, ep.replicate), name
