@@ -666,9 +666,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
     ap.add_argument("--sched", default="auto", choices=["auto", "persistent", "pole-blocks"],
-                    help="long rows: auto = pole-major persistent warps with warp-aggregated "
-                         "atomics; pole-blocks = per-block shared-memory histograms; "
-                         "persistent = pole-cycling warps, one atomic per exit (A/B)")
+                    help="auto: per-block shared-memory histograms where the rows exceed half "
+                         "the L2, else pole-cycling persistent warps; pole-blocks / persistent "
+                         "force one (A/B)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: strong (default) = cyclic row shard of the fixed workload + "
                          "NCCL all-gather of the rows inside every timed step; weak = every "

@@ -134,17 +134,15 @@ typedef struct {
  * itself, so one step samples the domain's Poisson kernel exactly: the
  * closed-form test of the production samplers (tests/test_gpu_closed_form.py). */
 #define EM_FLAG_TANGENT_ON_IDENTITY 1
-/* Scheduler of the FP32 tangent-chain kernels for long rows (>= 1024 bins).
- * Default: persistent warps claiming chunks in POLE-MAJOR order (the warps
- * in flight share a handful of count rows, which stay L2-resident), every
- * 32-exit binning pass adding one int64 atomic per distinct bin
- * (__match_any_sync aggregation).  EM_FLAG_POLE_BLOCKS: one block per
- * (pole, replicate range), the row's histogram in shared memory with
- * warp-aggregated adds, flushed once per block.  EM_FLAG_PERSISTENT: the
- * pole-cycling persistent scheduler with one int64 atomic per exit (the
- * scheduler of short rows).  Counts are identical under all three (every
- * walk's stream is keyed by (seed, pole, replicate), all accumulation is
- * integer); the flags exist for A/B measurements. */
+/* Scheduler of the FP32 tangent-chain kernels (counts are identical under
+ * both: every walk's stream is keyed by (seed, pole, replicate) and all
+ * accumulation is integer).  Pole-cycling persistent warps add every exit
+ * straight into the int64 rows; the pole-block scheduler runs one block per
+ * (pole, replicate range) with the row's histogram in shared memory
+ * (warp-aggregated __match_any_sync adds, one flush per block).  Default:
+ * pole blocks where the rows (n_poles x (n0 + n1) x 8 B) exceed 64 MiB --
+ * half the L2 -- and rows are >= 1024 bins, else pole-cycling warps.  The
+ * flags force one or the other (A/B measurements). */
 #define EM_FLAG_PERSISTENT 2
 #define EM_FLAG_POLE_BLOCKS 4
 
@@ -230,8 +228,7 @@ int em_plan_last_launches(const em_plan* p, int64_t* launches);
 int64_t em_plan_n_bins(const em_plan* p, int side);
 /* scheduler of the last integer-count run: 0 persistent pole-cycling warps,
  * 1 the same with per-warp shared step-statistics tables (tiny jobs), 2 the
- * pole-block scheduler with per-block shared-memory histograms, 3 persistent
- * pole-major warps with warp-aggregated atomics; -1 none */
+ * pole-block scheduler with per-block shared-memory histograms; -1 none */
 int em_plan_last_scheduler(const em_plan* p);
 /* the walk chain the plan runs (EM_CHAIN_*): EM_CHAIN_TANGENT falls back to
  * EM_CHAIN_MAX where no tangent-ball step exists for the geometry */

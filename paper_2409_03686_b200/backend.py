@@ -507,8 +507,7 @@ class Plan:
 
     def last_scheduler(self) -> str:
         """Scheduler of the last integer-count run (em_plan_last_scheduler)."""
-        return {0: "persistent", 1: "persistent+smem-stats", 2: "pole-blocks",
-                3: "pole-major"}.get(
+        return {0: "persistent", 1: "persistent+smem-stats", 2: "pole-blocks"}.get(
             int(N.lib().em_plan_last_scheduler(self._h)), "none")
 
     def last_launches(self) -> int:

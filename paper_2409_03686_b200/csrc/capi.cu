@@ -741,7 +741,6 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         rb = std::min(rb, lim);
         P.rho_h = (float)(lim * (1.0 - 1e-6));
         P.rho_h2 = (float)((double)P.rho_h * (double)P.rho_h);
-        P.mid2 = (float)(0.25 * (gf[d] + gf[d + 1 + d]) * (gf[d] + gf[d + 1 + d]));
       }
       rb *= 1.0 - 1e-6;
       P.rho_b = (float)rb;
@@ -837,6 +836,10 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       }
       P.hr[h] = (float)gf[off + d];
       P.hr2[h] = (float)(gf[off + d] * gf[off + d]);
+    }
+    if (g->gi[1] == 0 && nh == 1) {  // owner / candidate-disk split of a shell
+      const double mid = 0.5 * (gf[d] + gf[d + 1 + d]);
+      P.mid2 = (float)(mid * mid);
     }
     if (nn) {
       const int off = (d + 1) * (1 + nh);
@@ -1026,6 +1029,20 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       for (int64_t i = 0; i < S->n_anchors; ++i)
         for (int j = 0; j < d; ++j) af[i * 4 + j] = (float)S->anchors[i * d + j];
       put(af.data(), (size_t)S->n_anchors * 16, (void**)&D.anchors);
+      // one uniform circle block: the Voronoi boundaries between consecutive
+      // anchors are the bisector rays at (k - 1/2 + phase) 2 pi / count
+      D.bis = nullptr;
+      if (D.n_blk == 1 && D.kind[0] == BLK_CIRCLE && D.count[0] <= kBisMax) {
+        const int cnt = D.count[0];
+        const double ph = S->blk_phase ? S->blk_phase[0] : 0.0;
+        std::vector<float> bt(2 * (size_t)cnt);
+        for (int k = 0; k < cnt; ++k) {
+          const double b = (k - 0.5 + ph) * (2.0 * M_PI / cnt);
+          bt[2 * k] = (float)std::cos(b);
+          bt[2 * k + 1] = (float)std::sin(b);
+        }
+        put(bt.data(), bt.size() * 4, (void**)&D.bis);
+      }
       // one generic block covering the family: accelerate with the grid
       if (D.n_blk == 1 && D.kind[0] == BLK_GENERIC && S->n_anchors > 8) {
         if (auto G = cached_device_grid(S->anchors, S->n_anchors, d, eps, o.device)) {
@@ -1131,21 +1148,24 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     // (few rows, e.g. a row shard, or few walks per row) the flushes
     // serialise on the 3 n_poles addresses in L2: spread them over copies
     // (folded by a second kernel) so every address sees <= 32 / 2^17 per walk
-    // pole-block scheduler for long rows: one block per (pole, replicate
-    // range) in pole-major order, the row's histogram in shared memory, one
-    // flush per block (north_star's exit binning).  Concurrent blocks then
-    // share a handful of rows, which stay L2-resident, instead of every
-    // warp adding straight into rows spread over all poles (cfg5's 256 MiB
-    // of rows exceed the 126 MB L2).  Blocks hold ~1/24 of a resident wave's
-    // share of the walks, so the last wave's tail stays short.
+    // pole-block scheduler (north_star's exit binning): one block per
+    // (pole, replicate range) in pole-major order, the row's histogram in
+    // shared memory with warp-aggregated adds, one int64 flush per block.
+    // Default where the count rows exceed half the 126 MB L2: there the
+    // pole-cycling warps' direct atomics miss L2 and re-read / write back
+    // DRAM sectors (cfg5: 40 GB of DRAM traffic for 267 MB of rows at full
+    // scale; pole blocks: 0.44 GB, at 1% lower walks/s).  L2-resident rows
+    // keep the pole-cycling persistent warps (1-4% faster there: no block
+    // tails).  Blocks hold ~1/24 of a resident wave's share of the walks, so
+    // the last wave's tail stays short.
     w->bc = 0;
     w->splits = 0;
-    w->nbp = (n_rep + rb - 1) / rb;
-    w->inv_nbp = 1.0 / (double)std::max<long long>(w->nbp, 1);
     const int64_t row_len = p->n0 + p->n1;
-    const bool long_rows = p->precision == EM_PREC_FP32 && mode == 0 && p->pole_blocks &&
-                           !(p->flags & EM_FLAG_PERSISTENT) && row_len >= 1024 && n_rep >= 4096;
-    if (long_rows && (p->flags & EM_FLAG_POLE_BLOCKS) && row_len * 4 <= 160 * 1024) {
+    const double row_bytes = (double)p->n_poles * (double)row_len * 8.0;
+    const bool want_blocks = (p->flags & EM_FLAG_POLE_BLOCKS) ||
+                             (!(p->flags & EM_FLAG_PERSISTENT) && row_bytes > 64.0 * 1024 * 1024);
+    if (p->precision == EM_PREC_FP32 && mode == 0 && p->pole_blocks && want_blocks &&
+        row_len >= 1024 && row_len * 4 <= 160 * 1024 && n_rep >= 4096) {
       long long bc = 1024;
       while (bc < 65536 && (double)total / ((double)p->grid * 24.0) >= (double)(bc * 2)) bc *= 2;
       if (bc > n_rep) bc = n_rep;
@@ -1155,14 +1175,10 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
         w->splits = splits;
         w->smem_stats = 2;
       }
-    } else if (long_rows) {
-      w->smem_stats = 3;  // persistent, pole-major, warp-aggregated atomics
     }
     w->stat_copies = 1;
-    if (p->precision == EM_PREC_FP32 && mode == 0 && (w->smem_stats == 0 || w->smem_stats == 3)) {
-      // pole-major chunks put every warp on the same few poles: spread the
-      // statistics flushes over at least 8 copies
-      int c = w->smem_stats == 3 ? 8 : 1;
+    if (p->precision == EM_PREC_FP32 && mode == 0 && w->smem_stats == 0) {
+      int c = 1;
       while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 131072.0) c *= 2;
       w->stat_copies = c;
     }

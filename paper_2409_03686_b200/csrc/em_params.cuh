@@ -31,6 +31,7 @@
 namespace em {
 
 constexpr int kMaxBlk = 16;         // structured anchor blocks per side
+constexpr int kBisMax = 16384;      // circle blocks binned by boundary table
 constexpr int kMaxComp = EM_MAX_HOLES + 2;
 constexpr int kGfMax = 4 + 4 * EM_MAX_HOLES + 2;
 
@@ -62,6 +63,9 @@ struct Side32 {
   float cx[kMaxBlk], cy[kMaxBlk], cz[kMaxBlk], radius[kMaxBlk], phase[kMaxBlk];
   float scale[kMaxBlk];  // circle: count/2pi, square: count/8h
   const float4* anchors;
+  // one uniform circle block (BIN_CIRCLE binner, count <= kBisMax): unit
+  // directions of the Voronoi boundaries, bis[k] between anchors k-1 and k
+  const float2* bis;
   int has_grid;
   Grid32 grid;
 };
@@ -85,10 +89,6 @@ struct WorkOut {
   // b / splits, replicates [(b % splits) * bc, + bc), into a shared-memory
   // histogram of the row flushed once per block
   long long bc, splits;
-  // pole-major chunk order (walk_f32_kernel SMEM == 3): chunk c -> pole
-  // c / nbp, replicate block c % nbp (nbp = chunks per pole)
-  long long nbp;
-  double inv_nbp;
   unsigned long long *ssum, *ssq, *smax;
   // first failing walk as ~(pole * n_rep + rep) under atomicMax: a zero-filled
   // output block means "no failure" and the smallest key wins

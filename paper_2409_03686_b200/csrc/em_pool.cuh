@@ -101,10 +101,7 @@ __device__ __forceinline__ bool pool_take(WarpPool& wp, unsigned need_mask, cons
 // (the current chunk covers every idle lane) is straight-line predicated
 // code; only a chunk claim branches.  eq / lt are this lane's bit and the
 // bits below it, kept in registers by the caller.
-// PM (pole-major): chunk c -> (pole c / nbp, replicate block c % nbp), so the
-// warps in flight share a handful of rows (L2-resident even when all rows
-// are not) -- the persistent scheduler's order for long rows.
-template <class RepT, bool PM = false>
+template <class RepT>
 __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask, const WorkOut& W,
                                                int& pole, RepT& rep_off, unsigned eq, unsigned lt) {
   const int n_need = __popc(need_mask);
@@ -123,27 +120,14 @@ __device__ __forceinline__ bool pool_take_fast(WarpPool& wp, unsigned need_mask,
       if (c >= W.n_chunks) {
         wp.exhausted = 1;
       } else {
-        long long b, p;
-        if (PM) {
-          p = (long long)((double)c * W.inv_nbp);
-          b = (long long)c - p * W.nbp;
-          if (b < 0) {
-            p -= 1;
-            b += W.nbp;
-          } else if (b >= W.nbp) {
-            p += 1;
-            b -= W.nbp;
-          }
-        } else {
-          b = (long long)((double)c * W.inv_poles);
-          p = (long long)c - b * W.n_poles;
-          if (p < 0) {
-            b -= 1;
-            p += W.n_poles;
-          } else if (p >= W.n_poles) {
-            b += 1;
-            p -= W.n_poles;
-          }
+        long long b = (long long)((double)c * W.inv_poles);
+        long long p = (long long)c - b * W.n_poles;
+        if (p < 0) {
+          b -= 1;
+          p += W.n_poles;
+        } else if (p >= W.n_poles) {
+          b += 1;
+          p -= W.n_poles;
         }
         const long long r0 = b * W.rb;
         const int valid = (int)(W.n_rep - r0 < W.rb ? W.n_rep - r0 : W.rb);

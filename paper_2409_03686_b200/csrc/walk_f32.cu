@@ -281,6 +281,13 @@ __device__ __forceinline__ void dist(const F32Params& P, const float* x, float& 
 // (S/_kernel.pyx:145-156).
 template <int D, int OUTER, int NH>
 __device__ __forceinline__ int owner(const F32Params& P, const float* x) {
+  if (OUTER == OUTER_BALL && NH == 1 && P.concentric) {
+    // concentric shell: |R - r| <= |r - rho| (ties to the outer component)
+    // exactly when r >= (R + rho) / 2
+    float s2 = x[0] * x[0] + x[1] * x[1];
+    if (D == 3) s2 = fmaf(x[2], x[2], s2);
+    return s2 >= P.mid2 ? 0 : 1;
+  }
   float best;
   if (OUTER == OUTER_BALL) {
     const float v0 = x[0], v1 = x[1];
@@ -348,6 +355,30 @@ __device__ int brute(const Side32& S, const float* x, int start, int count) {
   return bi;
 }
 
+// Cell of one uniform circle block (count <= kBisMax) holding the offset
+// (dx, dy) from its centre.  The nearest of equally spaced anchors on a
+// circle is the one of nearest angle: a cheap angle (|error| < 8.2e-5 rad,
+// far below half a cell) picks a cell k, then exact side tests against its
+// two Voronoi boundary rays (cross products with bis[k], bis[k + 1]) move
+// it by at most one -- atan2f's work at about half its instructions.
+__device__ __forceinline__ int circle_cell(const float2* bis, int count, float scale, float phase,
+                                           float dx, float dy) {
+  const float ax = fabsf(dx), ay = fabsf(dy);
+  const float q = fdiv(fminf(ax, ay), fmaxf(ax, ay));
+  const float q2 = q * q;
+  float a = q * fmaf(q2, fmaf(q2, fmaf(q2, -0.03899375721812248f, 0.14627520740032196f),
+                              -0.3211793601512909f), 0.999214231967926f);
+  a = ay > ax ? 1.5707963267948966f - a : a;
+  a = dx < 0.0f ? kPi - a : a;
+  a = copysignf(a, dy);
+  const int k = wrapi((int)floorf(fmaf(a, scale, -phase) + 0.5f), count);
+  const int k1 = k + 1 == count ? 0 : k + 1;
+  const float2 bl = __ldg(&bis[k]), bh = __ldg(&bis[k1]);
+  const float cl = fmaf(bl.x, dy, -bl.y * dx);  // < 0: clockwise of the cell's lower ray
+  const float ch = fmaf(bh.x, dy, -bh.y * dx);  // > 0: counter-clockwise of its upper ray
+  return cl < 0.0f ? (k == 0 ? count - 1 : k - 1) : (ch > 0.0f ? k1 : k);
+}
+
 // Nearest anchor (family-local index) of one side's family.
 template <int D>
 __device__ int nearest_anchor(const Side32& S, const float* x) {
@@ -380,7 +411,10 @@ __device__ int nearest_anchor(const Side32& S, const float* x) {
   for (int b = 0; b < S.n_blk; ++b) {
     int idx;
     const int count = S.count[b];
-    if (S.kind[b] == BLK_CIRCLE) {
+    if (S.kind[b] == BLK_CIRCLE && S.n_blk == 1 && S.bis) {
+      idx = S.start[b] + circle_cell(S.bis, count, S.scale[b], S.phase[b], x[0] - S.cx[b],
+                                     x[1] - S.cy[b]);
+    } else if (S.kind[b] == BLK_CIRCLE) {
       const float ang = atan2f(x[1] - S.cy[b], x[0] - S.cx[b]);
       const float t = fmaf(ang, S.scale[b], -S.phase[b]);
       idx = S.start[b] + wrapi((int)floorf(t + 0.5f), count);
@@ -427,11 +461,17 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
   const Side32& S0 = P.side[0];
   const Side32& S1 = P.side[1];
   if (BINK == BIN_CIRCLE) {
-    const float ang = atan2f(x[1] - pick(side, S0.cy[0], S1.cy[0]),
-                             x[0] - pick(side, S0.cx[0], S1.cx[0]));
+    const float dx = x[0] - pick(side, S0.cx[0], S1.cx[0]);
+    const float dy = x[1] - pick(side, S0.cy[0], S1.cy[0]);
+    const float2* bis = pick(side, S0.bis, S1.bis);
+    const int count = pick(side, S0.count[0], S1.count[0]);
+    if (bis)
+      return circle_cell(bis, count, pick(side, S0.scale[0], S1.scale[0]),
+                         pick(side, S0.phase[0], S1.phase[0]), dx, dy);
+    const float ang = atan2f(dy, dx);
     const float t = fmaf(ang, pick(side, S0.scale[0], S1.scale[0]),
                          -pick(side, S0.phase[0], S1.phase[0]));
-    return wrapi((int)floorf(t + 0.5f), pick(side, S0.count[0], S1.count[0]));
+    return wrapi((int)floorf(t + 0.5f), count);
   } else if (BINK == BIN_SQUARE) {
     const float h = pick(side, S0.radius[0], S1.radius[0]);
     const float px = x[0] - pick(side, S0.cx[0], S1.cx[0]);
@@ -1030,17 +1070,7 @@ __device__ __forceinline__ void retire(const F32Params& P, const float* x, int p
     acc.mx = (unsigned long long)steps > acc.mx ? (unsigned long long)steps : acc.mx;
     return;
   }
-  unsigned long long* cell = &W.counts[(long long)pole * W.row_len + col];
-  if (SMEM == 3 && FULL) {
-    // pole-major chunks: the 32 exits of a binning pass mostly share a row,
-    // and near-pole bins are hot -- one RED per distinct address, adding the
-    // group's count (__match_any_sync over the 64-bit address)
-    const unsigned peers = __match_any_sync(kFull, (unsigned long long)cell);
-    if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u)
-      atomicAdd(cell, (unsigned long long)__popc(peers));
-  } else {
-    atomicAdd(cell, 1ULL);
-  }
+  atomicAdd(&W.counts[(long long)pole * W.row_len + col], 1ULL);
   acc_add<SMEM>(acc, W, pole, (unsigned long long)steps);
 }
 
@@ -1225,7 +1255,7 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
           }
         }
       } else {
-        took = pool_take_fast<int, SMEM == 3>(wp, need, W, pole, rep_off, eq, lt);
+        took = pool_take_fast(wp, need, W, pole, rep_off, eq, lt);
       }
       if (took) {
         EM_DEV_ASSERT(pole >= 0 && pole < W.n_poles && rep_off >= 0 && rep_off < W.n_rep);
@@ -1531,8 +1561,7 @@ using F32Kernel = void (*)(F32Params);
 // shared-memory histogram per block (capi.cu picks it for long rows; only
 // the closed-form / grid binners are instantiated with it)
 #define EM_SCHED3(ARGS, BK)                                                          \
-  (smem == 3 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 3> :                            \
-   smem == 2 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 2>                              \
+  (smem == 2 ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 2>                              \
              : (smem ? walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 1>                      \
                      : walk_f32_kernel<EM_UNPAREN ARGS, 0, BK, 0>))
 #define EM_UNPAREN(...) __VA_ARGS__
@@ -1552,7 +1581,7 @@ static F32Kernel pick_chain_sm(int mode, int chain, bool ident) {
 
 template <int D, int OUTER, int NH, int BINK>
 static F32Kernel pick_chain(int mode, int chain, bool ident, int smem) {
-  if (smem >= 2) return nullptr;  // pole-block / pole-major schedulers: tangent chains only
+  if (smem >= 2) return nullptr;  // the pole-block scheduler: tangent chains only
   return smem ? pick_chain_sm<D, OUTER, NH, BINK, 1>(mode, chain, ident)
               : pick_chain_sm<D, OUTER, NH, BINK, 0>(mode, chain, ident);
 }
@@ -1668,7 +1697,7 @@ cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mo
   return cudaGetLastError();
 }
 
-// the pole-block / pole-major schedulers exist for this plan's kernel family
+// the pole-block scheduler exists for this plan's kernel family
 bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink) {
   return pick_f32(d, outer, nh_mode, 0, chain, ident, bink, 2) != nullptr;
 }

@@ -292,18 +292,21 @@ def test_ref64_idw_bit_identical(B, golden_idw, name):
     assert np.array_equal(r.steps_sum, c["rsteps"]) and r.idw_fallbacks == int(c["rfb"])
 
 
-@pytest.mark.parametrize("idx", [4, 5])
+@pytest.mark.parametrize("idx", [1, 3, 4, 5])
 def test_fp32_grid_binning_equals_exact(B, idx):
-    """The FP32 candidate-grid binner assigns real FP32 exit points to the
-    same anchors as the exact lexicographic brute-force rule (REF64)."""
+    """The FP32 binners -- the candidate grid (cfg4, cfg5) and the circle
+    cells by cheap angle + exact boundary-ray tests (cfg1, cfg3: both
+    circles of the annulus, exits from both rings of poles) -- assign real
+    FP32 exit points to the same anchors as the exact lexicographic
+    brute-force rule (REF64)."""
     from paper_2409_03686_b200 import configs
 
     cfg = configs.get(idx).subset(4)
     geom = B.pack_geometry(cfg.dom)
-    s0 = B.pack_side(cfg.fam0, 3, cfg.eps)
-    s1 = B.pack_side(cfg.fam1, 3, cfg.eps)
-    x, _, _ = B.run_exits(cfg.dom, cfg.kt.k_sqrt, cfg.poles[1], 1, cfg.seed, cfg.eps, 10**6,
-                          100_000, precision="fp32")
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    x = np.concatenate([B.run_exits(cfg.dom, cfg.kt.k_sqrt, cfg.poles[i], i, cfg.seed, cfg.eps,
+                                    10**6, 100_000, precision="fp32")[0] for i in (1, 3)])
     bins = {}
     for prec in ("fp32", "ref64"):
         with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles[:1], cfg.eps, 10**6, s0, s1,
