@@ -281,6 +281,15 @@ int em_run_exits(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
 int em_debug_step(em_plan* p, const double* x, const uint32_t* words, int64_t n, double* y,
                   float* mask);
 
+/* Host unit-test hook (no device needed): one named closed-form constant of
+ * the FP32 kernel for geometry g on chain `chain` (the chain the plan runs)
+ * with K = I flag `ident`, as em_plan_create computes it -- e.g. "t3" (the
+ * 3 x 24 per-face tables of the tangent chain on 3D boxes), "tbt", "rho_b",
+ * "rho_h", "mid2", "Ad", "Q", "shk", "sb", "g", "m2", "stop_scale".  Returns
+ * the number of floats written, -1 for an unknown name. */
+int em_f32_constant(const em_geometry* g, int chain, int ident, double eps, const char* name,
+                    float* out, int n);
+
 /* Micro-benchmark used for the roofline denominator: achieved FP32 FFMA
  * lane-ops/s of an issue-bound kernel on `device` (its own CUDA events). */
 int em_fp32_peak(int device, double* flops_per_s, double* ms);

@@ -122,6 +122,8 @@ def lib():
                             ctypes.c_int),
         "em_bin_points": ([_p, _p, _i64, _p, _p, _p], ctypes.c_int),
         "em_debug_step": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
+        "em_f32_constant": ([ctypes.POINTER(EmGeometry), ctypes.c_int, ctypes.c_int, _dbl,
+                             ctypes.c_char_p, _p, ctypes.c_int], ctypes.c_int),
         "em_fp32_peak": ([ctypes.c_int, _p, _p], ctypes.c_int),
         "em_philox4x64_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "em_philox4x32_blocks": ([_p, _p, ctypes.c_int, ctypes.c_int], ctypes.c_int),

@@ -85,6 +85,21 @@ def resolve_chain(geom: "GeomPack", ksqrt, precision: str | None = None,
     return _CHAIN_NAMES[rc]
 
 
+def f32_constant(geom: "GeomPack", ksqrt, chain: str, eps: float, name: str,
+                 ident: bool = False) -> np.ndarray:
+    """One closed-form constant of the FP32 kernel for this geometry and
+    (resolved) chain, as em_plan_create computes it -- host only, no device
+    (em_f32_constant; the host unit tests of the plan constants)."""
+    m = _Marshal()
+    g = m.geometry(geom.gi, geom.gf, geom.comp_side, ksqrt)
+    out = np.zeros(128, dtype=np.float32)
+    k = N.lib().em_f32_constant(ctypes.byref(g), _CHAINS[chain], int(ident), float(eps),
+                                name.encode(), N.ptr(out), out.size)
+    if k < 0:
+        raise ValidationError(f"unknown FP32 constant {name!r}")
+    return out[:k].copy()
+
+
 def default_device() -> int:
     return int(os.environ.get("EXITMEASURE_B200_DEVICE", "0"))
 

@@ -53,6 +53,7 @@ def units(debug: bool = False):
         ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false"]
          + [f"-D{k}={v}" for k, v in knobs().items()] + dbg),
         ("capi.cu", dbg),
+        ("plan_f32.cu", dbg),
         ("kat_curand.cu", dbg),
     ]
 
