@@ -43,21 +43,22 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 # Algorithmic FP32 lane-ops per walk step of the IMPLEMENTED chain, counted
-# with SURVEY.md §8(d)'s convention (add/sub/mul/fma/min/max/compare = 1;
-# sqrt/rsqrt/div/sin/cos are XU ops, counted separately; RNG separately).
-# Derivation per term is in DESIGN.md ("F_step of the implemented kernels").
+# with SURVEY.md §8(d)'s convention: add/sub/mul/fma/min/max/compare = 1 on
+# the path a step takes -- no selects, and exclusive branch arms weighted by
+# how often a step takes them (cfg3: the centred disk on 17.7% of steps,
+# cfg4: the centred ball on 25.4%, from the chains' float64 restatements);
+# sqrt/rsqrt/rcp/sin/cos are XU ops, counted apart; RNG and per-walk
+# bookkeeping excluded.  Term by term in DESIGN.md §3.3.
 F_STEP = {
-    # (cfg, chain): (fp32 ops, xu ops) -- DESIGN.md "F_step of the implemented
-    # kernels" derives each entry term by term from walk_f32.cu
     (1, "woe"): (11, 3), (1, "max"): (11, 3),   # K = I: both chains are the sphere step
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
-    (2, "tangent"): (44, 3),                     # tangent balls: ~4x fewer, costlier steps
-    (3, "woe"): (19, 4), (3, "max"): (31, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
-    (3, "tangent"): (91, 9),                     # rolling disks + disks tangent to the hole
+    (2, "tangent"): (37, 3),                     # tangent balls in the whitened parallelogram
+    (3, "woe"): (19, 4), (3, "max"): (29, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
+    (3, "tangent"): (55.6, 6.35),                # one rolling / hole-tangent disk, else centred
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
-    (4, "tangent"): (93, 10),                    # rolling balls (max-chain ball off the near side)
+    (4, "tangent"): (79.3, 8.25),                # rolling balls, else the centred ball
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
-    (5, "tangent"): (101, 5),                    # tangent balls in 3D, notch planes as faces
+    (5, "tangent"): (87, 5),                     # tangent balls in 3D, notch planes as faces
 }
 
 # the reference chain's FP32 ops per step (same counting

@@ -207,3 +207,26 @@ def test_fp32_rolling_chain_pole_at_the_centre(B, d):
     half = r.counts.shape[1] // 2
     lower = r.counts[0, half:].sum() / n
     assert abs(lower - 0.5) < 0.01, lower
+
+
+def test_family_check_under_device_asserts():
+    """tools/family_check.py (every walk-kernel family: exact rows, finite
+    exits, in-range bins) on the EM_DEBUG build, whose device bounds asserts
+    trap on any out-of-range count-row write or work hand-out."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    if not (root / "paper_2409_03686_b200" / "lib" / "libexitmeasure_b200_debug.so").exists():
+        pytest.skip("debug library not built")
+    env = dict(os.environ, EXITMEASURE_B200_DEBUG="1", EXITMEASURE_B200_AUTOBUILD="0")
+    code = ("import runpy, sys; sys.path.insert(0, %r); "
+            "from paper_2409_03686_b200 import _native; "
+            "assert _native.build_info()['debug'] == '1'; "
+            "runpy.run_path(%r, run_name='__main__')") % (str(root), str(root / "tools" / "family_check.py"))
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "family_check ok" in res.stdout

@@ -120,3 +120,40 @@ def test_reference_driver_threads_over_the_chunk_dropin(ref):
         assert np.array_equal(getattr(cpu, name), getattr(gpu, name)), name
     for a, b in zip(x_cpu, x_gpu):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.slow
+def test_five_disc_anchor_through_the_cli(ref, tmp_path):
+    """The paper's published accuracy anchor (R/PAPER.md:202-203; acceptance
+    C03, T/test_acceptance.py:135-152): the averaged inaccessible exit mass of
+    the five-disc geometry ex5_4 over its 100 poles at 1e5 walks per pole,
+    read back from the reference CLI's summary.json.  The reference itself
+    (compiled Cython kernel) gives 0.1125; REF64 through plugin.install()
+    must reproduce its value EXACTLY, FP32 within 4 standard errors of the
+    difference of two independent estimates."""
+    import json
+
+    from exitmeasure.cli import RunConfig, run
+
+    from paper_2409_03686_b200 import plugin
+
+    def avg(label):
+        out = tmp_path / label
+        run(RunConfig(example="ex5_4", solution="sol2d_3", n=10**5, seed=314, r="1:6",
+                      out=str(out)))
+        s = json.loads((out / "summary.json").read_text())["replicates"][0]
+        return float(s["mu_gamma1_avg"])
+
+    mu_ref = avg("reference")
+    assert round(mu_ref, 4) == 0.1125
+    out = {}
+    for prec in ("ref64", "fp32"):
+        try:
+            plugin.install(precision=prec, module=ref)
+            out[prec] = avg(prec)
+        finally:
+            plugin.uninstall(ref)
+    assert out["ref64"] == mu_ref
+    # SE of a 100-pole average of binomial fractions near 0.11 at 1e5 walks
+    se = np.sqrt(mu_ref * (1 - mu_ref) / 10**5 / 100)
+    assert abs(out["fp32"] - mu_ref) <= 4 * np.sqrt(2) * se, (out, mu_ref, se)
