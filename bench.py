@@ -282,7 +282,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "walks/s", "value": wps, "unit": "walks/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "steps_per_s": sps, "mean_steps_per_walk": info[4],
         "config": {"workload": workload_name(cfg), "precision": "fp64 (the reference chain)",
                    "sample_per_step": f"{cfg.n_poles} poles x {n_sample} walks",
@@ -305,7 +305,7 @@ def _nccl_lines():
     out = []
     for f in sorted(glob.glob(os.environ.get("EM_NCCL_LOG_GLOB", "/nonexistent"))):
         for line in open(f, errors="replace"):
-            if re.search(r"nranks \d+", line) and "Init COMPLETE" in line:
+            if re.search(r"nranks \d+", line, re.I) and re.search(r"init complete", line, re.I):
                 out.append(line.strip())
     return out
 

@@ -512,6 +512,17 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
   if (o.precision != EM_PREC_REF64 && (s0->wkind == 1 || s1->wkind == 1))
     return fail(EM_ERR_UNSUPPORTED, "IDW weight families run on the REF64 path only");
+  if (o.precision == EM_PREC_FP32) {
+    // the FP32 kernel's step margins are a few ulps of the domain scale; a
+    // shell thinner than 2^-20 x scale (8 ulps) cannot be reached by steps
+    // that keep those margins (the walks would stall at the budget): such
+    // runs need the FP64 mirror
+    const double dscale = std::max(1.0, std::fabs(g->gf[d]));
+    if (eps < std::ldexp(dscale, -20))
+      return fail(EM_ERR_UNSUPPORTED, "eps " + std::to_string(eps) +
+                                          " is below the FP32 kernel's resolution (2^-20 x the "
+                                          "domain scale): use precision ref64");
+  }
   if (o.precision == EM_PREC_FP32 && o.block > 0 && o.block != 256)
     return fail(EM_ERR_UNSUPPORTED, "the FP32 kernel runs 256-thread blocks");
   int ndev = em_device_count();

@@ -230,3 +230,21 @@ def test_family_check_under_device_asserts():
                          timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "family_check ok" in res.stdout
+
+
+def test_fp32_rejects_shells_below_its_resolution(B):
+    """eps below 2^-20 x the domain scale cannot be reached by FP32 steps that
+    keep their rounding margins: the plan refuses it (EM_ERR_UNSUPPORTED)
+    instead of stalling every walk at the budget; REF64 runs it."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.errors import NativeError
+
+    cfg = configs.get(1).subset(2, 100)
+    s0 = B.pack_side(cfg.fam0, 2, 1e-10)
+    s1 = B.pack_side(cfg.fam1, 2, 1e-10)
+    with pytest.raises(NativeError, match="ref64"):
+        B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, 1, 1e-10, 10**6, 100, s0, s1,
+                         precision="fp32")
+    r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, 1, 1e-10, 10**6, 100, s0, s1,
+                         precision="ref64")
+    assert np.array_equal(r.counts.sum(1), np.full(2, 100))

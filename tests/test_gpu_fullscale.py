@@ -212,6 +212,7 @@ def test_cfg2_leading_singular_values(cfg2_estimates):
     pf = 2 * np.minimum(stats.f.cdf(f, len(sg) - 1, len(sr) - 1),
                         stats.f.sf(f, len(sg) - 1, len(sr) - 1))
     summary["variance_ratio_p"] = pf.tolist()
+    (ROOT / "gpurun_out" / "fullscale_cfg2_sigma.json").write_text(json.dumps(summary, indent=1))
     assert np.all(pf > 1e-3 / 8), summary
     assert np.all(rel <= 2e-3), summary
 

@@ -137,20 +137,23 @@ def test_five_disc_anchor_through_the_cli(ref, tmp_path):
 
     from paper_2409_03686_b200 import plugin
 
-    def avg(label):
+    def avg(label, eps=None):
         out = tmp_path / label
         run(RunConfig(example="ex5_4", solution="sol2d_3", n=10**5, seed=314, r="1:6",
-                      out=str(out)))
+                      out=str(out), eps=eps))
         s = json.loads((out / "summary.json").read_text())["replicates"][0]
         return float(s["mu_gamma1_avg"])
 
     mu_ref = avg("reference")
     assert round(mu_ref, 4) == 0.1125
     out = {}
-    for prec in ("ref64", "fp32"):
+    # ex5_4 runs at eps = 1e-10, below the FP32 kernel's resolution (it
+    # refuses such shells); the FP32 arm runs eps = 1e-6, whose eps-shell
+    # shift of the exit law (order eps) is ~1e-2 standard errors here
+    for prec, eps in (("ref64", None), ("fp32", 1e-6)):
         try:
             plugin.install(precision=prec, module=ref)
-            out[prec] = avg(prec)
+            out[prec] = avg(prec, eps)
         finally:
             plugin.uninstall(ref)
     assert out["ref64"] == mu_ref

@@ -39,7 +39,7 @@ def test_reference_suite_passes_on_gpu_backend(tmp_path):
                PYTHONPATH=os.pathsep.join([str(ROOT / "tests" / "refsuite"), str(REF),
                                            str(ROOT)]))
     env.pop("EXITMEASURE_BACKEND", None)
-    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-rfE"] + SUITE
+    cmd = [sys.executable, "-m", "pytest", "-q", "-s", "-p", "no:cacheprovider", "-rfE"] + SUITE
     res = subprocess.run(cmd, cwd=REF / "ref_tests", env=env, capture_output=True, text=True,
                          timeout=1800)
     out = res.stdout + res.stderr
