@@ -213,7 +213,7 @@ CPU_SAMPLE = {1: 10_000, 2: 163_840, 3: 32_768, 4: 16_384, 5: 1024}
 # committed ncu captures of the walk kernel per (config, chain): key metrics
 # in "metric,value,unit" rows (tools/ncu_metrics.py from the raw page of one
 # `ncu --set full` capture of `bench.py --config C`)
-PROFILES = {(2, "tangent"): "profiles/r01_cfg2_walk_f32_ncu_raw.csv",
+PROFILES = {(2, "tangent"): "profiles/r02_cfg2_walk_f32_ncu_metrics.csv",
             (3, "tangent"): "profiles/r02_cfg3_walk_f32_ncu_metrics.csv",
             (4, "tangent"): "profiles/r02_cfg4_walk_f32_ncu_metrics.csv",
             (5, "tangent"): "profiles/r02_cfg5_walk_f32_ncu_metrics.csv"}
