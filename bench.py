@@ -364,9 +364,7 @@ def run_ours(args):
     gathered = full = perm = None
     if world > 1 and not weak:
         gathered = torch.zeros((world, blk_len), dtype=torch.int64, device="cuda")
-        # global pole g lives in rank g % N's block at row g // N
-        g = torch.arange(cfg.n_poles, device="cuda")
-        perm = (g % world) * m_pad + g // world
+        perm = distributed.cyclic_gather_index(cfg.n_poles, world, m_pad, device="cuda")
         full = torch.zeros((cfg.n_poles, row), dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -375,9 +373,7 @@ def run_ours(args):
         plan.run_device(cfg.seed, cfg.n_rep, counts.data_ptr(), stats.data_ptr(),
                         stream.cuda_stream, rep_start)
         if gathered is not None:
-            dist.all_gather_into_tensor(gathered.view(-1), buf)
-            rows = gathered[:, : m_pad * row].reshape(world * m_pad, row)
-            torch.index_select(rows, 0, perm, out=full)
+            distributed.exchange_rows(buf, gathered, perm, m_pad, row, full)
 
     for _ in range(args.warmup):
         flush.zero_()

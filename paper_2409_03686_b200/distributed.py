@@ -44,6 +44,29 @@ def gather_rows(local, n_poles: int, world: int, group=None):
     return out
 
 
+def cyclic_gather_index(n_poles: int, world: int, m_pad: int, device=None):
+    """Row index into the rank-major all-gather of per-rank blocks of m_pad
+    rows: global pole g lives in rank g % world's block at row g // world."""
+    import torch
+
+    g = torch.arange(n_poles, device=device)
+    return (g % world) * m_pad + g // world
+
+
+def exchange_rows(buf, gathered, index, m_pad: int, row: int, out, group=None) -> None:
+    """The one exchange of a strong-scaling step: ONE all-gather of every
+    rank's flat block (count rows (m_pad, row) first), then the un-permute of
+    the gathered rows into pole order (``out``, (n_poles, row)) on the
+    device.  ``gathered`` is (world, len(buf)), ``index`` from
+    cyclic_gather_index."""
+    import torch
+    import torch.distributed as dist
+
+    dist.all_gather_into_tensor(gathered.view(-1), buf, group=group)
+    rows = gathered[:, : m_pad * row].reshape(gathered.shape[0] * m_pad, row)
+    torch.index_select(rows, 0, index, out=out)
+
+
 _NO_ERROR = np.iinfo(np.int64).max
 
 

@@ -248,3 +248,44 @@ def test_fp32_rejects_shells_below_its_resolution(B):
     r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, 1, 1e-10, 10**6, 100, s0, s1,
                          precision="ref64")
     assert np.array_equal(r.counts.sum(1), np.full(2, 100))
+
+
+def test_idw_family_refused_on_integer_rows(B):
+    """An IDW weight family has fractional rows: the integer-count entry
+    points refuse it (EM_ERR_UNSUPPORTED / ValidationError) instead of
+    silently binning to the nearest anchor; run_raw serves it."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.errors import NativeError, ValidationError
+
+    cfg = configs.get(3).subset(2, 64)
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, 2, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 2, cfg.eps, "idw", np.full(cfg.fam1.points.shape[0], 0.3), 2)
+    import torch
+
+    with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, 10**6, s0, s1,
+                precision="ref64") as plan:
+        counts = torch.zeros((2, plan.n0 + plan.n1), dtype=torch.int64, device="cuda")
+        stats = torch.zeros((3, 2), dtype=torch.int64, device="cuda")
+        with pytest.raises(ValidationError):
+            plan.run_device(1, 64, counts.data_ptr(), stats.data_ptr())
+        r = plan.run(1, 64)  # routes to run_raw
+        assert np.allclose(r.raw0.sum(1) + r.raw1.sum(1), 64)
+    # the C ABI's integer entry point refuses it outright
+    from paper_2409_03686_b200 import _native as N
+
+    m = B._Marshal()
+    g = m.geometry(geom.gi, geom.gf, geom.comp_side, cfg.kt.k_sqrt)
+    ms0, ms1 = m.sidepack(s0), m.sidepack(s1)
+    out = N.EmOutputs(*[m.arr(np.zeros(n, np.int64), np.int64).ctypes.data
+                        for n in (2 * (s0.size + s1.size), 2, 2, 2)], -1, -1)
+    import ctypes
+
+    opt = N.EmOptions(N.EM_PREC_REF64, N.EM_CHAIN_WOE, 0, 0, 0, 0)
+    pl = m.arr(cfg.poles, np.float64)
+    rc = N.lib().em_run_accumulate(ctypes.byref(g), ctypes.byref(ms0), ctypes.byref(ms1),
+                                   N.ptr(pl), None, 2, 1, cfg.eps, 10**6, 64,
+                                   ctypes.byref(opt), ctypes.byref(out))
+    assert rc == N.EM_ERR_UNSUPPORTED, rc
+    with pytest.raises(NativeError):
+        N.check(rc, "em_run_accumulate")

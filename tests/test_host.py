@@ -366,3 +366,41 @@ def test_bench_rejects_world_mismatch():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4"],
                          capture_output=True, text=True, env=env, timeout=600)
     assert res.returncode == 2 and "WORLD_SIZE" in res.stderr
+
+
+_EXCHANGE_WORKER = textwrap.dedent("""
+    import sys
+    import torch, torch.distributed as dist
+    sys.path.insert(0, sys.argv[1])
+    from paper_2409_03686_b200.distributed import cyclic_gather_index, exchange_rows, shard_rows
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    for n_poles, row in ((7, 5), (8, 3), (1, 4)):
+        ids = shard_rows(n_poles, world, rank)
+        m_pad = -(-n_poles // world)
+        buf = torch.full((m_pad * row + 3 * m_pad,), -1, dtype=torch.int64)
+        rows = buf[: m_pad * row].view(m_pad, row)
+        for j, g in enumerate(ids):  # this rank's rows hold their GLOBAL pole id
+            rows[j] = torch.arange(row) + 1000 * int(g)
+        gathered = torch.zeros((world, buf.numel()), dtype=torch.int64)
+        out = torch.zeros((n_poles, row), dtype=torch.int64)
+        exchange_rows(buf, gathered, cyclic_gather_index(n_poles, world, m_pad), m_pad, row, out)
+        want = torch.arange(row)[None, :] + 1000 * torch.arange(n_poles)[:, None]
+        assert torch.equal(out, want), (rank, n_poles, out)
+    dist.barrier(); dist.destroy_process_group()
+    print("rank", rank, "ok")
+""")
+
+
+def test_strong_scaling_exchange_gloo_two_ranks(tmp_path):
+    """The bench's per-step exchange (one all-gather of the flat blocks, the
+    un-permute to pole order) reassembles cyclic row shards -- ragged shards
+    and an empty shard included -- on 2 gloo ranks."""
+    w = tmp_path / "worker.py"
+    w.write_text(_EXCHANGE_WORKER)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29581", str(w), str(ROOT)]
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
+    assert res.stdout.count("ok") == 2
