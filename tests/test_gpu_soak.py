@@ -1,5 +1,5 @@
 """High-power parity of the production FP32 tangent / rolling chains
-(formerly tools/soak_tangent.py, now in the suite): per config, 1e7 GPU walks
+(formerly tools/diag/soak_tangent.py, now in the suite): per config, 1e7 GPU walks
 per pole against 2e5 .. 2e6 walks per pole of the C oracle (the reference's
 FP64 walk-on-ellipsoids chain, S/_kernel.pyx:163-197, brute-force Voronoi
 binning, all host threads).  Two statistics per config: the per-pole
