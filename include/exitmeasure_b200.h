@@ -114,7 +114,7 @@ typedef struct {
   const int64_t* blk;
   const double* blkf;
   int64_t n_blk;
-  int32_t wkind; /* 0 voronoi, 1 idw (REF64 only, via em_plan_run_raw) */
+  int32_t wkind; /* 0 voronoi, 1 idw (fractional rows via em_plan_run_raw) */
   int32_t idw_power;
   const double* idw_radii;
   const double* blk_phase;
@@ -238,8 +238,10 @@ int em_plan_chain(const em_plan* p);
  * step exists; negative EM_ERR_* for an invalid geometry or pair */
 int em_resolve_chain(const em_geometry* g, int precision, int chain);
 
-/* Fractional rows (REF64 only; required for IDW weight families, valid for
- * Voronoi too): raw0 (n_poles, n0) and raw1 (n_poles, n1) doubles.  With
+/* Fractional rows (required for IDW weight families; on REF64 valid for
+ * Voronoi too): raw0 (n_poles, n0) and raw1 (n_poles, n1) doubles.  On an
+ * FP32 plan the walks are the FP32 kernel's and the IDW weights (FP64,
+ * S/_kernel.pyx:323-369) are summed over its exits in the same fixed order.  With
  * init0/init1 the sums continue in place from those values in replicate
  * order (the chunk contract, S/_kernel.pyx:451-461); without, every `chunk`
  * replicates (8192 in the reference driver) start a zeroed partial that is

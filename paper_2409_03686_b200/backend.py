@@ -343,8 +343,6 @@ class Plan:
         if chain not in _CHAINS:
             raise ValidationError(f"unknown chain {chain!r}")
         self.idw = _has_idw(side0, side1)
-        if self.idw and _PRECISIONS[precision] != N.EM_PREC_REF64:
-            raise ValidationError("IDW weight families run on the bit-exact REF64 path only")
         self.device = default_device() if device is None else int(device)
         N.require_device(self.device)
         self.precision, self.chain = precision, chain
@@ -400,8 +398,9 @@ class Plan:
 
     def run_raw(self, seed: int, n_rep: int, rep_start: int = 0,
                 chunk: int = CHUNK) -> AccumulateResult:
-        """Fractional rows (IDW families; REF64), summed with the reference
-        driver's per-CHUNK partials in job order -- bit-identical rows."""
+        """Fractional rows (IDW families), summed with the reference driver's
+        per-CHUNK partials in job order -- bit-identical rows on REF64; on
+        FP32 the same fixed-order FP64 weights over the FP32 kernel's exits."""
         raw0 = np.zeros((self.n_poles, self.n0))
         raw1 = np.zeros((self.n_poles, self.n1))
         stats = np.zeros((3, self.n_poles), dtype=np.int64)

@@ -510,8 +510,6 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     return fail(EM_ERR_INVALID, "unknown chain");
   if (o.precision == EM_PREC_REF64 && o.chain != EM_CHAIN_WOE)
     return fail(EM_ERR_INVALID, "the REF64 mirror runs the reference chain only");
-  if (o.precision != EM_PREC_REF64 && (s0->wkind == 1 || s1->wkind == 1))
-    return fail(EM_ERR_UNSUPPORTED, "IDW weight families run on the REF64 path only");
   if (o.precision == EM_PREC_FP32) {
     // the FP32 kernel's step margins are a few ulps of the domain scale; a
     // shell thinner than 2^-20 x scale (8 ulps) cannot be reached by steps
@@ -601,19 +599,11 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
   w.stat_copies = 1;
 
   const em_side* sides[2] = {s0, s1};
-  if (p->precision == EM_PREC_REF64) {
-    Ref64Params& P = p->p64;
+  // the FP64 side tables (exact binning, IDW weights): the REF64 mirror's,
+  // and the FP32 path's IDW post-processing of its exits
+  auto fill_sides64 = [&](Ref64Params& P) {
     P.d = d;
-    P.outer_kind = (int)g->gi[1];
-    P.n_holes = nh;
-    P.n_notch = nn;
-    const int64_t ngf = (d + 1) * (1 + nh) + 2 * nn;
-    for (int64_t i = 0; i < ngf; ++i) P.gf[i] = g->gf[i];
     for (int c = 0; c < 1 + nh + nn; ++c) P.comp_side[c] = g->comp_side[c];
-    for (int i = 0; i < d * d; ++i) P.ks[i] = g->ksqrt[i];
-    P.eps = eps;
-    P.max_steps = max_steps;
-    put(poles, (size_t)n_poles * d * 8, (void**)&P.poles);
     for (int s = 0; s < 2; ++s) {
       const em_side* S = sides[s];
       Side64& D = P.side[s];
@@ -635,9 +625,26 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         put(S->idw_radii, (size_t)S->n_anchors * 8, (void**)&p->radii_dev[s]);
       if (S->n_anchors > 0) put(S->anchors, (size_t)S->n_anchors * d * 8, (void**)&D.anchors);
     }
+  };
+  if (p->precision == EM_PREC_REF64) {
+    Ref64Params& P = p->p64;
+    fill_sides64(P);
+    P.d = d;
+    P.outer_kind = (int)g->gi[1];
+    P.n_holes = nh;
+    P.n_notch = nn;
+    const int64_t ngf = (d + 1) * (1 + nh) + 2 * nn;
+    for (int64_t i = 0; i < ngf; ++i) P.gf[i] = g->gf[i];
+    for (int i = 0; i < d * d; ++i) P.ks[i] = g->ksqrt[i];
+    P.eps = eps;
+    P.max_steps = max_steps;
+    put(poles, (size_t)n_poles * d * 8, (void**)&P.poles);
     P.w = w;
   } else {
     F32Params& P = p->p32;
+    // IDW families: FP32 walks, the FP64 weights of S/_kernel.pyx:323-369 in
+    // a fixed (replicate) order on their exits (em_plan_run_raw)
+    if (s0->wkind == 1 || s1->wkind == 1) fill_sides64(p->p64);
     // every closed-form constant of the kernel (plan_f32.cu)
     void* fb = f32_build_new(g, p->chain, ident, eps, max_steps, P);
     struct FbFree {
@@ -1134,7 +1141,8 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                     const double* init0, const double* init1, double* raw0, double* raw1,
                     int64_t* stats, int64_t* idw_fallbacks, int64_t* err_pole, int64_t* err_rep) {
   if (!p || !raw0 || !raw1 || !stats) return fail(EM_ERR_INVALID, "null");
-  if (p->precision != EM_PREC_REF64) return fail(EM_ERR_UNSUPPORTED, "raw rows need REF64");
+  if (p->precision == EM_PREC_FP32 && !p->wkind[0] && !p->wkind[1])
+    return fail(EM_ERR_UNSUPPORTED, "FP32 raw rows are for IDW families (Voronoi: em_plan_run)");
   if (n_rep < 0 || rep_start < 0) return fail(EM_ERR_INVALID, "negative replicate range");
   DeviceGuard dg(p->device);
   const int64_t total = p->n_poles * n_rep;
@@ -1148,7 +1156,7 @@ int em_plan_run_raw(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
       (ce = p->iraw0.alloc((size_t)std::max<int64_t>(p->n_poles * p->n0, 1) * 8)) != cudaSuccess ||
       (ce = p->iraw1.alloc((size_t)std::max<int64_t>(p->n_poles * p->n1, 1) * 8)) != cudaSuccess)
     return fail(EM_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
-  WorkOut* w = &p->p64.w;
+  WorkOut* w = p->precision == EM_PREC_REF64 ? &p->p64.w : &p->p32.w;
   w->x_out = p->xo.as<double>();
   w->steps_out = p->so.as<long long>();
   w->comp_out = p->co.as<long long>();

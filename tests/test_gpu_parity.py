@@ -531,3 +531,38 @@ def test_fp32_rolling_disk_without_hole_matches_max_chain(B):
     pv = np.array([stats.chi2_contingency(np.vstack([ga[i], gb[i]]))[1] for i in range(len(a))])
     assert pv.min() > 1e-4 / len(pv), pv
     assert stats.combine_pvalues(pv)[1] > 1e-4, pv
+
+
+@pytest.mark.parametrize("name", ["annulus", "square_hole"])
+def test_fp32_idw_matches_ref64_statistically(B, golden_idw, name):
+    """FP32 IDW families: the FP32 kernel's exits with the
+    reference's FP64 inverse-distance weights (S/_kernel.pyx:323-369) summed
+    in fixed replicate order.  Against the bit-exact REF64 IDW rows: every
+    row sums to its walk count (each walk's weights are normalised), and
+    every entry's mean over 8 batches of 2e4 walks agrees with REF64's by a
+    pooled two-sample t-test at family-wise level 1e-3 (the golden cases'
+    geometry and IDW radii/powers, eps raised to 1e-5 for both arms: the
+    cases' own 1e-9 / 1e-7 are below the FP32 kernel's resolution)."""
+    from scipy import stats
+
+    c = case(golden_idw, "idw_" + name)
+    geom = B.GeomPack(c["gi"], c["gf"], c["comp_side"])
+    s0 = B.SidePack(c["a0"], c["blk0"], c["blkf0"], 1, c["r0"], 3)
+    s1 = B.SidePack(c["a1"], c["blk1"], c["blkf1"], 1, c["r1"], 2)
+    eps, n, k = 1e-5, 20_000, 8
+    rows = {}
+    for prec, seed in (("fp32", 101), ("ref64", 202)):
+        with B.Plan(geom, c["ksqrt"], c["poles2"], eps, 10**6, s0, s1, precision=prec) as plan:
+            batches = []
+            for b in range(k):
+                r = plan.run_raw(seed, n, rep_start=b * n)
+                a = np.concatenate([r.raw0, r.raw1], 1)
+                assert np.allclose(a.sum(1), n, rtol=1e-9), (prec, a.sum(1))
+                batches.append(a / n)
+            rows[prec] = np.array(batches)
+    g, r = rows["fp32"], rows["ref64"]
+    sp2 = (g.var(0, ddof=1) + r.var(0, ddof=1)) / 2
+    live = sp2 > 0
+    t = (g.mean(0) - r.mean(0))[live] / np.sqrt(sp2[live] * 2 / k)
+    crit = stats.t.isf(1e-3 / (2 * live.sum()), 2 * k - 2)
+    assert np.abs(t).max() <= crit, (np.abs(t).max(), crit)

@@ -3,7 +3,7 @@
 VAR=$1; VALS=$2
 mkdir -p gpurun_out
 for V in $VALS; do
-  env $VAR=$V python -m paper_2409_03686_b200.build_native --force > /dev/null 2>&1
+  env EXITMEASURE_B200_KNOBS=1 $VAR=$V python -m paper_2409_03686_b200.build_native --force > /dev/null 2>&1
   for C in 2 3 4 5; do
     NR=""; [ $C -ge 3 ] && NR="--n-rep 100000"; [ $C -eq 5 ] && NR="--n-rep 20000"
     timeout 300 python bench.py --steps 10 --warmup 2 --config $C $NR --no-cpu-baseline > gpurun_out/ab_${V}_c$C.log 2>&1
