@@ -714,8 +714,9 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
   const float fj = fmaf(m, P.tcd, sg * xj);                // s * foot_j
   float rho = fminf(bti, fminf((btj - fj) * P.tim, (btj + fj) * P.tip));
   rho = fmaf(fmaxf(rho, m), P.tkeep, -P.tsa);
-  // psi uniform in [-pi/2, pi/2): 23 bits into the mantissa of 1.0f
-  const float psi = fmaf(__uint_as_float(one_bits | (word >> 9)), kPi, -1.5f * kPi);
+  // psi uniform in [-pi/2, pi/2): the low 23 bits into the mantissa of 1.0f
+  // (one LOP3: (word & 0x7fffff) | one_bits)
+  const float psi = fmaf(__uint_as_float(one_bits | (word & 0x7fffffu)), kPi, -1.5f * kPi);
   float sn, cs;
   __sincosf(psi, &sn, &cs);
   const float N = m * sn, Dd = fmaf(2.0f, rho, -m) * cs;
@@ -906,22 +907,26 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
   const float aa = fmaf(P.Kd[0], p0, P.Kd[1] * p1);
   float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
   if (NH == 1) wm = fminf(wm, __saturatef(fmaf(s2, P.h2_scale, P.h2_bias)));
-  // clamped: a walk at the exact centre (x = 0) keeps finite terms
-  const float iaa = rsq(fmaxf(aa, 1e-30f));
+  // clamped: a walk at the exact centre (x = 0) keeps finite terms.  In the
+  // annulus (NH == 1) a walking lane has rho + eps < |x| < R - eps, so every
+  // square and root argument below is positive; a lane that is not walking
+  // (stopped, parked far outside) may produce NaNs, but its mask is 0 and
+  // the caller keeps its point -- no clamps there
+  const float iaa = rsq(NH == 1 ? aa : fmaxf(aa, 1e-30f));
   const float sa = aa * iaa;  // |Ax|
-  const float ir = rsq(fmaxf(s2, 1e-30f));
+  const float ir = rsq(NH == 1 ? s2 : fmaxf(s2, 1e-30f));
   // max chain: the largest centred whitened disk
   float rm;
   if (NH == 0) {
     const float q = P.oR2 - s2;
     rm = fmaf(fdiv(q, sa + fsqrt(fmaxf(aa + q, 0.0f))), P.keep, -P.shrink_abs);
   } else {
+    // min(qo / Do, qh / Dh) with one reciprocal: min(qo Dh, qh Do) / (Do Dh)
     const float qo = P.oR2 - s2;
-    const float Do = sa + fsqrt(fmaxf(aa + qo, 0.0f));
+    const float Do = sa + fsqrt(aa + qo);
     const float qh = s2 - P.hr2[0];
-    const float Dh = sa + fsqrt(fmaxf(fmaf(-P.m2, qh, aa), 0.0f));
-    const bool outer = qo * Dh <= qh * Do;
-    rm = fmaf(fdiv(outer ? qo : qh, outer ? Do : Dh), P.keep, -P.shrink_abs);
+    const float Dh = sa + fsqrt(fmaf(-P.m2, qh, aa));
+    rm = fmaf(fdiv(fminf(qo * Dh, qh * Do), Do * Dh), P.keep, -P.shrink_abs);
   }
   // rolling disk at the outer ellipse
   float rb = P.rho_b, rb2 = P.rho_b2, rh = P.rho_h, rh2 = P.rho_h2;
@@ -980,8 +985,8 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
   const float d = use ? d2 * id : 0.0f;
   const float e0 = use ? w0 * id : 1.0f, e1 = use ? w1 * id : 0.0f;
   const float m = rho - d;
-  // Moebius: psi uniform in [-pi/2, pi/2) from 23 bits
-  const float psi = fmaf(__uint_as_float(one_bits | (word >> 9)), kPi, -1.5f * kPi);
+  // Moebius: psi uniform in [-pi/2, pi/2) from the low 23 bits (one LOP3)
+  const float psi = fmaf(__uint_as_float(one_bits | (word & 0x7fffffu)), kPi, -1.5f * kPi);
   float sn, cs;
   __sincosf(psi, &sn, &cs);
   const float N = m * sn, Dd = fmaf(2.0f, rho, -m) * cs;
@@ -1681,16 +1686,19 @@ cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mo
     // one block per (pole, replicate range), the row's histogram in shared
     smem = ((size_t)P.w.row_len * 4 + 15) & ~(size_t)15;
     grid = (int)(P.w.n_poles * P.w.splits);
+    // the attribute is per (kernel, device context): remember both
     static std::mutex mu;
-    static std::vector<std::pair<const void*, size_t>> set;
+    static std::vector<std::pair<std::pair<const void*, int>, size_t>> set;
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
     bool done = false;
     for (auto& e : set)
-      if (e.first == (const void*)k && e.second >= smem) done = true;
+      if (e.first.first == (const void*)k && e.first.second == dev && e.second >= smem) done = true;
     if (!done) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      set.push_back({(const void*)k, smem});
+      set.push_back({{(const void*)k, dev}, smem});
     }
   }
   k<<<grid, block, smem, s>>>(P);
