@@ -205,6 +205,12 @@ int em_plan_run(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, em_
  * host copy for callers that convert the rows anyway. */
 int em_plan_run_host(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
                      const int64_t** block, int64_t* err_pole, int64_t* err_rep);
+/* same, with the count rows converted to float64 on the device (exact below
+ * 2^53): the first n_poles * (n0 + n1) words of *block are doubles -- the
+ * reference's float64 raw rows (S/backend.py:137-144) without a host-side
+ * conversion; the stats stay int64. */
+int em_plan_run_host_f64(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                         const int64_t** block, int64_t* err_pole, int64_t* err_rep);
 /* hand the page-locked block of the last em_plan_run_host to the caller
  * (zero-copy results): *block stays valid until em_host_block_free(*block);
  * the plan stages its next run in another block.  (Host-side adapters only:

@@ -101,6 +101,8 @@ def lib():
         "em_plan_run": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs)], ctypes.c_int),
         "em_plan_run_host": ([_p, _u64, _i64, _i64, ctypes.POINTER(ctypes.POINTER(_i64)), _p, _p],
                              ctypes.c_int),
+        "em_plan_run_host_f64": ([_p, _u64, _i64, _i64, ctypes.POINTER(ctypes.POINTER(_i64)),
+                                  _p, _p], ctypes.c_int),
         "em_plan_detach_block": ([_p, ctypes.POINTER(ctypes.POINTER(_i64))], ctypes.c_int),
         "em_host_block_free": ([_p], ctypes.c_int),
         "em_plan_run_device": ([_p, _u64, _i64, _i64, ctypes.POINTER(EmOutputs), _p],

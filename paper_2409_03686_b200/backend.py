@@ -415,15 +415,22 @@ class Plan:
         return AccumulateResult(raw0, raw1, stats[0].copy(), stats[1].copy(), stats[2].copy(),
                                 int(fb.value))
 
-    def run(self, seed: int, n_rep: int, rep_start: int = 0) -> AccumulateResult:
+    def run(self, seed: int, n_rep: int, rep_start: int = 0,
+            rows: str = "int64") -> AccumulateResult:
+        """All walks of the plan; ``rows="float64"`` returns the reference's
+        float64 raw0 / raw1 converted on the device (em_plan_run_host_f64,
+        no host-side conversion; ``counts`` is then None)."""
         if self.idw:
             return self.run_raw(seed, n_rep, rep_start)
+        if rows not in ("int64", "float64"):
+            raise ValidationError("rows must be 'int64' or 'float64'")
         row = self.n0 + self.n1
         blk = ctypes.POINTER(ctypes.c_int64)()
         ep, er = ctypes.c_int64(-1), ctypes.c_int64(-1)
-        rc = N.check(N.lib().em_plan_run_host(self._h, int(seed) & (2**64 - 1), int(rep_start),
-                                              int(n_rep), ctypes.byref(blk), ctypes.byref(ep),
-                                              ctypes.byref(er)), "em_plan_run_host")
+        fn = N.lib().em_plan_run_host_f64 if rows == "float64" else N.lib().em_plan_run_host
+        rc = N.check(fn(self._h, int(seed) & (2**64 - 1), int(rep_start), int(n_rep),
+                        ctypes.byref(blk), ctypes.byref(ep), ctypes.byref(er)),
+                     "em_plan_run_host")
         if rc == N.EM_BUDGET:
             raise self._budget_error(ep.value, rep_start + er.value)
         nc = self.n_poles * row
@@ -434,10 +441,14 @@ class Plan:
         cbuf = (ctypes.c_int64 * (nc + 3 * self.n_poles)).from_address(addr)
         weakref.finalize(cbuf, _free_block, addr)  # every numpy view keeps cbuf alive
         view = np.frombuffer(cbuf, dtype=np.int64)
-        counts = view[:nc].reshape(self.n_poles, row)
         stats = view[nc:].reshape(3, self.n_poles)
         ms = ctypes.c_double(0)
         N.lib().em_plan_last_stats(self._h, ctypes.byref(ms), None, None)
+        if rows == "float64":
+            f = np.frombuffer(cbuf, dtype=np.float64, count=nc).reshape(self.n_poles, row)
+            return AccumulateResult(f[:, : self.n0], f[:, self.n0:], stats[0], stats[1],
+                                    stats[2], 0, None, ms.value, n0=self.n0)
+        counts = view[:nc].reshape(self.n_poles, row)
         return AccumulateResult(None, None, stats[0], stats[1], stats[2], 0, counts, ms.value,
                                 n0=self.n0)
 
@@ -566,11 +577,12 @@ def _plan_key(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain
 def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_rep: int,
                    side0, side1, threads: int | None = None, *, precision: str | None = None,
                    chain: str | None = None, device: int | None = None,
-                   pole_ids=None, cache: bool = True) -> AccumulateResult:
+                   pole_ids=None, cache: bool = True, rows: str = "int64") -> AccumulateResult:
     """All (pole, replicate) walks in one kernel launch (S/backend.py:147-199).
 
     ``cache=False`` builds (and uploads) a one-shot plan even when a cached
-    plan for the same inputs exists.
+    plan for the same inputs exists.  ``rows="float64"`` converts the rows
+    to the reference's float64 raw0 / raw1 on the device (``counts`` None).
 
     ``threads`` is accepted for signature compatibility and ignored.  Raises
     WalkBudgetError(pole, replicate, max_steps) for the lexicographically
@@ -592,7 +604,7 @@ def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_r
     if not cache:
         with Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
                   pole_ids) as plan:
-            return plan.run(seed, n_rep)
+            return plan.run(seed, n_rep, rows=rows)
     key = _plan_key(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
                     pole_ids)
     with _PLAN_CACHE_LOCK:
@@ -601,14 +613,14 @@ def run_accumulate(dom, ksqrt, poles, seed: int, eps: float, max_steps: int, n_r
             _PLAN_CACHE.move_to_end(key)
     if hit is not None and hit[1].acquire(blocking=False):
         try:
-            return hit[0].run(seed, n_rep)
+            return hit[0].run(seed, n_rep, rows=rows)
         finally:
             hit[1].release()
     plan = Plan(geom, ksqrt, poles, eps, max_steps, side0, side1, precision, chain, device,
                 pole_ids)
     lock = threading.Lock()
     with lock:
-        res = plan.run(seed, n_rep)
+        res = plan.run(seed, n_rep, rows=rows)
     if hit is None:
         with _PLAN_CACHE_LOCK:
             if key not in _PLAN_CACHE:

@@ -41,6 +41,7 @@ cudaError_t launch_bin_points_f32(const F32Params& P, int d, int outer, const do
 cudaError_t launch_ffma_peak(float* out, int iters, int grid, int block, cudaStream_t s);
 cudaError_t launch_zero_ranges(unsigned long long* const* ptrs, const long long* words, int n,
                                cudaStream_t s);
+cudaError_t launch_rows_to_f64(unsigned long long* rows, long long n, cudaStream_t s);
 cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, long long n_poles,
                               unsigned long long* stats, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
@@ -952,10 +953,15 @@ static int plan_finish(em_plan* p, cudaStream_t s, int64_t n_rep, em_outputs* ou
 
 // run + one D2H of the whole output block into the plan's pinned staging
 static int plan_run_staged(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
-                           em_outputs* out) {
+                           em_outputs* out, bool f64 = false) {
   DeviceGuard dg(p->device);
   int rc = plan_launch(p, seed, rep_start, n_rep, 0, p->blk_counts, p->blk_stats, p->stream);
   if (rc) return rc;
+  if (f64) {  // the rows as float64 in place (exact: counts < 2^53), on the device
+    cudaError_t e = launch_rows_to_f64(p->blk_counts, p->n_poles * (p->n0 + p->n1), p->stream);
+    if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("rows to float64: ") + cudaGetErrorString(e));
+    p->last_launches += 1;
+  }
   cudaError_t ce = p->pin.alloc(p->blk_words * 8);
   if (ce != cudaSuccess) return fail(EM_ERR_NOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce));
   EM_CUDA(cudaMemcpyAsync(p->pin.p, p->blk_counts, p->blk_words * 8, cudaMemcpyDeviceToHost, p->stream));
@@ -1001,6 +1007,18 @@ struct Detached {
 std::mutex g_detached_mu;
 std::unordered_map<void*, Detached> g_detached;
 }  // namespace
+
+int em_plan_run_host_f64(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep,
+                         const int64_t** block, int64_t* err_pole, int64_t* err_rep) {
+  if (!p || !block) return fail(EM_ERR_INVALID, "plan/block null");
+  em_outputs o{};
+  int rc = plan_run_staged(p, seed, rep_start, n_rep, &o, true);
+  if (rc < 0) return rc;
+  *block = reinterpret_cast<const int64_t*>(p->pin.p);
+  if (err_pole) *err_pole = o.err_pole;
+  if (err_rep) *err_rep = o.err_rep;
+  return rc;
+}
 
 int em_plan_detach_block(em_plan* p, int64_t** block) {
   if (!p || !block) return fail(EM_ERR_INVALID, "plan/block null");

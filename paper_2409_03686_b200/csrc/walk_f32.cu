@@ -1825,6 +1825,21 @@ cudaError_t launch_zero_ranges(unsigned long long* const* ptrs, const long long*
   return cudaGetLastError();
 }
 
+// ---- count rows -> float64 in place (em_plan_run_host_f64: the reference's
+// float64 raw rows straight from the device; exact below 2^53) ----
+__global__ void rows_to_f64_kernel(unsigned long long* rows, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    rows[i] = (unsigned long long)__double_as_longlong((double)(long long)rows[i]);
+}
+
+cudaError_t launch_rows_to_f64(unsigned long long* rows, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+  rows_to_f64_kernel<<<(unsigned)blocks, 256, 0, s>>>(rows, n);
+  return cudaGetLastError();
+}
+
 // ---- fold the step-statistics copies (WorkOut::stat_copies) ----
 __global__ void stats_fold_kernel(const unsigned long long* scratch, int copies, long long n_poles,
                                   unsigned long long* stats) {

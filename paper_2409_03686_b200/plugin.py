@@ -91,7 +91,7 @@ def install(precision: str | None = None, chain: str | None = None, device: int 
         try:
             res = B.run_accumulate(dom, ksqrt, poles, seed, eps, max_steps, n_rep, side0, side1,
                                    threads, precision=precision, chain=chain, device=device,
-                                   cache=cache)
+                                   cache=cache, rows="float64")
         except WalkBudgetError as e:
             raise ref_budget(e.pole, e.replicate, e.max_steps) from None
         return module.AccumulateResult(res.raw0, res.raw1, res.steps_sum, res.steps_sq_sum,

@@ -289,3 +289,22 @@ def test_idw_family_refused_on_integer_rows(B):
     assert rc == N.EM_ERR_UNSUPPORTED, rc
     with pytest.raises(NativeError):
         N.check(rc, "em_run_accumulate")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "ref64"])
+def test_float64_rows_from_the_device(B, precision):
+    """em_plan_run_host_f64: the reference's float64 raw rows converted on
+    the device equal the int64 counts exactly (the plugin's path)."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(3).subset(8, 3000)
+    s0 = B.pack_side(cfg.fam0, 2, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, 2, cfg.eps)
+    a = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, 5, cfg.eps, 10**6, cfg.n_rep, s0, s1,
+                         precision=precision, cache=False)
+    f = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, 5, cfg.eps, 10**6, cfg.n_rep, s0, s1,
+                         precision=precision, cache=False, rows="float64")
+    assert f.counts is None and f.raw0.dtype == np.float64
+    assert np.array_equal(f.raw0, a.counts[:, : s0.size].astype(np.float64))
+    assert np.array_equal(f.raw1, a.counts[:, s0.size:].astype(np.float64))
+    assert np.array_equal(f.steps_sum, a.steps_sum) and np.array_equal(f.steps_max, a.steps_max)

@@ -67,3 +67,27 @@ if len(sys.argv) > 2 and sys.argv[2] == "prof":
                          s0, s1, precision="fp32", cache=False)
     pr.disable()
     pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+
+# the reference's entry point with the plugin installed (bench.py's e2e path)
+ref = Path(__file__).resolve().parents[1] / "oracle" / "_ref"
+if (ref / "exitmeasure").exists():
+    sys.path.insert(0, str(ref))
+    from paper_2409_03686_b200 import plugin
+
+    rb = plugin.install(precision="fp32", cache=False)
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    for it in range(4):
+        t0 = time.perf_counter()
+        r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
+                             cfg.n_rep, s0, s1, precision="fp32", cache=False)
+        t1 = time.perf_counter()
+        a0, a1 = r.raw0, r.raw1
+        t2 = time.perf_counter()
+        rr = rb.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
+                               cfg.n_rep, s0, s1)
+        t3 = time.perf_counter()
+        print(f"plugin path: backend.run_accumulate {1e3*(t1-t0):.3f} ms (kernel "
+              f"{r.kernel_ms:.3f}), raw0/raw1 float64 {1e3*(t2-t1):.3f} ms, reference entry "
+              f"point total {1e3*(t3-t2):.3f} ms")
+    plugin.uninstall(rb)
