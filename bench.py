@@ -321,6 +321,16 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL's communicator-init lines (rank / nranks) into per-rank files
+        # rank 0 reads back (NCCL reads these at init; a launcher's own
+        # settings win)
+        logdir = Path(os.environ.get("TMPDIR", "/tmp")) / \
+            f"em_nccl_{os.environ.get('TORCHELASTIC_RUN_ID', 'run')}_{os.environ.get('MASTER_PORT', 'x')}"
+        logdir.mkdir(parents=True, exist_ok=True)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", str(logdir / "nccl.%h.%p.log"))
+        os.environ.setdefault("EM_NCCL_LOG_GLOB", str(logdir / "nccl.*.log"))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local if world > 1 else 0
@@ -627,7 +637,8 @@ def run_harness_check(args):
 
 def self_launch(argv, n: int) -> int:
     """--gpus N without a torchrun environment: launch N ranks (one process
-    per GPU) through torch.distributed.run on 127.0.0.1, NCCL logging on."""
+    per GPU) through torch.distributed.run on 127.0.0.1 (each rank turns NCCL
+    init logging on, run_ours)."""
     import socket
     import subprocess
 
@@ -635,12 +646,6 @@ def self_launch(argv, n: int) -> int:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     env = dict(os.environ)
-    logdir = Path(os.environ.get("TMPDIR", "/tmp")) / f"em_nccl_{os.getpid()}"
-    logdir.mkdir(parents=True, exist_ok=True)
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    env.setdefault("NCCL_DEBUG_FILE", str(logdir / "nccl.%h.%p.log"))
-    env["EM_NCCL_LOG_GLOB"] = str(logdir / "nccl.*.log")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())]
     return subprocess.call(cmd + list(argv), env=env)
