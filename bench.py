@@ -54,7 +54,7 @@ F_STEP = {
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
     (2, "tangent"): (37, 3),                     # tangent balls in the whitened parallelogram
     (3, "woe"): (19, 4), (3, "max"): (29, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
-    (3, "tangent"): (55.6, 6.35),                # one rolling / hole-tangent disk, else centred
+    (3, "tangent"): (53.4, 6.35),                # one rolling / hole-tangent disk, else centred
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (4, "tangent"): (79.3, 8.25),                # rolling balls, else the centred ball
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
