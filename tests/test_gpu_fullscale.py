@@ -62,7 +62,7 @@ def _ref_module():
     return rb
 
 
-def reference_counts(cfg, n, seed, oracle=None):
+def reference_counts(cfg, n, seed, oracle=None, with_stats=False):
     """(n_poles, n0 + n1) exit counts in this package's column order from the
     reference's own run_accumulate (cfg1-cfg4, SURVEY Appendix A
     expressions) or, for cfg5, from the C oracle (brute-force binning)."""
@@ -97,7 +97,10 @@ def reference_counts(cfg, n, seed, oracle=None):
         s0 = rb.pack_side(None, cfg.d, cfg.eps)
     r = rb.run_accumulate(dom, cfg.kt.k_sqrt, cfg.poles, seed, cfg.eps, 10**6, n, s0, s1,
                           threads=THREADS)
-    return np.concatenate([r.raw0, r.raw1], 1).astype(np.int64)
+    counts = np.concatenate([r.raw0, r.raw1], 1).astype(np.int64)
+    if with_stats:
+        return counts, (r.steps_sum, r.steps_sq_sum, r.steps_max)
+    return counts
 
 
 def appendix_b(gpu, n_gpu, ref, n_ref, label):
@@ -266,3 +269,28 @@ def test_cfg2_reconstructed_u1(cfg2_estimates):
     (ROOT / "gpurun_out" / "fullscale_cfg2_u1.json").write_text(json.dumps(summary, indent=1))
     assert np.all(eg < 0.5) and np.all(er < 0.5), summary
     assert np.all(np.abs(t) <= crit), summary
+
+
+def test_ref64_reproduces_the_reference_at_full_scale(B):
+    """The bit-exact FP64 mirror at BASELINE scale: cfg2 at its full 256 poles
+    x 1e5 walks and cfg4 at 64 poles x 1e4, the REFERENCE's own compiled
+    kernel (oracle/_ref, all host threads) against this library's REF64 path
+    on the same seed -- every count and every step statistic identical."""
+    from paper_2409_03686_b200 import configs
+
+    rb = _ref_module()
+    for idx, n_poles, n in ((2, None, None), (4, 64, 10_000)):
+        cfg = configs.get(idx)
+        cfg = cfg.subset(n_poles, n) if n_poles else cfg
+        ref, st = reference_counts(cfg, cfg.n_rep, cfg.seed, with_stats=True)
+        s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+        s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+        # the reference expression bins by brute force over the generic family
+        # (reference_counts): the mirror with the same generic blocks
+        g1 = B.SidePack(s1.anchors, np.array([[0, 0, s1.size]], dtype=np.int64),
+                        np.zeros((1, 4)), 0, np.zeros(0), 2, np.zeros(1))
+        r = B.run_accumulate(cfg.dom, cfg.kt.k_sqrt, cfg.poles, cfg.seed, cfg.eps, 10**6,
+                             cfg.n_rep, s0, g1, precision="ref64")
+        assert np.array_equal(r.counts, ref), idx
+        assert np.array_equal(r.steps_sum, st[0]) and np.array_equal(r.steps_sq_sum, st[1])
+        assert np.array_equal(r.steps_max, st[2]), idx
