@@ -331,10 +331,19 @@ def run_ours(args):
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", str(logdir / "nccl.%h.%p.log"))
         os.environ.setdefault("EM_NCCL_LOG_GLOB", str(logdir / "nccl.*.log"))
+        # EXITMEASURE_B200_DEVICE pins every rank to one device: the harness
+        # self-test on a 1-GPU box (--dist-backend gloo; the ranks' kernels
+        # are independent, the exchange runs on the host)
+        if os.environ.get("EXITMEASURE_B200_DEVICE") is not None:
+            local = int(os.environ["EXITMEASURE_B200_DEVICE"])
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
+    coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"  # small collectives
     from paper_2409_03686_b200 import _native, backend, configs, distributed
 
     cfg = configs.get(args.config)
@@ -415,17 +424,22 @@ def run_ours(args):
     if dist and weak:
         # the one exchange, outside the timed region: sum the ranks' rows into
         # the N*n-walk estimate and check every row counts all of its walks
-        dist.all_reduce(counts)
+        if coll_dev == "cpu":
+            c = counts.cpu()
+            dist.all_reduce(c)
+            counts.copy_(c)
+        else:
+            dist.all_reduce(counts)
         combined_ok = bool((counts.sum(dim=1) == world * cfg.n_rep).all().item())
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([tot_ms, kernel_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([tot_ms, kernel_ms], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms, kernel_ms = float(t[0].item()), float(t[1].item())
-        st = torch.tensor([steps_per_run], device="cuda", dtype=torch.int64)
+        st = torch.tensor([steps_per_run], device=coll_dev, dtype=torch.int64)
         dist.all_reduce(st)
         steps_total_run = int(st.item())
     else:
@@ -487,7 +501,7 @@ def run_ours(args):
         r = call()
         dt = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            t = torch.tensor([dt], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e_vals.append(dt)
@@ -533,10 +547,10 @@ def run_ours(args):
                                           f" (row sums {'ok' if combined_ok else 'WRONG'})")
                                        if weak else
                                        f"rows cyclic over {world} GPU(s) (pole i -> rank i mod "
-                                       f"{world})" + (", one NCCL all-gather of the count rows + "
-                                                      "step statistics and the un-permute to pole "
-                                                      "order inside every timed step"
-                                                      if world > 1 else "")),
+                                       f"{world})" + (f", one {args.dist_backend.upper()} all-gather "
+                                                      "of the count rows + step statistics and the "
+                                                      "un-permute to pole order inside every timed "
+                                                      "step" if world > 1 else "")),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "counts": "int64 (n_poles, n0+n1) rows + step stats",
                        "scheduler": plan.last_scheduler(),
@@ -678,6 +692,9 @@ def main(argv=None):
                          "the timed region")
     ap.add_argument("--harness-check", action="store_true",
                     help="launch / rendezvous plumbing only (gloo, no GPU)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 exchange backend (gloo: the multi-rank harness self-test on one "
+                         "GPU with EXITMEASURE_B200_DEVICE=0; not a measurement)")
     args = ap.parse_args(argv)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return self_launch(argv, args.gpus)

@@ -62,7 +62,12 @@ def exchange_rows(buf, gathered, index, m_pad: int, row: int, out, group=None) -
     import torch
     import torch.distributed as dist
 
-    dist.all_gather_into_tensor(gathered.view(-1), buf, group=group)
+    if dist.get_backend(group) == "gloo" and buf.is_cuda:  # host exchange (harness test)
+        g = gathered.cpu()
+        dist.all_gather_into_tensor(g.view(-1), buf.cpu(), group=group)
+        gathered.copy_(g)
+    else:
+        dist.all_gather_into_tensor(gathered.view(-1), buf, group=group)
     rows = gathered[:, : m_pad * row].reshape(gathered.shape[0] * m_pad, row)
     torch.index_select(rows, 0, index, out=out)
 
@@ -102,7 +107,7 @@ def run_accumulate_sharded(dom, ksqrt, poles, seed: int, eps: float, max_steps: 
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    device = int(os.environ.get("LOCAL_RANK", "0"))
+    device = int(os.environ.get("EXITMEASURE_B200_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     poles = np.ascontiguousarray(poles, dtype=np.float64)
     n_poles = poles.shape[0]
     ids = shard_rows(n_poles, world, rank)

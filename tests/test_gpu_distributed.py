@@ -53,3 +53,34 @@ def test_nccl_sharded_equals_single(tmp_path):
     res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
     assert res.stdout.count("ok ") == 2
+
+
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_bench_multi_rank_path_self_test(scaling):
+    """bench.py's N > 1 path end to end with 2 ranks on this one GPU
+    (EXITMEASURE_B200_DEVICE=0; the ranks' kernels are independent and the
+    exchange runs over gloo on the host -- a harness self-test, not a
+    measurement): row shards / replicate ranges, the all-gather and
+    un-permute (strong) or row sum (weak), max-over-ranks timing, the e2e
+    path, one JSON line from rank 0 with n_gpus 2."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["EXITMEASURE_B200_DEVICE"] = "0"
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--dist-backend",
+                          "gloo", "--scaling", scaling, "--config", "2", "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True,
+                         env=env, timeout=900)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
+    if scaling == "weak":
+        assert "row sums ok" in d["config"]["parallelism"]
