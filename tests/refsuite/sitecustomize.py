@@ -56,3 +56,29 @@ if os.environ.get("EM_B200_REFSUITE") == "1" and \
             f.write(f"{os.getpid()} {' '.join(sys.argv[:3])} backend={_rb.BACKEND} "
                     f"kernel={getattr(sys.modules['exitmeasure._kernel'], '__em_b200__', False)}\n")
     del types
+
+
+def _chain_next_sitecustomize():
+    """Run the next sitecustomize on sys.path too (this one shadows it), so a
+    launcher's own hook (e.g. one that records loaded libraries) still runs."""
+    import importlib.util
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    for entry in sys.path:
+        try:
+            cand = Path(entry or ".").resolve() / "sitecustomize.py"
+        except OSError:
+            continue
+        if cand.parent == here or not cand.is_file():
+            continue
+        spec = importlib.util.spec_from_file_location("_em_chained_sitecustomize", cand)
+        mod = importlib.util.module_from_spec(spec)
+        try:
+            spec.loader.exec_module(mod)
+        except Exception:  # a foreign hook's failure must not break the suite
+            pass
+        return
+
+
+_chain_next_sitecustomize()

@@ -36,8 +36,9 @@ def test_reference_suite_passes_on_gpu_backend(tmp_path):
     log = tmp_path / "patched.log"
     env = dict(os.environ, EM_B200_REFSUITE="1", EM_B200_ROOT=str(ROOT),
                EM_B200_REFSUITE_LOG=str(log),
-               PYTHONPATH=os.pathsep.join([str(ROOT / "tests" / "refsuite"), str(REF),
-                                           str(ROOT)]))
+               PYTHONPATH=os.pathsep.join([str(ROOT / "tests" / "refsuite"), str(REF), str(ROOT)]
+                                          + [p for p in os.environ.get("PYTHONPATH", "").split(
+                                              os.pathsep) if p]))
     env.pop("EXITMEASURE_BACKEND", None)
     cmd = [sys.executable, "-m", "pytest", "-q", "-s", "-p", "no:cacheprovider", "-rfE"] + SUITE
     res = subprocess.run(cmd, cwd=REF / "ref_tests", env=env, capture_output=True, text=True,
