@@ -399,7 +399,11 @@ def run_ours(args):
         one_step()
     torch.cuda.synchronize()
     steps_per_run = int(stats[0, :m_local].sum().item())
-    if full is not None:  # the gathered rows count every walk of every pole once
+    # every walk of every pole counted exactly once (this rank's rows; at N>1
+    # strong also the gathered full matrix) -- checked on the device
+    if not bool((counts[:m_local].sum(1) == cfg.n_rep).all().item()):
+        raise RuntimeError("count rows do not sum to the walk count")
+    if full is not None:
         assert bool((full.sum(1) == cfg.n_rep).all().item()), "gathered rows wrong"
     ffma_peak, _ = _native.fp32_peak(device)
     info = _native.device_info(device)
