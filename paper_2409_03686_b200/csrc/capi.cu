@@ -80,6 +80,7 @@ struct DeviceGrid {
   void* dev = nullptr;
   const uint32_t* cell = nullptr;
   const uint32_t* cand = nullptr;
+  const float4* candv = nullptr;  // the candidates' coordinates, index in .w (bits)
   ~DeviceGrid() {
     if (!dev) return;
     int prev = -1;
@@ -347,21 +348,34 @@ std::shared_ptr<DeviceGrid> cached_device_grid(const double* anchors, int64_t m,
   GridHost G;
   if (!build_grid(anchors, m, d, eps, G)) return nullptr;
   auto D = std::make_shared<DeviceGrid>();
+  // candidate lists twice: indices (the point binner) and the candidates'
+  // FP32 coordinates with the index in .w (the walk kernel's scan: one load
+  // per candidate instead of two dependent ones)
   const size_t cb = G.cell.size() * 4, nb = G.cand.size() * 4;
+  const size_t vo = (cb + nb + 15) & ~(size_t)15, vb = G.cand.size() * 16;
+  std::vector<float> cv(G.cand.size() * 4, 0.0f);
+  for (size_t k = 0; k < G.cand.size(); ++k) {
+    const uint32_t a = G.cand[k];
+    for (int j = 0; j < d; ++j) cv[4 * k + j] = (float)anchors[(size_t)a * d + j];
+    std::memcpy(&cv[4 * k + 3], &a, 4);
+  }
   D->device = device;
-  if (cudaMalloc(&D->dev, cb + nb) != cudaSuccess) {
+  if (cudaMalloc(&D->dev, vo + vb) != cudaSuccess) {
     D->dev = nullptr;
     cudaGetLastError();
     return nullptr;
   }
   if (cudaMemcpy(D->dev, G.cell.data(), cb, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(static_cast<char*>(D->dev) + cb, G.cand.data(), nb, cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cudaMemcpy(static_cast<char*>(D->dev) + vo, cv.data(), vb, cudaMemcpyHostToDevice) !=
           cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
   D->cell = static_cast<const uint32_t*>(D->dev);
   D->cand = reinterpret_cast<const uint32_t*>(static_cast<char*>(D->dev) + cb);
+  D->candv = reinterpret_cast<const float4*>(static_cast<char*>(D->dev) + vo);
   for (int j = 0; j < 3; ++j) {
     D->lo[j] = G.lo[j];
     D->n[j] = G.n[j];
@@ -700,6 +714,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
         if (auto G = cached_device_grid(S->anchors, S->n_anchors, d, eps, o.device)) {
           D.grid.cell = G->cell;
           D.grid.cand = G->cand;
+          D.grid.candv = G->candv;
           D.has_grid = 1;
           for (int j = 0; j < 3; ++j) {
             D.grid.lo[j] = (float)G->lo[j];

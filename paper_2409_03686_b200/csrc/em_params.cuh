@@ -46,6 +46,7 @@ struct Grid32 {
   int n[3];
   const unsigned* cell;
   const unsigned* cand;
+  const float4* candv;  // the same lists as coordinates, anchor index in .w (bits)
 };
 
 struct Side64 {

@@ -507,17 +507,28 @@ __device__ __forceinline__ int bin_exit(const F32Params& P, int side, const floa
       cnt = w & 255u;
       off = w >> 8;
     }
-    const unsigned* cand = pick(side, S0.grid.cand, S1.grid.cand);
-    const bool brute = cnt == 255u;
-    const int n = brute ? na : (int)cnt;
     float best = kInf;
     int bi = 0;
-    for (int j = 0; j < n; ++j) {
-      const int a = brute ? j : (int)__ldg(&cand[off + j]);
-      const float t = d2_to<D>(__ldg(&anchors[a]), x);
-      if (t < best || (t == best && a < bi)) {
+    if (cnt != 255u) {
+      // the cell's candidates with their coordinates inline: one 16-byte
+      // load per candidate
+      const float4* cv = pick(side, S0.grid.candv, S1.grid.candv) + off;
+      for (unsigned j = 0; j < cnt; ++j) {
+        const float4 c = __ldg(&cv[j]);
+        const int a = __float_as_int(c.w);
+        const float t = d2_to<D>(c, x);
+        if (t < best || (t == best && a < bi)) {
+          best = t;
+          bi = a;
+        }
+      }
+      return bi;
+    }
+    for (int j = 0; j < na; ++j) {  // outside the band: brute force
+      const float t = d2_to<D>(__ldg(&anchors[j]), x);
+      if (t < best) {
         best = t;
-        bi = a;
+        bi = j;
       }
     }
     return bi;
