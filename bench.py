@@ -370,7 +370,8 @@ def run_ours(args):
                         precision=args.precision, chain=args.chain, device=device,
                         pole_ids=ids, grid=args.grid,
                         flags={"auto": 0, "persistent": _native.EM_FLAG_PERSISTENT,
-                               "pole-blocks": _native.EM_FLAG_POLE_BLOCKS}[args.sched])
+                               "pole-blocks": _native.EM_FLAG_POLE_BLOCKS}[args.sched]
+                        | (_native.EM_FLAG_ONE_WALK_PER_LANE if args.lanes == "one" else 0))
     row = plan.n0 + plan.n1
     m_local = len(ids)
     m_pad = m_local if weak else -(-cfg.n_poles // world)
@@ -698,6 +699,9 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", type=int, default=0, help="persistent blocks (0 = auto)")
+    ap.add_argument("--lanes", default="auto", choices=["auto", "one"],
+                    help="one: force the one-walk-per-lane kernel where the packed "
+                         "two-walks-per-lane kernel exists (A/B)")
     ap.add_argument("--sched", default="auto", choices=["auto", "persistent", "pole-blocks"],
                     help="auto: per-block shared-memory histograms where the rows exceed half "
                          "the L2, else pole-cycling persistent warps; pole-blocks / persistent "

@@ -145,6 +145,13 @@ typedef struct {
  * flags force one or the other (A/B measurements). */
 #define EM_FLAG_PERSISTENT 2
 #define EM_FLAG_POLE_BLOCKS 4
+/* FP32 counts on the 2D ball's rolling-disk chain (cfg3) run TWO walks per
+ * lane with packed FP32 arithmetic (FFMA2 / FMUL2 / FADD2: one issued
+ * instruction per pair of operations; walk_f32x2.cu).  Same walks, same
+ * streams, same operation tree: the counts equal the one-walk-per-lane
+ * kernel's bit for bit.  This flag forces the one-walk-per-lane kernel
+ * (A/B measurements, the equality test). */
+#define EM_FLAG_ONE_WALK_PER_LANE 8
 
 /* Per-run outputs.  Host pointers for em_plan_run / em_run_accumulate,
  * device pointers for em_plan_run_device.  counts is (n_poles, n0 + n1)
@@ -236,6 +243,9 @@ int64_t em_plan_n_bins(const em_plan* p, int side);
  * 1 the same with per-warp shared step-statistics tables (tiny jobs), 2 the
  * pole-block scheduler with per-block shared-memory histograms; -1 none */
 int em_plan_last_scheduler(const em_plan* p);
+/* walks per lane of the plan's integer-count kernel: 2 where the packed
+ * two-walks-per-lane kernel runs (EM_FLAG_ONE_WALK_PER_LANE forces 1) */
+int em_plan_walks_per_lane(const em_plan* p);
 /* the walk chain the plan runs (EM_CHAIN_*): EM_CHAIN_TANGENT falls back to
  * EM_CHAIN_MAX where no tangent-ball step exists for the geometry */
 int em_plan_chain(const em_plan* p);

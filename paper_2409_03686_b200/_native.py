@@ -22,6 +22,10 @@ from .errors import NativeError
 DEBUG = os.environ.get("EXITMEASURE_B200_DEBUG") == "1"
 LIB_PATH = (Path(__file__).resolve().parent / "lib"
             / ("libexitmeasure_b200_debug.so" if DEBUG else "libexitmeasure_b200.so"))
+# A/B tooling only (tools/diag/x2_variants.sh): load a variant build instead;
+# em_build_info() in every bench line says what was loaded
+if os.environ.get("EXITMEASURE_B200_LIB"):
+    LIB_PATH = Path(os.environ["EXITMEASURE_B200_LIB"]).resolve()
 
 EM_OK = 0
 EM_BUDGET = 1
@@ -37,6 +41,7 @@ EM_CHAIN_TANGENT = 2
 EM_FLAG_TANGENT_ON_IDENTITY = 1
 EM_FLAG_PERSISTENT = 2
 EM_FLAG_POLE_BLOCKS = 4
+EM_FLAG_ONE_WALK_PER_LANE = 8
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
@@ -115,6 +120,7 @@ def lib():
                              ctypes.c_int),
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
         "em_plan_last_scheduler": ([_p], ctypes.c_int),
+        "em_plan_walks_per_lane": ([_p], ctypes.c_int),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),
                                ctypes.POINTER(EmSide), _p, _p, _i64, _u64, _dbl, _i64, _i64,
                                ctypes.POINTER(EmOptions), ctypes.POINTER(EmOutputs)],

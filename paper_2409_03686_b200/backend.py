@@ -535,6 +535,10 @@ class Plan:
         return {0: "persistent", 1: "persistent+smem-stats", 2: "pole-blocks"}.get(
             int(N.lib().em_plan_last_scheduler(self._h)), "none")
 
+    def walks_per_lane(self) -> int:
+        """2 where counts run on the packed two-walks-per-lane kernel."""
+        return int(N.lib().em_plan_walks_per_lane(self._h))
+
     def last_launches(self) -> int:
         v = ctypes.c_int64(0)
         N.lib().em_plan_last_launches(self._h, ctypes.byref(v))

@@ -36,7 +36,7 @@ NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 KNOB_DEFAULTS = {"EM_BATCH_STEPS": "8", "EM_MIN_BLOCKS": "0", "EM_ANGLE_BITS": "16",
                  "EM_Z_BITS": "16", "EM_TAB_WARP": "0", "EM_ROLL2_BLOCKS": "4",
                  "EM_ROLL2_DYN": "0", "EM_POST_STOP": "1", "EM_TANG_K": "4",
-                 "EM_ROLL2_ONE": "1", "EM_POLY_SINCOS": "0"}
+                 "EM_ROLL2_ONE": "1", "EM_POLY_SINCOS": "0", "EM_X2_BLOCKS": "4"}
 
 
 def knobs() -> dict:
@@ -51,6 +51,8 @@ def units(debug: bool = False):
     return [
         ("walk_ref64.cu", ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"] + dbg),
         ("walk_f32.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false"]
+         + [f"-D{k}={v}" for k, v in knobs().items()] + dbg),
+        ("walk_f32x2.cu", ["-fmad=true", "-prec-sqrt=false", "-prec-div=false"]
          + [f"-D{k}={v}" for k, v in knobs().items()] + dbg),
         ("capi.cu", dbg),
         ("plan_f32.cu", dbg),

@@ -46,6 +46,11 @@ cudaError_t launch_stats_fold(const unsigned long long* scratch, int copies, lon
                               unsigned long long* stats, cudaStream_t s);
 cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ident, int bink, int* nb);
 bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink);
+// two walks per lane, packed FP32 arithmetic (walk_f32x2.cu)
+bool f32x2_available(int d, int outer, int nh_mode, int chain, bool ident);
+cudaError_t f32x2_blocks_per_sm(int nh_mode, int bink, int* nb);
+cudaError_t launch_f32x2(const F32Params& P, int nh_mode, int bink, int grid, int block,
+                         cudaStream_t s);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
@@ -280,6 +285,8 @@ struct em_plan {
   int wkind[2] = {0, 0}, idw_power[2] = {2, 2};
   int flags = 0;  // em_options.flags
   bool pole_blocks = false;  // the FP32 kernel family has the pole-block scheduler
+  bool pack2 = false;        // counts mode runs two walks per lane (walk_f32x2.cu)
+  int grid2 = 0;             // its persistent grid
   int last_sched = -1;       // scheduler of the last integer-count launch
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -775,8 +782,16 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
       per_sm = nb;
   }
   p->grid = o.grid > 0 ? o.grid : sm_count_of(o.device) * per_sm * (256 / p->block > 0 ? 256 / p->block : 1);
-  if (p->precision == EM_PREC_FP32)
+  if (p->precision == EM_PREC_FP32) {
     p->pole_blocks = f32_has_pole_blocks(p->d, p->outer, p->nh_mode, p->chain, p->ident, p->bink);
+    int nb2 = 0;
+    if (!(o.flags & EM_FLAG_ONE_WALK_PER_LANE) && p->block == 256 &&
+        f32x2_available(p->d, p->outer, p->nh_mode, p->chain, p->ident) &&
+        f32x2_blocks_per_sm(p->nh_mode, p->bink, &nb2) == cudaSuccess && nb2 > 0) {
+      p->pack2 = true;
+      p->grid2 = o.grid > 0 ? o.grid : sm_count_of(o.device) * nb2;
+    }
+  }
   *out = p;
   return EM_OK;
 }
@@ -799,7 +814,8 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   w->total = total;
   // chunk size: enough chunks for ~8 per resident warp, 32..2048 replicates
   {
-    const double warps = (double)p->grid * (p->block / 32);
+    const bool x2 = p->pack2 && mode == 0;
+    const double warps = (double)(x2 ? p->grid2 : p->grid) * (p->block / 32);
     long long rb = 32;
     while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
     w->rb = rb;
@@ -899,8 +915,9 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   }
   p->last_timed = false;
   if (total > 0) {
-    const int64_t lanes_needed = (total + 31) / 32 * 32;
-    int grid = p->grid;
+    const bool x2 = p->pack2 && mode == 0;
+    const int64_t lanes_needed = x2 ? (total + 63) / 64 * 32 : (total + 31) / 32 * 32;
+    int grid = x2 ? p->grid2 : p->grid;
     const int64_t blocks_needed = (lanes_needed + p->block - 1) / p->block;
     if (blocks_needed < grid) grid = (int)std::max<int64_t>(1, blocks_needed);
     EM_CUDA(cudaEventRecord(p->ev0, s));
@@ -914,8 +931,11 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
       p->p32.key0 = (unsigned)(seed & 0xffffffffULL);
       p->p32.key1 = (unsigned)(seed >> 32);
       p->p32.rk = philox32_schedule(p->p32.key0, p->p32.key1);
-      e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, p->bink,
-                     grid, p->block, s);
+      if (x2)
+        e = launch_f32x2(p->p32, p->nh_mode, p->bink, grid, p->block, s);
+      else
+        e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, p->bink,
+                       grid, p->block, s);
     }
     if (e != cudaSuccess) return fail(EM_ERR_CUDA, std::string("walk kernel launch: ") + cudaGetErrorString(e));
     launches += 1;
@@ -1124,6 +1144,7 @@ int em_plan_last_launches(const em_plan* p, int64_t* launches) {
 }
 
 int em_plan_last_scheduler(const em_plan* p) { return p ? p->last_sched : -1; }
+int em_plan_walks_per_lane(const em_plan* p) { return p ? (p->pack2 ? 2 : 1) : -1; }
 
 int64_t em_plan_n_bins(const em_plan* p, int side) {
   if (!p) return -1;

@@ -189,6 +189,9 @@ struct F32Params {
   float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
   float oR2, s2_scale, s2_bias;  // ball: R^2 and sat(-|x|^2 s + b) = [|x|^2 < (R - eps)^2]
   float h2_scale, h2_bias;       // concentric hole: sat(|x|^2 s + b) = [|x|^2 > (rho + eps)^2]
+  // the same two thresholds as plain numbers (the two-walks-per-lane kernel
+  // tests them with compares): walking <=> s2_lo < |x|^2 < s2_hi
+  float s2_hi, s2_lo;
   float shrink_rel, shrink_abs;  // step safety margins
   float keep;                    // 1 - shrink_rel
   unsigned one_bits;             // 0x3f800000 (1.0f), opaque to the compiler: PRMT operand

@@ -306,6 +306,8 @@ struct F32Build {
       const int k = 24 - (ex - 1) + 2;
       P.s2_scale = std::ldexp(1.0f, k);
       P.s2_bias = c * P.s2_scale;
+      P.s2_hi = c;
+      P.s2_lo = -1.0f;  // no hole: |x|^2 >= 0 always passes
       if (nh >= 1) {
         // concentric hole: the same construction for |x|^2 > (rho + eps)^2
         const double rho = gf[d + 1 + d];
@@ -314,6 +316,7 @@ struct F32Build {
         const int kh = 24 - (ex - 1) + 2;
         P.h2_scale = std::ldexp(1.0f, kh);
         P.h2_bias = -ch * P.h2_scale;
+        P.s2_lo = ch;
       }
     }
   }

@@ -1,0 +1,133 @@
+"""The packed two-walks-per-lane kernel equals the one-walk-per-lane kernel.
+
+FP32 counts on the 2D ball's rolling-disk chain (cfg3, the headline) run two
+walks per lane with Blackwell's packed FP32 instructions (FFMA2 / FMUL2 /
+FADD2, csrc/walk_f32x2.cu).  Both kernels instantiate ONE operation tree
+(csrc/walk_f32_dev.cuh roll2_core, explicit round-to-nearest operations), key
+every walk's random stream by (seed, global pole id, replicate) and
+accumulate integers, so counts and step statistics must agree EXACTLY --
+on every scheduler, on row shards, with replicate offsets, and in the budget
+error they report.  The one-walk kernel's sampler is the one the closed-form
+tests pin (tests/test_gpu_closed_form.py); this file carries that evidence
+over to the packed kernel bit for bit."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2409_03686_b200 import _native, backend
+
+    _native.require_device(0)
+    return backend
+
+
+def _plans(B, cfg, pole_ids=None, max_steps=10**6, sched=0):
+    from paper_2409_03686_b200 import _native
+
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    mk = lambda fl: B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, max_steps, s0, s1,
+                           precision="fp32", pole_ids=pole_ids, flags=fl | sched)
+    return mk(0), mk(_native.EM_FLAG_ONE_WALK_PER_LANE)
+
+
+def _same(a, b):
+    assert np.array_equal(a.counts, b.counts)
+    assert np.array_equal(a.steps_sum, b.steps_sum)
+    assert np.array_equal(a.steps_sq_sum, b.steps_sq_sum)
+    assert np.array_equal(a.steps_max, b.steps_max)
+
+
+@pytest.mark.parametrize("n_poles,n_rep", [(1024, 20_000), (64, 300_000), (7, 1), (3, 65), (1, 5_000)])
+def test_packed_equals_one_walk_per_lane_cfg3(B, n_poles, n_rep):
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(3).subset(n_poles)
+    p2, p1 = _plans(B, cfg)
+    with p2, p1:
+        assert p2.walks_per_lane() == 2 and p1.walks_per_lane() == 1
+        r2, r1 = p2.run(cfg.seed, n_rep), p1.run(cfg.seed, n_rep)
+    assert np.array_equal(r2.counts.sum(1), np.full(cfg.n_poles, n_rep))
+    _same(r2, r1)
+
+
+def test_packed_equals_one_walk_per_lane_schedulers_shards_offsets(B):
+    """Pole blocks (shared-memory histograms) and pole-cycling warps, on a
+    row shard with global pole ids and a replicate offset beyond 2^32."""
+    from paper_2409_03686_b200 import _native, configs
+
+    cfg = configs.get(3).subset(16)
+    ids = np.arange(3, 64, 4)
+    ref = None
+    for sched in (_native.EM_FLAG_PERSISTENT, _native.EM_FLAG_POLE_BLOCKS):
+        p2, p1 = _plans(B, cfg, pole_ids=ids, sched=sched)
+        with p2, p1:
+            r2 = p2.run(cfg.seed, 40_000, (1 << 32) + 12_345)
+            r1 = p1.run(cfg.seed, 40_000, (1 << 32) + 12_345)
+            assert p2.walks_per_lane() == 2
+            assert p2.last_scheduler() == p1.last_scheduler()
+        _same(r2, r1)
+        if ref is not None:
+            _same(r2, ref)
+        ref = r2
+
+
+def test_packed_budget_error_equals_one_walk_per_lane(B):
+    """A step budget the walks overrun (the per-step budget path of the packed
+    kernel): the same lexicographically first (global pole, replicate)."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.errors import WalkBudgetError
+
+    cfg = configs.get(3).subset(5)
+    ids = np.array([9, 4, 11, 2, 40])
+    errs = []
+    for plan in _plans(B, cfg, pole_ids=ids, max_steps=3):
+        with plan:
+            with pytest.raises(WalkBudgetError) as ei:
+                plan.run(cfg.seed, 8192)
+            errs.append((ei.value.pole, ei.value.replicate))
+    assert errs[0] == errs[1] and errs[0][0] == 9
+    # a budget only the long walks overrun: some batches take the per-step
+    # path, the rest the fast path; results must still agree where no walk fails
+    p2, p1 = _plans(B, cfg, max_steps=64)
+    with p2, p1:
+        try:
+            r2 = p2.run(cfg.seed, 2000)
+        except WalkBudgetError as e:
+            r2 = (e.pole, e.replicate)
+        try:
+            r1 = p1.run(cfg.seed, 2000)
+        except WalkBudgetError as e:
+            r1 = (e.pole, e.replicate)
+    if isinstance(r2, tuple) or isinstance(r1, tuple):
+        assert r2 == r1
+    else:
+        _same(r2, r1)
+
+
+def test_packed_disc_without_hole_equals_one_walk_per_lane(B):
+    """The no-hole instantiation (2D ball, K != I, rolling disks): cfg3's K on
+    the unit disc with 256 arcs."""
+    from paper_2409_03686_b200 import _native, configs
+    from paper_2409_03686_b200.geometry import Ball, Domain, circle_points
+
+    cfg = configs.get(3)
+    dom = Domain(2, Ball(np.zeros(2), 1.0), (), frozenset())
+    fam1 = circle_points(np.zeros(2), 1.0, 256, component=0, phase=0.5)
+    geom = B.pack_geometry(dom)
+    s0 = B.pack_side(None, 2, cfg.eps)
+    s1 = B.pack_side(fam1, 2, cfg.eps)
+    poles = 0.8 * cfg.poles[:48]
+    out = []
+    for fl in (0, _native.EM_FLAG_ONE_WALK_PER_LANE):
+        with B.Plan(geom, cfg.kt.k_sqrt, poles, cfg.eps, 10**6, s0, s1, precision="fp32",
+                    flags=fl) as plan:
+            out.append((plan.run(cfg.seed, 50_000), plan.walks_per_lane()))
+    assert out[0][1] == 2 and out[1][1] == 1
+    assert np.array_equal(out[0][0].counts.sum(1), np.full(48, 50_000))
+    _same(out[0][0], out[1][0])
