@@ -176,6 +176,10 @@ struct F32Params {
   float rho_b, rho_b2;
   float rho_h, rho_h2;  // 2D concentric annulus: disks tangent to the hole from outside
   float mid2;           // ((R + rho) / 2)^2: which boundary's disk a step tries (EM_ROLL2_ONE)
+  // roll2_core's blends and centred radius: rc_d = rho_b - rho_h with
+  // fl(rho_h + rc_d) == rho_b exactly, nr_d = hr - R, im2 = 1 / m2 (rounded
+  // down), shrink_c = shrink_abs + the error bound of the difference forms
+  float rc_d, nr_d, im2, shrink_c;
   // EM_ROLL2_DYN: per-step radii (R - rho)(1 - 1e-6) / (max Ad + |diag(Ad) n|)
   float rb_bl, gap, amax, K4[3];
   float ia[3];      // 1 / Ad

@@ -78,6 +78,7 @@ struct F32Build {
   F32Params& P;
   double frame[3] = {0.0, 0.0, 0.0};
   double scale = 1.0;
+  double roll_S = 0.0;  // rolling chains: bound of |Ax| and of the roots of the centred radius
   double Qd[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
   double Adiag[3] = {1.0, 1.0, 1.0};
   double axd[3] = {1.0, 1.0, 1.0}, shear_g[3] = {1.0, 1.0, 1.0};
@@ -154,7 +155,17 @@ struct F32Build {
       }
       rb *= 1.0 - 1e-6;
       P.rho_b = (float)rb;
-      P.rho_b2 = (float)(rb * rb);
+      if (nh == 1 && d == 2) {
+        // roll2_core blends the radius as fl(rho_h + of rc_d), of in {0, 1}:
+        // round rho_b down to a value that sum reproduces exactly
+        float dd = P.rho_b - P.rho_h;  // <= 0
+        while (P.rho_h + dd > P.rho_b) dd = std::nextafter(dd, -1.0e30f);
+        P.rc_d = dd;
+        P.rho_b = P.rho_h + dd;
+        P.nr_d = (float)gf[d + 1 + d] - (float)gf[d];
+      }
+      P.rho_b2 = (float)((double)P.rho_b * (double)P.rho_b);
+      roll_S = std::max(amax, 1.0) * gf[d];
       for (int i = 0; i < d; ++i) P.ia[i] = (float)(1.0 / Adiag[i]);
     }
   }
@@ -326,6 +337,11 @@ struct F32Build {
     P.shrink_rel = 4.0e-6f;
     P.shrink_abs = (float)(scale * 1.1920928955078125e-07);
     P.keep = 1.0f - P.shrink_rel;
+    // the centred radius of roll2_core as a difference of two terms <= roll_S,
+    // each within ~2e-7 relative (rsqrt.approx / sqrt.approx bounds, the
+    // rounding of their arguments), times 1 / m2 on the hole's side
+    P.im2 = P.m2 > 0.0f ? std::nextafter(1.0f / P.m2, 0.0f) : 0.0f;
+    P.shrink_c = P.shrink_abs + (float)(5.0e-7 * roll_S * std::max(1.0, (double)P.im2));
     for (int i = 0; i < 3; ++i)  // rounded down: the folded margin is never smaller
       P.gk[i] = std::nextafter((float)((double)P.g[i] * (double)P.keep), 0.0f);
   }
@@ -501,6 +517,8 @@ extern "C" int em_f32_constant(const em_geometry* g, int chain, int ident, doubl
       {"stop_scale", &P.stop_scale, 1},                     {"stop_bias", &P.stop_bias, 1},
       {"s2_scale", &P.s2_scale, 1},                         {"s2_bias", &P.s2_bias, 1},
       {"h2_scale", &P.h2_scale, 1},                         {"h2_bias", &P.h2_bias, 1},
+      {"s2_hi", &P.s2_hi, 1},    {"s2_lo", &P.s2_lo, 1},    {"rc_d", &P.rc_d, 1},
+      {"nr_d", &P.nr_d, 1},      {"im2", &P.im2, 1},        {"shrink_c", &P.shrink_c, 1},
       {"oR2", &P.oR2, 1},        {"hr", P.hr, 1},           {"hc", &P.hc[0][0], 3},
       {"frame", P.frame, 3},     {"eps", &P.eps, 1},
   };

@@ -1120,21 +1120,29 @@ __device__ __forceinline__ void roll2_core(const F32Params& P, T x0, T x1, WD wo
   // point -- no clamps there
   const T iaa = vrsq(NH == 1 ? aa : vmaxs(aa, 1e-30f));
   const T ir = vrsq(NH == 1 ? s2 : vmaxs(s2, 1e-30f));
-  // max chain: the largest centred whitened disk
+  // max chain: the largest centred whitened disk, in its difference forms
+  //   outer: q / (|Ax| + sqrt(|Ax|^2 + q)) = sqrt(|Ax|^2 + q) - |Ax|,  q = R^2 - |x|^2
+  //   hole:  q / (|Ax| + sqrt(|Ax|^2 - m2 q)) = (|Ax| - sqrt(|Ax|^2 - m2 q)) / m2,
+  //          q = |x|^2 - rho^2
+  // (no reciprocal: two MUFU ops instead of three, five fewer operations than
+  // the quotient forms).  The differences cancel near a boundary, but the
+  // centred disk is only USED far from both (otherwise z lies in a rolling /
+  // hole-tangent disk): there its radius is >= ~the rolling radius and the
+  // absolute error of a difference -- bounded by shrink_c, which the plan
+  // derives from the MUFU error bounds and max |A| R -- is a ~1e-5 relative
+  // shrink.  |Ax| = aa * rsqrt(aa), folded into the fmas.
   T rm;
   const T qo = vfma(s2, -1.0f, P.oR2);
   if (NH == 0) {
-    const T den = vfma(aa, iaa, vsqrt(vmaxs(vadd(aa, qo), 0.0f)));  // |Ax| + root
-    rm = vfma(vmul(qo, vrcp(den)), P.keep, -P.shrink_abs);
+    const T ro = vfma(vneg(aa), iaa, vsqrt(vmaxs(vadd(aa, qo), 0.0f)));
+    rm = vfma(ro, P.keep, -P.shrink_c);
   } else {
-    // min(qo / Do, qh / Dh) with one reciprocal: min(qo Dh, qh Do) / (Do Dh)
-    const T Do = vfma(aa, iaa, vsqrt(vadd(aa, qo)));  // |Ax| + root, |Ax| = aa / sqrt(aa)
+    const T ro = vfma(vneg(aa), iaa, vsqrt(vadd(aa, qo)));
     const T qh = vadd(s2, -P.hr2[0]);
-    const T Dh = vfma(aa, iaa, vsqrt(vfma(qh, -P.m2, aa)));
-    const T mn = vmin(vmul(qo, Dh), vmul(qh, Do));
-    rm = vfma(vmul(mn, vrcp(vmul(Do, Dh))), P.keep, -P.shrink_abs);
+    const T rh_ = vmul(vfma(aa, iaa, vneg(vsqrt(vfma(qh, -P.m2, aa)))), P.im2);
+    rm = vfma(vmin(ro, rh_), P.keep, -P.shrink_c);
   }
-  const float rb = P.rho_b, rb2 = P.rho_b2, rh = P.rho_h, rh2 = P.rho_h2;
+  const float rb = P.rho_b, rb2 = P.rho_b2, rh = P.rho_h;
   T w0, w1, d2, rho;
   auto use = vlt(s2, s2);  // (type only)
   if (NH == 1) {
@@ -1145,15 +1153,20 @@ __device__ __forceinline__ void roll2_core(const F32Params& P, T x0, T x1, WD wo
     // Any disk containing z inside the domain is a valid step; this choice
     // matches trying the outer disk first and then the hole's (same steps
     // per walk on cfg3), at one disk's cost instead of two.
-    const auto outer = vgt(s2, P.mid2);
-    const T rc = vsel(outer, rb, rh), rc2 = vsel(outer, rb2, rh2);
-    const T bs = vsel(outer, rb, -rh);  // signed radius: inward from the outer circle
-    const T al = vfma(vsel(outer, -P.oR, -P.hr[0]), ir, 1.0f);
-    const T be = vmul(bs, iaa);
+    // The choice enters as a 0/1 blend factor, so the four constants it
+    // picks are fmas (packed: one instruction for both walks) instead of
+    // selects: radius rc = rh + of (rb - rh) -- exact: the plan rounds rb so
+    // that fl(rh + rc_d) == rho_b -- side sign sg = 2 of - 1, and minus the
+    // tangent circle's radius nr = -hr + of (hr - R).
+    const T of = vsel(vgt(s2, P.mid2), 1.0f, 0.0f);
+    const T rc = vfma(of, P.rc_d, rh);
+    const T sg = vfma(of, 2.0f, -1.0f);  // +1: inward from the outer circle, -1: outward from the hole
+    const T al = vfma(vfma(of, P.nr_d, -P.hr[0]), ir, 1.0f);
+    const T be = vmul(vmul(rc, iaa), sg);
     w0 = vmul(x0, vfma(al, P.ia[0], vmul(be, P.Ad[0])));
     w1 = vmul(x1, vfma(al, P.ia[1], vmul(be, P.Ad[1])));
     d2 = vfma(w0, w0, vmul(w1, w1));
-    use = vand(vlt(d2, rc2), vgt(vmul(vfma(al, s2, vmul(be, aa)), bs), 0.0f));
+    use = vand(vlt(d2, vmul(rc, rc)), vgt(vmul(vfma(al, s2, vmul(be, aa)), sg), 0.0f));
     rho = vsel(use, rc, rm);
   } else {
     const T al = vfma(ir, -P.oR, 1.0f);
@@ -1164,9 +1177,10 @@ __device__ __forceinline__ void roll2_core(const F32Params& P, T x0, T x1, WD wo
     use = vand(vlt(d2, rb2), vgt(vfma(al, s2, vmul(be, aa)), 0.0f));
     rho = vsel(use, rb, rm);
   }
-  const T id = vrsq(vmaxs(d2, 1e-30f));
-  const T d = vsel(use, vmul(d2, id), 0.0f);
-  const T e0 = vsel(use, vmul(w0, id), 1.0f), e1 = vsel(use, vmul(w1, id), 0.0f);
+  // the centred disk is the d = 0 case: 1 / d masked once, axis (1, 0)
+  const T id = vsel(use, vrsq(vmaxs(d2, 1e-30f)), 0.0f);
+  const T d = vmul(d2, id);
+  const T e0 = vsel(use, vmul(w0, id), 1.0f), e1 = vmul(w1, id);
   const T m = vsub(rho, d);
   // Moebius: psi uniform in [-pi/2, pi/2) from the low 23 bits (one LOP3)
   const T psi = vfma(vbits23(word, one_bits), kPi, -1.5f * kPi);

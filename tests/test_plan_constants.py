@@ -160,6 +160,36 @@ def test_annulus_disk_radii(B):
             assert (xr <= R * (1 + 1e-7)).all() and (xr >= rho * (1 - 1e-7)).all()
 
 
+def test_rolling_disk_blend_and_difference_constants(B):
+    """roll2_core's blend constants reproduce the radii exactly and its
+    centred-radius margin covers the error bound of the difference forms:
+    fl(rho_h + rc_d) == rho_b, nr_d == rho - R, im2 <= 1 / m2, shrink_c >=
+    shrink_abs + 5e-7 max|A| R max(1, 1/m2); the plain stop thresholds equal
+    the FFMA.SAT ones (bias / scale, exact: the scales are powers of two).
+    An anisotropy whose rolling radius is far below the hole-tangent one
+    (rho_b << rho_h) keeps the exact blend."""
+    from paper_2409_03686_b200 import configs
+    from paper_2409_03686_b200.conductivity import make_tensor
+
+    cfg = configs.get(3)
+    for kmat in (None, np.diag([1.0, 400.0]), np.array([[3.0, 1.2], [1.2, 0.9]])):
+        if kmat is not None:
+            cfg.kt = make_tensor(kmat)
+        c = lambda name: np.float32(_const(B, cfg, "tangent", name)[0])
+        rb, rh, rcd = c("rho_b"), c("rho_h"), c("rc_d")
+        assert np.float32(rh + rcd) == rb and rb <= rh
+        assert c("nr_d") == np.float32(np.float32(0.5) - np.float32(1.0))
+        m2 = c("m2")
+        assert 0 < c("im2") <= np.float32(1.0) / m2
+        ad = np.sqrt(np.linalg.eigvalsh(cfg.kt.k_sqrt @ cfg.kt.k_sqrt))
+        bound = 5e-7 * max(ad.max(), 1.0) * 1.0 * max(1.0, float(c("im2")))
+        assert float(c("shrink_c")) >= float(c("shrink_abs")) + bound * (1 - 1e-3)
+        assert c("s2_hi") == np.float32(c("s2_bias") / c("s2_scale"))
+        assert c("s2_lo") == np.float32(-c("h2_bias") / c("h2_scale"))
+        assert c("s2_hi") == np.float32((1.0 - cfg.eps) ** 2)
+        assert c("s2_lo") == np.float32((0.5 + cfg.eps) ** 2)
+
+
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
 def test_stop_thresholds_are_exact(B, idx):
     """The FFMA.SAT stop tests: stop_scale is a power of two with (e - eps)
