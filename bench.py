@@ -54,7 +54,7 @@ F_STEP = {
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
     (2, "tangent"): (37, 3),                     # tangent balls in the whitened parallelogram
     (3, "woe"): (19, 4), (3, "max"): (29, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
-    (3, "tangent"): (53.4, 6.35),                # one rolling / hole-tangent disk, else centred
+    (3, "tangent"): (49.9, 6.2),                 # one rolling / hole-tangent disk, else centred (difference form)
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
     (4, "tangent"): (79.3, 8.25),                # rolling balls, else the centred ball
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
@@ -569,6 +569,7 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write)",
                        "counts": "int64 (n_poles, n0+n1) rows + step stats",
                        "scheduler": plan.last_scheduler(),
+                       "walks_per_lane": plan.last_walks_per_lane(),
                        "build": _native.build_info()},
             "roofline": {"bound": "fp32_issue", "achieved": achieved, "peak": peak_nominal,
                          "unit": "Top/s", "frac": achieved / peak_nominal,

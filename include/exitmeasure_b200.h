@@ -152,6 +152,10 @@ typedef struct {
  * kernel's bit for bit.  This flag forces the one-walk-per-lane kernel
  * (A/B measurements, the equality test). */
 #define EM_FLAG_ONE_WALK_PER_LANE 8
+/* By default the packed kernel runs where it exists once a run has >= 2e6
+ * walks (smaller jobs restart its two slots per lane less evenly and run the
+ * one-walk kernel).  This flag runs it at every size (tests). */
+#define EM_FLAG_TWO_WALKS_PER_LANE 16
 
 /* Per-run outputs.  Host pointers for em_plan_run / em_run_accumulate,
  * device pointers for em_plan_run_device.  counts is (n_poles, n0 + n1)
@@ -246,6 +250,8 @@ int em_plan_last_scheduler(const em_plan* p);
 /* walks per lane of the plan's integer-count kernel: 2 where the packed
  * two-walks-per-lane kernel runs (EM_FLAG_ONE_WALK_PER_LANE forces 1) */
 int em_plan_walks_per_lane(const em_plan* p);
+/* walks per lane of the last integer-count run (1 or 2; 0 before any run) */
+int em_plan_last_walks_per_lane(const em_plan* p);
 /* the walk chain the plan runs (EM_CHAIN_*): EM_CHAIN_TANGENT falls back to
  * EM_CHAIN_MAX where no tangent-ball step exists for the geometry */
 int em_plan_chain(const em_plan* p);

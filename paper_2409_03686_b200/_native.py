@@ -42,6 +42,7 @@ EM_FLAG_TANGENT_ON_IDENTITY = 1
 EM_FLAG_PERSISTENT = 2
 EM_FLAG_POLE_BLOCKS = 4
 EM_FLAG_ONE_WALK_PER_LANE = 8
+EM_FLAG_TWO_WALKS_PER_LANE = 16
 
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
@@ -121,6 +122,7 @@ def lib():
         "em_plan_n_bins": ([_p, ctypes.c_int], _i64),
         "em_plan_last_scheduler": ([_p], ctypes.c_int),
         "em_plan_walks_per_lane": ([_p], ctypes.c_int),
+        "em_plan_last_walks_per_lane": ([_p], ctypes.c_int),
         "em_run_accumulate": ([ctypes.POINTER(EmGeometry), ctypes.POINTER(EmSide),
                                ctypes.POINTER(EmSide), _p, _p, _i64, _u64, _dbl, _i64, _i64,
                                ctypes.POINTER(EmOptions), ctypes.POINTER(EmOutputs)],

@@ -539,6 +539,11 @@ class Plan:
         """2 where counts run on the packed two-walks-per-lane kernel."""
         return int(N.lib().em_plan_walks_per_lane(self._h))
 
+    def last_walks_per_lane(self) -> int:
+        """Walks per lane of the last integer-count run (small runs take the
+        one-walk kernel unless EM_FLAG_TWO_WALKS_PER_LANE)."""
+        return int(N.lib().em_plan_last_walks_per_lane(self._h))
+
     def last_launches(self) -> int:
         v = ctypes.c_int64(0)
         N.lib().em_plan_last_launches(self._h, ctypes.byref(v))

@@ -22,6 +22,20 @@
 
 #include "em_params.cuh"
 
+// chunks per resident warp the chunk size aims at on the packed kernel
+#ifndef EM_X2_CHUNKS
+#define EM_X2_CHUNKS 8.0
+#endif
+// per-lane step statistics flush three atomics per pole change; spread over
+// copies while copies x chunk x poles is below this many walks (measured on
+// cfg2: 131072 -> 524288 is +9% on the one-walk kernel, +17% on the packed one)
+#ifndef EM_STAT_SPREAD
+#define EM_STAT_SPREAD 524288.0
+#endif
+#ifndef EM_X1_CHUNKS
+#define EM_X1_CHUNKS 8.0
+#endif
+
 namespace em {
 cudaError_t launch_ref64(const Ref64Params& P, int mode, int grid, int block, cudaStream_t s);
 cudaError_t launch_f32(const F32Params& P, int d, int outer, int nh_mode, int mode, int chain,
@@ -48,9 +62,9 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
 bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink);
 // two walks per lane, packed FP32 arithmetic (walk_f32x2.cu)
 bool f32x2_available(int d, int outer, int nh_mode, int chain, bool ident);
-cudaError_t f32x2_blocks_per_sm(int nh_mode, int bink, int* nb);
-cudaError_t launch_f32x2(const F32Params& P, int nh_mode, int bink, int grid, int block,
-                         cudaStream_t s);
+cudaError_t f32x2_blocks_per_sm(int outer, int nh_mode, int bink, int* nb);
+cudaError_t launch_f32x2(const F32Params& P, int outer, int nh_mode, int bink, int grid,
+                         int block, cudaStream_t s);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
 cudaError_t launch_philox32_kat(const unsigned* in, unsigned* out, int n, cudaStream_t s);
@@ -288,6 +302,7 @@ struct em_plan {
   bool pack2 = false;        // counts mode runs two walks per lane (walk_f32x2.cu)
   int grid2 = 0;             // its persistent grid
   int last_sched = -1;       // scheduler of the last integer-count launch
+  int last_lanes = 0;        // walks per lane of the last integer-count launch
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
@@ -787,13 +802,21 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     int nb2 = 0;
     if (!(o.flags & EM_FLAG_ONE_WALK_PER_LANE) && p->block == 256 &&
         f32x2_available(p->d, p->outer, p->nh_mode, p->chain, p->ident) &&
-        f32x2_blocks_per_sm(p->nh_mode, p->bink, &nb2) == cudaSuccess && nb2 > 0) {
+        f32x2_blocks_per_sm(p->outer, p->nh_mode, p->bink, &nb2) == cudaSuccess && nb2 > 0) {
       p->pack2 = true;
       p->grid2 = o.grid > 0 ? o.grid : sm_count_of(o.device) * nb2;
     }
   }
   *out = p;
   return EM_OK;
+}
+
+// The packed kernel pays off once every slot walks a few walks in a row (two
+// slots per lane restart less evenly on tiny jobs: cfg3 at 1e6 walks -12%, at
+// 1e7 walks +8%); counts are identical either way.  EM_FLAG_TWO_WALKS_PER_LANE
+// forces it (tests of the small-job paths).
+static bool use_pack2(const em_plan* p, int64_t total) {
+  return (p->flags & EM_FLAG_TWO_WALKS_PER_LANE) || total >= 2000000;
 }
 
 static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_rep, int mode,
@@ -814,10 +837,10 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   w->total = total;
   // chunk size: enough chunks for ~8 per resident warp, 32..2048 replicates
   {
-    const bool x2 = p->pack2 && mode == 0;
+    const bool x2 = p->pack2 && mode == 0 && use_pack2(p, total);
     const double warps = (double)(x2 ? p->grid2 : p->grid) * (p->block / 32);
     long long rb = 32;
-    while (rb < 2048 && (double)total / (warps * 8.0) >= (double)(rb * 2)) rb *= 2;
+    while (rb < 2048 && (double)total / (warps * (x2 ? EM_X2_CHUNKS : EM_X1_CHUNKS)) >= (double)(rb * 2)) rb *= 2;
     w->rb = rb;
     w->n_chunks = (unsigned long long)p->n_poles * (unsigned long long)((n_rep + rb - 1) / rb);
     // minimum chunks (tiny jobs: ~1 walk per lane per chunk) mean a pole
@@ -862,7 +885,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
     w->stat_copies = 1;
     if (p->precision == EM_PREC_FP32 && mode == 0 && w->smem_stats == 0) {
       int c = 1;
-      while (c < 64 && (double)c * (double)rb * (double)p->n_poles < 131072.0) c *= 2;
+      while (c < 64 && (double)c * (double)rb * (double)p->n_poles < EM_STAT_SPREAD) c *= 2;
       w->stat_copies = c;
     }
   }
@@ -915,7 +938,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   }
   p->last_timed = false;
   if (total > 0) {
-    const bool x2 = p->pack2 && mode == 0;
+    const bool x2 = p->pack2 && mode == 0 && use_pack2(p, total);
     const int64_t lanes_needed = x2 ? (total + 63) / 64 * 32 : (total + 31) / 32 * 32;
     int grid = x2 ? p->grid2 : p->grid;
     const int64_t blocks_needed = (lanes_needed + p->block - 1) / p->block;
@@ -932,7 +955,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
       p->p32.key1 = (unsigned)(seed >> 32);
       p->p32.rk = philox32_schedule(p->p32.key0, p->p32.key1);
       if (x2)
-        e = launch_f32x2(p->p32, p->nh_mode, p->bink, grid, p->block, s);
+        e = launch_f32x2(p->p32, p->outer, p->nh_mode, p->bink, grid, p->block, s);
       else
         e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, p->bink,
                        grid, p->block, s);
@@ -950,6 +973,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
   p->last_launches = launches;
   p->last_walks = total;
   if (mode == 0) p->last_sched = w->smem_stats;
+  if (mode == 0) p->last_lanes = (p->pack2 && use_pack2(p, total)) ? 2 : 1;
   p->last_launch_stream = s;
   return EM_OK;
 }
@@ -1145,6 +1169,7 @@ int em_plan_last_launches(const em_plan* p, int64_t* launches) {
 
 int em_plan_last_scheduler(const em_plan* p) { return p ? p->last_sched : -1; }
 int em_plan_walks_per_lane(const em_plan* p) { return p ? (p->pack2 ? 2 : 1) : -1; }
+int em_plan_last_walks_per_lane(const em_plan* p) { return p ? p->last_lanes : -1; }
 
 int64_t em_plan_n_bins(const em_plan* p, int side) {
   if (!p) return -1;

@@ -704,38 +704,10 @@ struct Tangent {
 // One tangent-ball step from x: the 0/1 walking mask (sat of the Euclidean
 // stop margin, as everywhere) and the candidate next point n0, n1.  The
 // caller keeps x for lanes that do not walk (stopped, idle: their candidate
-// is not meaningful).  word: 32 random bits for psi.
+// is not meaningful).  word: 32 random bits for psi.  Defined below, after
+// the one-tree value operations (tang2_core).
 __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x, unsigned word,
-                                              unsigned one_bits, float& n0, float& n1) {
-  const float a0 = fabsf(x[0]), a1 = fabsf(x[1]);
-  const float m0 = P.tbt[0] - a0, m1 = P.tbt[1] - a1;
-  const float wm = __saturatef(fminf(P.tsb[0] - a0, P.tsb[1] - a1) * P.ss_scale);
-  const bool p0 = m0 <= m1;  // nearest face: axis 0
-  const float m = fminf(m0, m1);
-  const float xi = p0 ? x[0] : x[1], xj = p0 ? x[1] : x[0];
-  const float bti = p0 ? P.tbt[0] : P.tbt[1], btj = p0 ? P.tbt[1] : P.tbt[0];
-  // work in the frame mirrored by s = sign xt_i (s xt_j, faces j at -+bt_j
-  // swap roles), where the foot is fs = s xt_j + m c and the two face-j
-  // limits are (bt_j - fs) / (1 - c) and (bt_j + fs) / (1 + c): no selects
-  const float sg = copysignf(1.0f, xi);                    // s
-  const float fj = fmaf(m, P.tcd, sg * xj);                // s * foot_j
-  float rho = fminf(bti, fminf((btj - fj) * P.tim, (btj + fj) * P.tip));
-  rho = fmaf(fmaxf(rho, m), P.tkeep, -P.tsa);
-  // psi uniform in [-pi/2, pi/2): the low 23 bits into the mantissa of 1.0f
-  // (one LOP3: (word & 0x7fffff) | one_bits)
-  const float psi = fmaf(__uint_as_float(one_bits | (word & 0x7fffffu)), kPi, -1.5f * kPi);
-  float sn, cs;
-  psi_sincos(psi, &sn, &cs);
-  const float N = m * sn, Dd = fmaf(2.0f, rho, -m) * cs;
-  const float NN = N * N;
-  const float g = fdiv(rho + rho, fmaf(Dd, Dd, NN));
-  const float dep = g * NN, off = g * N * Dd;              // depth below face i, offset along it
-  const float ni = sg * (bti - dep);  // may lie past the centre line: no copysign
-  const float nj = sg * fmaf(off, P.tsd, fmaf(-dep, P.tcd, fj));
-  n0 = p0 ? ni : nj;
-  n1 = p0 ? nj : ni;
-  return wm;
-}
+                                              unsigned one_bits, float& n0, float& n1);
 
 // 3D box / L-box on tangent balls, same stored coordinates xt_i = a_i . z
 // (F32Params::t3 holds the per-face constants, T below is face i's row in
@@ -1211,6 +1183,64 @@ __device__ __forceinline__ float roll_step2(const F32Params& P, const float* x, 
 #else
   return roll_step2_legacy<NH>(P, x, word, one_bits, nx);
 #endif
+}
+
+// ---- 2D box on the tangent-ball chain, same one-tree form ----
+__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+__device__ __forceinline__ float2 vabs(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+__device__ __forceinline__ float vsign1(float a) { return copysignf(1.0f, a); }
+__device__ __forceinline__ float2 vsign1(float2 a) {
+  return make_float2(copysignf(1.0f, a.x), copysignf(1.0f, a.y));
+}
+__device__ __forceinline__ bool vle(float a, float b) { return a <= b; }
+__device__ __forceinline__ Mask2 vle(float2 a, float2 b) { return {a.x <= b.x, a.y <= b.y}; }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float2 vmax(float2 a, float2 b) {
+  return make_float2(fmaxf(a.x, b.x), fmaxf(a.y, b.y));
+}
+__device__ __forceinline__ float2 vmin(float2 a, float s) {
+  return make_float2(fminf(a.x, s), fminf(a.y, s));
+}
+
+// The tangent-ball step of the whitened parallelogram (comment above
+// tangent_step): |xt_0|, |xt_1| out (the stop tests read them), candidate
+// next point (n0, n1).
+template <class T, class WD>
+__device__ __forceinline__ void tang2_core(const F32Params& P, T x0, T x1, WD word,
+                                           unsigned one_bits, T& a0, T& a1, T& n0, T& n1) {
+  a0 = vabs(x0);
+  a1 = vabs(x1);
+  const T m0 = vfma(a0, -1.0f, P.tbt[0]), m1 = vfma(a1, -1.0f, P.tbt[1]);
+  const auto p0 = vle(m0, m1);  // nearest face: axis 0
+  const T m = vmin(m0, m1);
+  const T xi = vsel(p0, x0, x1), xj = vsel(p0, x1, x0);
+  const T bti = vsel(p0, P.tbt[0], P.tbt[1]), btj = vsel(p0, P.tbt[1], P.tbt[0]);
+  // work in the frame mirrored by s = sign xt_i (s xt_j, faces j at -+bt_j
+  // swap roles), where the foot is fs = s xt_j + m c and the two face-j
+  // limits are (bt_j - fs) / (1 - c) and (bt_j + fs) / (1 + c): no selects
+  const T sg = vsign1(xi);
+  const T fj = vfma(m, P.tcd, vmul(sg, xj));  // s * foot_j
+  T rho = vmin(bti, vmin(vmul(vsub(btj, fj), P.tim), vmul(vadd(btj, fj), P.tip)));
+  rho = vfma(vmax(rho, m), P.tkeep, -P.tsa);
+  // psi uniform in [-pi/2, pi/2): the low 23 bits into the mantissa of 1.0f
+  const T psi = vfma(vbits23(word, one_bits), kPi, -1.5f * kPi);
+  T sn, cs;
+  vsincos(psi, sn, cs);
+  const T N = vmul(m, sn), Dd = vmul(vfma(rho, 2.0f, vneg(m)), cs);
+  const T NN = vmul(N, N);
+  const T g = vmul(vadd(rho, rho), vrcp(vfma(Dd, Dd, NN)));
+  const T dep = vmul(g, NN), off = vmul(vmul(g, N), Dd);  // depth below face i, offset along it
+  const T ni = vmul(sg, vfma(vneg(g), NN, bti));  // s (bt_i - depth); may pass the centre line
+  const T nj = vmul(sg, vfma(off, P.tsd, vfma(vneg(dep), P.tcd, fj)));
+  n0 = vsel(p0, ni, nj);
+  n1 = vsel(p0, nj, ni);
+}
+
+__device__ __forceinline__ float tangent_step(const F32Params& P, const float* x, unsigned word,
+                                              unsigned one_bits, float& n0, float& n1) {
+  float a0, a1;
+  tang2_core<float, unsigned>(P, x[0], x[1], word, one_bits, a0, a1, n0, n1);
+  return __saturatef(fminf(P.tsb[0] - a0, P.tsb[1] - a1) * P.ss_scale);
 }
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>

@@ -12,8 +12,9 @@
 // Same chain, same stop test, same RNG streams (keyed by global pole id and
 // replicate index) and the same operation tree as the one-walk-per-lane
 // kernel (walk_f32.cu), so a walk does not depend on which kernel or slot
-// runs it.  Built for the 2D ball on the rolling-disk chain with no hole or
-// one concentric hole (cfg3, the headline; walk_f32_dev.cuh roll_step2).
+// runs it.  Built for the 2D tangent chains: the ball on rolling disks with
+// no hole or one concentric hole (cfg3, the headline; roll2_core) and the box
+// on tangent balls (cfg2; tang2_core), both in walk_f32_dev.cuh.
 #include "walk_f32_dev.cuh"
 
 // resident 256-thread blocks per SM: 4 (64 registers, a few spilled words in
@@ -35,6 +36,29 @@ __device__ __forceinline__ Mask2 walking2(const F32Params& P, float2 s2) {
   return g;
 }
 
+// CH: 0 = ball, no hole; 1 = ball, one concentric hole (rolling disks); 2 =
+// box (tangent balls).  One step of both walks: candidate points and the
+// walking masks of the CURRENT points.
+template <int CH>
+__device__ __forceinline__ Mask2 step2(const F32Params& P, float2 x0, float2 x1, uint2 w,
+                                       float2& n0, float2& n1) {
+  if (CH == 2) {
+    float2 a0, a1;
+    tang2_core<float2, uint2>(P, x0, x1, w, P.one_bits, a0, a1, n0, n1);
+    return vand(vlt(a0, P.tsb[0]), vlt(a1, P.tsb[1]));
+  }
+  float2 s2;
+  roll2_core<CH == 1 ? 1 : 0, float2, uint2>(P, x0, x1, w, P.one_bits, s2, n0, n1);
+  return walking2<CH == 1 ? 1 : 0>(P, s2);
+}
+
+// the walking masks alone (post-batch stop test)
+template <int CH>
+__device__ __forceinline__ Mask2 walking_at(const F32Params& P, float2 x0, float2 x1) {
+  if (CH == 2) return vand(vlt(vabs(x0), P.tsb[0]), vlt(vabs(x1), P.tsb[1]));
+  return walking2<CH == 1 ? 1 : 0>(P, roll2_s2(x0, x1));
+}
+
 // Per-warp exit queue as four word arrays (x, y, pole, steps): a lane's two
 // walks keep each AXIS as one register pair, so a slot's (x, y) are not
 // adjacent registers and a 128-bit store would cost moves every batch.
@@ -47,11 +71,13 @@ __device__ __forceinline__ float& comp(float2& v, int t) { return t ? v.y : v.x;
 
 // Two walks per lane: slot t of a lane owns component t of every float2.
 // Scheduling, exit queue, binning and statistics as walk_f32_kernel (MODE 0).
-template <int NH, int BINK, int SMEM>
+template <int CH, int BINK, int SMEM>
 __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32Params P) {
   const WorkOut& W = P.w;
   constexpr int D = 2;
-  constexpr int OUTER = OUTER_BALL;
+  constexpr int OUTER = CH == 2 ? OUTER_BOX : OUTER_BALL;
+  constexpr int NH = CH == 1 ? 1 : 0;
+  constexpr bool SCALED = CH == 2;  // box axes stored scaled (to_frame)
   __shared__ ExitQueue2 q_all[kWarps];
   int lane = threadIdx.x & 31;
   unsigned eq = 1u << lane, lt = eq - 1u;
@@ -128,7 +154,7 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(ex[1]) : "r"(qa + kQueue * 4u) : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ep) : "r"(qa + kQueue * 8u) : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qa + kQueue * 12u) : "memory");
-            retire<D, OUTER, NH, BINK, SMEM, false>(P, ex, ep, es, acc);
+            retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, ep, es, acc);
             qn -= 32;
             __syncwarp();
           }
@@ -192,27 +218,23 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
       Mask2 go = {false, false};
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float2 s2, n0, n1;
-        roll2_core<NH, float2, uint2>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), P.one_bits, s2,
-                                      n0, n1);
-        go = walking2<NH>(P, s2);
+        float2 n0, n1;
+        go = step2<CH>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), n0, n1);
         x0 = vsel(go, n0, x0);
         x1 = vsel(go, n1, x1);
         steps[0] += go.x;
         steps[1] += go.y;
       }
       // post-batch stop test of the landing point (walk_f32_kernel: EM_POST_STOP)
-      const Mask2 g2 = walking2<NH>(P, roll2_s2(x0, x1));
+      const Mask2 g2 = walking_at<CH>(P, x0, x1);
       walking[0] = go.x & g2.x;
       walking[1] = go.y & g2.y;
     } else {
       int failed[2] = {0, 0};
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float2 s2, n0, n1;
-        roll2_core<NH, float2, uint2>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), P.one_bits, s2,
-                                      n0, n1);
-        const Mask2 gk = walking2<NH>(P, s2);
+        float2 n0, n1;
+        const Mask2 gk = step2<CH>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), n0, n1);
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           const int stop = walking[t] & !(t ? gk.y : gk.x);
@@ -249,7 +271,7 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
   if (lane < qn) {  // drain the queue
     const ExitQueue2& q = q_all[threadIdx.x >> 5];
     const float ex[3] = {q.x[lane], q.y[lane], 0.0f};
-    retire<D, OUTER, NH, BINK, SMEM, false, false>(P, ex, q.p[lane], q.s[lane], acc);
+    retire<D, OUTER, NH, BINK, SMEM, SCALED, false>(P, ex, q.p[lane], q.s[lane], acc);
   }
   if (SMEM == 2) {
     unsigned long long sm = acc.sum, sq = acc.sq, mx = acc.mx;
@@ -293,36 +315,49 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
 
 using F32Kernel = void (*)(F32Params);
 
-static F32Kernel pick_f32x2(int nh_mode, int bink, int smem) {
+// ch: 0 / 1 = ball without / with one concentric hole, 2 = box
+static F32Kernel pick_f32x2(int ch, int bink, int smem) {
   using namespace f32;
-  if (smem == 2) {
-    if (bink != BIN_CIRCLE) return nullptr;
-    return nh_mode == 0 ? walk_f32x2_kernel<0, BIN_CIRCLE, 2> : walk_f32x2_kernel<1, BIN_CIRCLE, 2>;
+#define EM_X2_SCHED(CH_, BK_)                                                     \
+  (smem == 2 ? walk_f32x2_kernel<CH_, BK_, 2>                                      \
+             : (smem ? walk_f32x2_kernel<CH_, BK_, 1> : walk_f32x2_kernel<CH_, BK_, 0>))
+#define EM_X2_ANY(CH_)                                                            \
+  (smem == 2 ? (F32Kernel) nullptr                                                 \
+             : (smem ? walk_f32x2_kernel<CH_, BIN_ANY, 1> : walk_f32x2_kernel<CH_, BIN_ANY, 0>))
+  if (ch == 2) {
+    if (bink == BIN_SQUARE) return EM_X2_SCHED(2, BIN_SQUARE);
+    if (bink == BIN_GRID) return EM_X2_SCHED(2, BIN_GRID);
+    return EM_X2_ANY(2);
   }
-  if (bink == BIN_CIRCLE) {
-    if (nh_mode == 0) return smem ? walk_f32x2_kernel<0, BIN_CIRCLE, 1> : walk_f32x2_kernel<0, BIN_CIRCLE, 0>;
-    return smem ? walk_f32x2_kernel<1, BIN_CIRCLE, 1> : walk_f32x2_kernel<1, BIN_CIRCLE, 0>;
-  }
-  if (nh_mode == 0) return smem ? walk_f32x2_kernel<0, BIN_ANY, 1> : walk_f32x2_kernel<0, BIN_ANY, 0>;
-  return smem ? walk_f32x2_kernel<1, BIN_ANY, 1> : walk_f32x2_kernel<1, BIN_ANY, 0>;
+  if (bink == BIN_CIRCLE) return ch == 0 ? EM_X2_SCHED(0, BIN_CIRCLE) : EM_X2_SCHED(1, BIN_CIRCLE);
+  return ch == 0 ? EM_X2_ANY(0) : EM_X2_ANY(1);
+#undef EM_X2_SCHED
+#undef EM_X2_ANY
+}
+
+static int x2_family(int d, int outer, int nh_mode, int chain, bool ident) {
+  if (!EM_ROLL2_GENERIC || d != 2 || chain != EM_CHAIN_TANGENT || ident) return -1;
+  if (outer == OUTER_BALL && nh_mode <= 1) return nh_mode;
+  if (outer == OUTER_BOX && nh_mode == 0) return 2;
+  return -1;
 }
 
 // The packed kernel exists for this plan's family (counts mode only).
 bool f32x2_available(int d, int outer, int nh_mode, int chain, bool ident) {
-  return d == 2 && outer == OUTER_BALL && nh_mode <= 1 && chain == EM_CHAIN_TANGENT && !ident;
+  return x2_family(d, outer, nh_mode, chain, ident) >= 0;
 }
 
-cudaError_t f32x2_blocks_per_sm(int nh_mode, int bink, int* nb) {
-  F32Kernel k = pick_f32x2(nh_mode, bink, 0);
+cudaError_t f32x2_blocks_per_sm(int outer, int nh_mode, int bink, int* nb) {
+  F32Kernel k = pick_f32x2(outer == OUTER_BOX ? 2 : nh_mode, bink, 0);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
 }
 
-cudaError_t launch_f32x2(const F32Params& P, int nh_mode, int bink, int grid, int block,
-                         cudaStream_t s) {
+cudaError_t launch_f32x2(const F32Params& P, int outer, int nh_mode, int bink, int grid,
+                         int block, cudaStream_t s) {
   if (block != 32 * f32::kWarps) return cudaErrorInvalidConfiguration;
   const int sched = P.w.smem_stats;
-  F32Kernel k = pick_f32x2(nh_mode, bink, sched);
+  F32Kernel k = pick_f32x2(outer == OUTER_BOX ? 2 : nh_mode, bink, sched);
   if (!k) return cudaErrorInvalidValue;
   size_t smem = 0;
   if (sched == 1) smem = (size_t)f32::kWarps * 3 * P.w.n_poles * 8;

@@ -33,7 +33,9 @@ def _plans(B, cfg, pole_ids=None, max_steps=10**6, sched=0):
     s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
     mk = lambda fl: B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, max_steps, s0, s1,
                            precision="fp32", pole_ids=pole_ids, flags=fl | sched)
-    return mk(0), mk(_native.EM_FLAG_ONE_WALK_PER_LANE)
+    # the packed kernel at every size (by default runs below 2e6 walks take
+    # the one-walk kernel) against the one-walk kernel
+    return mk(_native.EM_FLAG_TWO_WALKS_PER_LANE), mk(_native.EM_FLAG_ONE_WALK_PER_LANE)
 
 
 def _same(a, b):
@@ -52,8 +54,78 @@ def test_packed_equals_one_walk_per_lane_cfg3(B, n_poles, n_rep):
     with p2, p1:
         assert p2.walks_per_lane() == 2 and p1.walks_per_lane() == 1
         r2, r1 = p2.run(cfg.seed, n_rep), p1.run(cfg.seed, n_rep)
+        assert p2.last_walks_per_lane() == 2 and p1.last_walks_per_lane() == 1
     assert np.array_equal(r2.counts.sum(1), np.full(cfg.n_poles, n_rep))
     _same(r2, r1)
+
+
+def test_default_kernel_follows_job_size(B):
+    """Default flags: runs of >= 2e6 walks take the packed kernel, smaller
+    ones the one-walk kernel (identical counts either way)."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(3).subset(64)
+    geom = B.pack_geometry(cfg.dom)
+    s0 = B.pack_side(cfg.fam0, cfg.d, cfg.eps)
+    s1 = B.pack_side(cfg.fam1, cfg.d, cfg.eps)
+    with B.Plan(geom, cfg.kt.k_sqrt, cfg.poles, cfg.eps, 10**6, s0, s1, precision="fp32") as plan:
+        assert plan.walks_per_lane() == 2
+        plan.run(cfg.seed, 1000)
+        assert plan.last_walks_per_lane() == 1
+        plan.run(cfg.seed, 40_000)
+        assert plan.last_walks_per_lane() == 2
+    cfg4 = configs.get(4).subset(8)
+    with B.Plan(B.pack_geometry(cfg4.dom), cfg4.kt.k_sqrt, cfg4.poles, cfg4.eps, 10**6,
+                B.pack_side(cfg4.fam0, 3, cfg4.eps), B.pack_side(cfg4.fam1, 3, cfg4.eps),
+                precision="fp32") as plan:
+        assert plan.walks_per_lane() == 1  # no packed kernel for the 3D chains
+
+
+@pytest.mark.parametrize("n_poles,n_rep", [(256, 100_000), (256, 3_000), (5, 77)])
+def test_packed_equals_one_walk_per_lane_cfg2(B, n_poles, n_rep):
+    """The 2D box on tangent balls (tang2_core), square-arc binner."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(2).subset(n_poles)
+    p2, p1 = _plans(B, cfg)
+    with p2, p1:
+        assert p2.walks_per_lane() == 2 and p1.walks_per_lane() == 1
+        r2, r1 = p2.run(cfg.seed, n_rep), p1.run(cfg.seed, n_rep)
+    assert np.array_equal(r2.counts.sum(1), np.full(cfg.n_poles, n_rep))
+    _same(r2, r1)
+
+
+def test_packed_box_off_origin_grid_binner_and_budget(B):
+    """An off-origin rectangle with a strongly anisotropic K and an
+    unstructured anchor family (candidate-grid binner); then a step budget
+    the walks overrun."""
+    from paper_2409_03686_b200 import _native
+    from paper_2409_03686_b200.conductivity import make_tensor
+    from paper_2409_03686_b200.errors import WalkBudgetError
+    from paper_2409_03686_b200.geometry import Box, Domain, generic_points, square_points
+
+    dom = Domain(2, Box(np.array([1.5, -0.25]), 0.75), (), frozenset())
+    kt = make_tensor([[4.0, 1.5], [1.5, 1.0]])
+    pts = square_points(np.array([1.5, -0.25]), 0.75, 200, component=0, phase=0.5).points
+    fam1 = generic_points(pts, component=0)
+    rng = np.random.default_rng(5)
+    poles = np.array([1.5, -0.25]) + rng.uniform(-0.7, 0.7, size=(40, 2))
+    geom = B.pack_geometry(dom)
+    s0 = B.pack_side(None, 2, 1e-5)
+    s1 = B.pack_side(fam1, 2, 1e-5)
+    out = []
+    for fl in (_native.EM_FLAG_TWO_WALKS_PER_LANE, _native.EM_FLAG_ONE_WALK_PER_LANE):
+        with B.Plan(geom, kt.k_sqrt, poles, 1e-5, 10**6, s0, s1, precision="fp32", flags=fl) as plan:
+            out.append((plan.run(11, 30_000), plan.walks_per_lane()))
+    assert out[0][1] == 2 and out[1][1] == 1
+    _same(out[0][0], out[1][0])
+    errs = []
+    for fl in (_native.EM_FLAG_TWO_WALKS_PER_LANE, _native.EM_FLAG_ONE_WALK_PER_LANE):
+        with B.Plan(geom, kt.k_sqrt, poles, 1e-5, 2, s0, s1, precision="fp32", flags=fl) as plan:
+            with pytest.raises(WalkBudgetError) as ei:
+                plan.run(11, 4096)
+            errs.append((ei.value.pole, ei.value.replicate))
+    assert errs[0] == errs[1]
 
 
 def test_packed_equals_one_walk_per_lane_schedulers_shards_offsets(B):
@@ -124,7 +196,7 @@ def test_packed_disc_without_hole_equals_one_walk_per_lane(B):
     s1 = B.pack_side(fam1, 2, cfg.eps)
     poles = 0.8 * cfg.poles[:48]
     out = []
-    for fl in (0, _native.EM_FLAG_ONE_WALK_PER_LANE):
+    for fl in (_native.EM_FLAG_TWO_WALKS_PER_LANE, _native.EM_FLAG_ONE_WALK_PER_LANE):
         with B.Plan(geom, cfg.kt.k_sqrt, poles, cfg.eps, 10**6, s0, s1, precision="fp32",
                     flags=fl) as plan:
             out.append((plan.run(cfg.seed, 50_000), plan.walks_per_lane()))
