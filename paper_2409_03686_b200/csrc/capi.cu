@@ -62,8 +62,8 @@ cudaError_t f32_blocks_per_sm(int d, int outer, int nh_mode, int chain, bool ide
 bool f32_has_pole_blocks(int d, int outer, int nh_mode, int chain, bool ident, int bink);
 // two walks per lane, packed FP32 arithmetic (walk_f32x2.cu)
 bool f32x2_available(int d, int outer, int nh_mode, int chain, bool ident);
-cudaError_t f32x2_blocks_per_sm(int outer, int nh_mode, int bink, int* nb);
-cudaError_t launch_f32x2(const F32Params& P, int outer, int nh_mode, int bink, int grid,
+cudaError_t f32x2_blocks_per_sm(int d, int outer, int nh_mode, int bink, int* nb);
+cudaError_t launch_f32x2(const F32Params& P, int d, int outer, int nh_mode, int bink, int grid,
                          int block, cudaStream_t s);
 cudaError_t launch_philox64_kat(const unsigned long long* in, unsigned long long* out, int n,
                                 cudaStream_t s);
@@ -802,7 +802,7 @@ int em_plan_create(const em_geometry* g, const em_side* s0, const em_side* s1,
     int nb2 = 0;
     if (!(o.flags & EM_FLAG_ONE_WALK_PER_LANE) && p->block == 256 &&
         f32x2_available(p->d, p->outer, p->nh_mode, p->chain, p->ident) &&
-        f32x2_blocks_per_sm(p->outer, p->nh_mode, p->bink, &nb2) == cudaSuccess && nb2 > 0) {
+        f32x2_blocks_per_sm(p->d, p->outer, p->nh_mode, p->bink, &nb2) == cudaSuccess && nb2 > 0) {
       p->pack2 = true;
       p->grid2 = o.grid > 0 ? o.grid : sm_count_of(o.device) * nb2;
     }
@@ -955,7 +955,7 @@ static int plan_launch(em_plan* p, uint64_t seed, int64_t rep_start, int64_t n_r
       p->p32.key1 = (unsigned)(seed >> 32);
       p->p32.rk = philox32_schedule(p->p32.key0, p->p32.key1);
       if (x2)
-        e = launch_f32x2(p->p32, p->outer, p->nh_mode, p->bink, grid, p->block, s);
+        e = launch_f32x2(p->p32, p->d, p->outer, p->nh_mode, p->bink, grid, p->block, s);
       else
         e = launch_f32(p->p32, p->d, p->outer, p->nh_mode, mode, p->chain, p->ident, p->bink,
                        grid, p->block, s);

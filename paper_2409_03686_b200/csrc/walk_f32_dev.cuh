@@ -824,51 +824,7 @@ __device__ __forceinline__ float rsq(float x) {
 }
 
 __device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, unsigned word,
-                                            unsigned one_bits, float* nx) {
-  const float p0 = x[0] * x[0], p1 = x[1] * x[1], p2 = x[2] * x[2];
-  const float s2 = p0 + p1 + p2;
-  const float aa = fmaf(P.Kd[0], p0, fmaf(P.Kd[1], p1, P.Kd[2] * p2));
-  const float wm = __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
-  // clamped: a walk at the exact centre (x = 0) keeps finite terms
-  const float iaa = rsq(fmaxf(aa, 1e-30f));
-  const float sa = aa * iaa;  // |Ax|
-  // max chain: the largest centred whitened ball, r = q / (|Ax| + sqrt(|Ax|^2 + q))
-  const float q = P.oR2 - s2;
-  const float rm = fmaf(fdiv(q, sa + fsqrt(fmaxf(aa + q, 0.0f))), P.keep, -P.shrink_abs);
-  // rolling ball tangent at the radial projection
-  const float al = fmaf(-P.oR, rsq(fmaxf(s2, 1e-30f)), 1.0f);
-  const float be = P.rho_b * iaa;
-  const float w0 = x[0] * fmaf(al, P.ia[0], be * P.Ad[0]);
-  const float w1 = x[1] * fmaf(al, P.ia[1], be * P.Ad[1]);
-  const float w2 = x[2] * fmaf(al, P.ia[2], be * P.Ad[2]);
-  const float d2 = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-  const bool roll = (d2 < P.rho_b2) & (fmaf(al, s2, be * aa) > 0.0f);
-  const float rho = roll ? P.rho_b : rm;
-  const float id = rsq(fmaxf(d2, 1e-30f));
-  const float d = roll ? d2 * id : 0.0f;
-  const float e0 = roll ? w0 * id : 0.0f, e1 = roll ? w1 * id : 0.0f, e2 = roll ? w2 * id : 1.0f;
-  const float m = rho - d;
-  // V2 = 2V from the high half-word, azimuth from the low one
-  const float fv = __uint_as_float(__byte_perm(word, one_bits, 0x7632u));
-  const float v2 = fmaf(fv, 256.0f, -256.0f) + 1.52587890625e-05f;
-  const float g = fdiv(m, fmaf(d, v2, m));
-  const float dep = (g * g) * ((2.0f - v2) * fmaf(0.5f * d, v2, rho));
-  const float tr = fsqrt(fmaxf(dep * fmaf(2.0f, rho, -dep), 0.0f));
-  float sn, cs;
-  __sincosf(angle_of(__byte_perm(word, one_bits, 0x7610u)), &sn, &cs);
-  const float tc = tr * cs, ts = tr * sn;
-  // Duff et al.: (b1, b2, e) orthonormal, branch-free
-  const float sg = copysignf(1.0f, e2);
-  const float A = -fdiv(1.0f, sg + e2);
-  const float B = e0 * e1 * A;
-  const float b10 = fmaf(sg * e0 * e0, A, 1.0f), b11 = sg * B, b12 = -sg * e0;
-  const float b20 = B, b21 = fmaf(e1 * e1, A, sg), b22 = -e1;
-  const float h = m - dep;
-  nx[0] = fmaf(P.Ad[0], fmaf(h, e0, fmaf(tc, b10, ts * b20)), x[0]);
-  nx[1] = fmaf(P.Ad[1], fmaf(h, e1, fmaf(tc, b11, ts * b21)), x[1]);
-  nx[2] = fmaf(P.Ad[2], fmaf(h, e2, fmaf(tc, b12, ts * b22)), x[2]);
-  return wm;
-}
+                                            unsigned one_bits, float* nx);  // below: roll3_core
 
 // 2D ball / concentric annulus on the tangent chain: the same rolling disks
 // for the outer ellipse (radius rho_b, capped so the disk also clears the
@@ -1151,9 +1107,8 @@ __device__ __forceinline__ void roll2_core(const F32Params& P, T x0, T x1, WD wo
   }
   // the centred disk is the d = 0 case: 1 / d masked once, axis (1, 0)
   const T id = vsel(use, vrsq(vmaxs(d2, 1e-30f)), 0.0f);
-  const T d = vmul(d2, id);
   const T e0 = vsel(use, vmul(w0, id), 1.0f), e1 = vmul(w1, id);
-  const T m = vsub(rho, d);
+  const T m = vfma(vneg(d2), id, rho);  // rho - d, d = d2 / sqrt(d2)
   // Moebius: psi uniform in [-pi/2, pi/2) from the low 23 bits (one LOP3)
   const T psi = vfma(vbits23(word, one_bits), kPi, -1.5f * kPi);
   T sn, cs;
@@ -1241,6 +1196,82 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
   float a0, a1;
   tang2_core<float, unsigned>(P, x[0], x[1], word, one_bits, a0, a1, n0, n1);
   return __saturatef(fminf(P.tsb[0] - a0, P.tsb[1] - a1) * P.ss_scale);
+}
+
+// ---- 3D ball on rolling balls (comment above roll_step3), one-tree form ----
+// half-words of the random word into the mantissa of 1.0f (one PRMT each)
+__device__ __forceinline__ float vhalf_hi(unsigned w, unsigned one_bits) {
+  return __uint_as_float(__byte_perm(w, one_bits, 0x7632u));
+}
+__device__ __forceinline__ float vhalf_lo(unsigned w, unsigned one_bits) {
+  return __uint_as_float(__byte_perm(w, one_bits, 0x7610u));
+}
+__device__ __forceinline__ float2 vhalf_hi(uint2 w, unsigned one_bits) {
+  return make_float2(vhalf_hi(w.x, one_bits), vhalf_hi(w.y, one_bits));
+}
+__device__ __forceinline__ float2 vhalf_lo(uint2 w, unsigned one_bits) {
+  return make_float2(vhalf_lo(w.x, one_bits), vhalf_lo(w.y, one_bits));
+}
+// sin / cos of an angle in [-pi, pi) (MUFU)
+__device__ __forceinline__ void vsincos_full(float a, float& sn, float& cs) { __sincosf(a, &sn, &cs); }
+__device__ __forceinline__ void vsincos_full(float2 a, float2& sn, float2& cs) {
+  __sincosf(a.x, &sn.x, &cs.x);
+  __sincosf(a.y, &sn.y, &cs.y);
+}
+
+template <class T, class WD>
+__device__ __forceinline__ void roll3_core(const F32Params& P, T x0, T x1, T x2, WD word,
+                                           unsigned one_bits, T& s2_out, T& n0, T& n1, T& n2) {
+  const T p0 = vmul(x0, x0), p1 = vmul(x1, x1), p2 = vmul(x2, x2);
+  const T s2 = vfma(x2, x2, vfma(x1, x1, p0));
+  s2_out = s2;
+  const T aa = vfma(p0, P.Kd[0], vfma(p1, P.Kd[1], vmul(p2, P.Kd[2])));
+  // clamped: a walk at the exact centre (x = 0) keeps finite terms
+  const T iaa = vrsq(vmaxs(aa, 1e-30f));
+  // max chain: the largest centred whitened ball, sqrt(|Ax|^2 + q) - |Ax|
+  // (roll2_core's difference form and margin)
+  const T q = vfma(s2, -1.0f, P.oR2);
+  const T rm = vfma(vfma(vneg(aa), iaa, vsqrt(vmaxs(vadd(aa, q), 0.0f))), P.keep, -P.shrink_c);
+  // rolling ball tangent at the radial projection
+  const T al = vfma(vrsq(vmaxs(s2, 1e-30f)), -P.oR, 1.0f);
+  const T be = vmul(iaa, P.rho_b);
+  const T w0 = vmul(x0, vfma(al, P.ia[0], vmul(be, P.Ad[0])));
+  const T w1 = vmul(x1, vfma(al, P.ia[1], vmul(be, P.Ad[1])));
+  const T w2 = vmul(x2, vfma(al, P.ia[2], vmul(be, P.Ad[2])));
+  const T d2 = vfma(w0, w0, vfma(w1, w1, vmul(w2, w2)));
+  const auto roll = vand(vlt(d2, P.rho_b2), vgt(vfma(al, s2, vmul(be, aa)), 0.0f));
+  const T rho = vsel(roll, P.rho_b, rm);
+  // the centred ball is the d = 0 case: 1 / d masked once, axis (0, 0, 1)
+  const T id = vsel(roll, vrsq(vmaxs(d2, 1e-30f)), 0.0f);
+  const T d = vmul(d2, id);
+  const T e0 = vmul(w0, id), e1 = vmul(w1, id), e2 = vsel(roll, vmul(w2, id), 1.0f);
+  const T m = vfma(vneg(d2), id, rho);  // rho - d
+  // V2 = 2V from the high half-word, azimuth from the low one
+  const T v2 = vadd(vfma(vhalf_hi(word, one_bits), 256.0f, -256.0f), 1.52587890625e-05f);
+  const T g = vmul(m, vrcp(vfma(d, v2, m)));
+  const T gg = vmul(g, g), tt = vmul(vfma(v2, -1.0f, 2.0f), vfma(vmul(d, 0.5f), v2, rho));
+  const T dep = vmul(gg, tt);
+  const T tr = vsqrt(vmaxs(vmul(dep, vfma(rho, 2.0f, vneg(dep))), 0.0f));
+  T sn, cs;
+  vsincos_full(vfma(vhalf_lo(word, one_bits), kAngScale, kAngBias), sn, cs);
+  const T tc = vmul(tr, cs), ts = vmul(tr, sn);
+  // Duff et al.: (b1, b2, e) orthonormal, branch-free
+  const T sg = vsign1(e2);
+  const T A = vneg(vrcp(vadd(sg, e2)));
+  const T B = vmul(vmul(e0, e1), A);
+  const T b10 = vfma(vmul(vmul(sg, e0), e0), A, 1.0f), b11 = vmul(sg, B), b12 = vneg(vmul(sg, e0));
+  const T b21 = vfma(vmul(e1, e1), A, sg), b22 = vneg(e1);
+  const T h = vfma(vneg(gg), tt, m);  // m - depth
+  n0 = vfma(vfma(h, e0, vfma(tc, b10, vmul(ts, B))), P.Ad[0], x0);
+  n1 = vfma(vfma(h, e1, vfma(tc, b11, vmul(ts, b21))), P.Ad[1], x1);
+  n2 = vfma(vfma(h, e2, vfma(tc, b12, vmul(ts, b22))), P.Ad[2], x2);
+}
+
+__device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, unsigned word,
+                                            unsigned one_bits, float* nx) {
+  float s2;
+  roll3_core<float, unsigned>(P, x[0], x[1], x[2], word, one_bits, s2, nx[0], nx[1], nx[2]);
+  return __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
 }
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>

@@ -23,6 +23,13 @@
 #ifndef EM_X2_BLOCKS
 #define EM_X2_BLOCKS 4
 #endif
+// the 3D ball's rolling-ball chain on the packed kernel (resident blocks per SM)
+#ifndef EM_X2_3D
+#define EM_X2_3D 1
+#endif
+#ifndef EM_X2_BLOCKS3
+#define EM_X2_BLOCKS3 3
+#endif
 
 namespace em {
 namespace f32 {
@@ -36,12 +43,18 @@ __device__ __forceinline__ Mask2 walking2(const F32Params& P, float2 s2) {
   return g;
 }
 
-// CH: 0 = ball, no hole; 1 = ball, one concentric hole (rolling disks); 2 =
-// box (tangent balls).  One step of both walks: candidate points and the
-// walking masks of the CURRENT points.
+// CH: 0 = 2D ball, no hole; 1 = 2D ball, one concentric hole (rolling disks);
+// 2 = 2D box (tangent balls); 3 = 3D ball, no hole (rolling balls).  One step
+// of both walks: candidate points and the walking masks of the CURRENT points.
 template <int CH>
-__device__ __forceinline__ Mask2 step2(const F32Params& P, float2 x0, float2 x1, uint2 w,
-                                       float2& n0, float2& n1) {
+__device__ __forceinline__ Mask2 step2(const F32Params& P, float2 x0, float2 x1, float2 x2,
+                                       uint2 w, float2& n0, float2& n1, float2& n2) {
+  if (CH == 3) {
+    float2 s2;
+    roll3_core<float2, uint2>(P, x0, x1, x2, w, P.one_bits, s2, n0, n1, n2);
+    return vlt(s2, P.s2_hi);
+  }
+  n2 = x2;
   if (CH == 2) {
     float2 a0, a1;
     tang2_core<float2, uint2>(P, x0, x1, w, P.one_bits, a0, a1, n0, n1);
@@ -54,7 +67,8 @@ __device__ __forceinline__ Mask2 step2(const F32Params& P, float2 x0, float2 x1,
 
 // the walking masks alone (post-batch stop test)
 template <int CH>
-__device__ __forceinline__ Mask2 walking_at(const F32Params& P, float2 x0, float2 x1) {
+__device__ __forceinline__ Mask2 walking_at(const F32Params& P, float2 x0, float2 x1, float2 x2) {
+  if (CH == 3) return vlt(vfma(x2, x2, vfma(x1, x1, vmul(x0, x0))), P.s2_hi);
   if (CH == 2) return vand(vlt(vabs(x0), P.tsb[0]), vlt(vabs(x1), P.tsb[1]));
   return walking2<CH == 1 ? 1 : 0>(P, roll2_s2(x0, x1));
 }
@@ -62,9 +76,11 @@ __device__ __forceinline__ Mask2 walking_at(const F32Params& P, float2 x0, float
 // Per-warp exit queue as four word arrays (x, y, pole, steps): a lane's two
 // walks keep each AXIS as one register pair, so a slot's (x, y) are not
 // adjacent registers and a 128-bit store would cost moves every batch.
+template <int D>
 struct ExitQueue2 {
   float x[kQueue], y[kQueue];
   int p[kQueue], s[kQueue];
+  float z[D == 3 ? kQueue : 1];
 };
 
 __device__ __forceinline__ float& comp(float2& v, int t) { return t ? v.y : v.x; }
@@ -72,21 +88,23 @@ __device__ __forceinline__ float& comp(float2& v, int t) { return t ? v.y : v.x;
 // Two walks per lane: slot t of a lane owns component t of every float2.
 // Scheduling, exit queue, binning and statistics as walk_f32_kernel (MODE 0).
 template <int CH, int BINK, int SMEM>
-__global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32Params P) {
+__global__ void __launch_bounds__(256, CH == 3 ? EM_X2_BLOCKS3 : EM_X2_BLOCKS)
+    walk_f32x2_kernel(const F32Params P) {
   const WorkOut& W = P.w;
-  constexpr int D = 2;
+  constexpr int D = CH == 3 ? 3 : 2;
   constexpr int OUTER = CH == 2 ? OUTER_BOX : OUTER_BALL;
   constexpr int NH = CH == 1 ? 1 : 0;
   constexpr bool SCALED = CH == 2;  // box axes stored scaled (to_frame)
-  __shared__ ExitQueue2 q_all[kWarps];
+  __shared__ ExitQueue2<D> q_all[kWarps];
   int lane = threadIdx.x & 31;
   unsigned eq = 1u << lane, lt = eq - 1u;
   unsigned qb = (unsigned)__cvta_generic_to_shared(&q_all[threadIdx.x >> 5]);
   asm volatile("" : "+r"(lane), "+r"(eq), "+r"(lt), "+r"(qb));
   int qn = 0;
   constexpr float kFar = 1.0e4f;
-  float2 X0 = make_float2(kFar, kFar), X1 = make_float2(kFar, kFar);  // axis 0 / 1 of both slots
-  float px = 0.0f, py = 0.0f;                      // cached pole (shared by both slots)
+  // axis 0 / 1 / 2 of both slots
+  float2 X0 = make_float2(kFar, kFar), X1 = make_float2(kFar, kFar), X2 = make_float2(kFar, kFar);
+  float px = 0.0f, py = 0.0f, pz = 0.0f;  // cached pole (shared by both slots)
   int cpole = -1;
   unsigned ccpid = 0;
   int steps[2] = {0, 0}, pole[2] = {0, 0}, rep_off[2] = {0, 0};
@@ -117,6 +135,7 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
     const float4 p = __ldg(&P.poles[bpole]);
     px = p.x;
     py = p.y;
+    pz = p.z;
     ccpid = W.pole_ids ? (unsigned)W.pole_ids[bpole] : (unsigned)bpole;
     cpole = (int)bpole;
     acc.pole = (int)bpole;
@@ -142,6 +161,8 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
             asm volatile("st.shared.f32 [%0], %1;" ::"r"(qa + kQueue * 4u), "f"(comp(X1, t)) : "memory");
             asm volatile("st.shared.s32 [%0], %1;" ::"r"(qa + kQueue * 8u), "r"(pole[t]) : "memory");
             asm volatile("st.shared.s32 [%0], %1;" ::"r"(qa + kQueue * 12u), "r"(steps[t]) : "memory");
+            if (D == 3)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(qa + kQueue * 16u), "f"(comp(X2, t)) : "memory");
           }
           qn += __popc(dm);
           if (qn >= 32) {
@@ -154,6 +175,8 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(ex[1]) : "r"(qa + kQueue * 4u) : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ep) : "r"(qa + kQueue * 8u) : "memory");
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(es) : "r"(qa + kQueue * 12u) : "memory");
+            if (D == 3)
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(ex[2]) : "r"(qa + kQueue * 16u) : "memory");
             retire<D, OUTER, NH, BINK, SMEM, SCALED>(P, ex, ep, es, acc);
             qn -= 32;
             __syncwarp();
@@ -184,11 +207,13 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
             const float4 p = __ldg(&P.poles[pole[t]]);
             px = p.x;
             py = p.y;
+            pz = p.z;
             ccpid = W.pole_ids ? (unsigned)W.pole_ids[pole[t]] : (unsigned)pole[t];
             cpole = pole[t];
           }
           comp(X0, t) = px;
           comp(X1, t) = py;
+          if (D == 3) comp(X2, t) = pz;
           cpid[t] = ccpid;
           const unsigned long long rep = (unsigned long long)W.rep_start + (unsigned)rep_off[t];
           rep_lo[t] = (unsigned)rep;
@@ -197,6 +222,7 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
           walking[t] = 1;
         } else if (!walking[t]) {
           comp(X0, t) = comp(X1, t) = kFar;  // park (walk_f32_kernel: EM_POST_STOP)
+          if (D == 3) comp(X2, t) = kFar;
         }
         live[t] = __ballot_sync(kFull, walking[t]);
       }
@@ -212,29 +238,30 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
       wv[t][2] = w.z;
       wv[t][3] = w.w;
     }
-    float2 x0 = X0, x1 = X1;
+    float2 x0 = X0, x1 = X1, x2 = X2;
     const int smax = steps[0] > steps[1] ? steps[0] : steps[1];
     if (__all_sync(kFull, smax + K <= P.max_steps)) {
       Mask2 go = {false, false};
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float2 n0, n1;
-        go = step2<CH>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), n0, n1);
+        float2 n0, n1, n2;
+        go = step2<CH>(P, x0, x1, x2, make_uint2(wv[0][k], wv[1][k]), n0, n1, n2);
         x0 = vsel(go, n0, x0);
         x1 = vsel(go, n1, x1);
+        if (D == 3) x2 = vsel(go, n2, x2);
         steps[0] += go.x;
         steps[1] += go.y;
       }
       // post-batch stop test of the landing point (walk_f32_kernel: EM_POST_STOP)
-      const Mask2 g2 = walking_at<CH>(P, x0, x1);
+      const Mask2 g2 = walking_at<CH>(P, x0, x1, x2);
       walking[0] = go.x & g2.x;
       walking[1] = go.y & g2.y;
     } else {
       int failed[2] = {0, 0};
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float2 n0, n1;
-        const Mask2 gk = step2<CH>(P, x0, x1, make_uint2(wv[0][k], wv[1][k]), n0, n1);
+        float2 n0, n1, n2;
+        const Mask2 gk = step2<CH>(P, x0, x1, x2, make_uint2(wv[0][k], wv[1][k]), n0, n1, n2);
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           const int stop = walking[t] & !(t ? gk.y : gk.x);
@@ -245,6 +272,7 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
         }
         x0 = make_float2(walking[0] ? n0.x : x0.x, walking[1] ? n0.y : x0.y);
         x1 = make_float2(walking[0] ? n1.x : x1.x, walking[1] ? n1.y : x1.y);
+        if (D == 3) x2 = make_float2(walking[0] ? n2.x : x2.x, walking[1] ? n2.y : x2.y);
       }
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
@@ -253,11 +281,9 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
           if (failed[t]) {
             atomicMax(W.err_key, ~(unsigned long long)((long long)pole[t] * W.n_rep + rep_off[t]));
             if (t == 0) {
-              x0.x = kFar;
-              x1.x = kFar;
+              x0.x = x1.x = x2.x = kFar;
             } else {
-              x0.y = kFar;
-              x1.y = kFar;
+              x0.y = x1.y = x2.y = kFar;
             }
           }
           live[t] &= ~fm;
@@ -266,11 +292,12 @@ __global__ void __launch_bounds__(256, EM_X2_BLOCKS) walk_f32x2_kernel(const F32
     }
     X0 = x0;
     X1 = x1;
+    X2 = x2;
   }
   __syncwarp();
   if (lane < qn) {  // drain the queue
-    const ExitQueue2& q = q_all[threadIdx.x >> 5];
-    const float ex[3] = {q.x[lane], q.y[lane], 0.0f};
+    const ExitQueue2<D>& q = q_all[threadIdx.x >> 5];
+    const float ex[3] = {q.x[lane], q.y[lane], D == 3 ? q.z[lane] : 0.0f};
     retire<D, OUTER, NH, BINK, SMEM, SCALED, false>(P, ex, q.p[lane], q.s[lane], acc);
   }
   if (SMEM == 2) {
@@ -324,6 +351,10 @@ static F32Kernel pick_f32x2(int ch, int bink, int smem) {
 #define EM_X2_ANY(CH_)                                                            \
   (smem == 2 ? (F32Kernel) nullptr                                                 \
              : (smem ? walk_f32x2_kernel<CH_, BIN_ANY, 1> : walk_f32x2_kernel<CH_, BIN_ANY, 0>))
+  if (ch == 3) {
+    if (bink == BIN_GRID) return EM_X2_SCHED(3, BIN_GRID);
+    return EM_X2_ANY(3);
+  }
   if (ch == 2) {
     if (bink == BIN_SQUARE) return EM_X2_SCHED(2, BIN_SQUARE);
     if (bink == BIN_GRID) return EM_X2_SCHED(2, BIN_GRID);
@@ -336,7 +367,8 @@ static F32Kernel pick_f32x2(int ch, int bink, int smem) {
 }
 
 static int x2_family(int d, int outer, int nh_mode, int chain, bool ident) {
-  if (!EM_ROLL2_GENERIC || d != 2 || chain != EM_CHAIN_TANGENT || ident) return -1;
+  if (!EM_ROLL2_GENERIC || chain != EM_CHAIN_TANGENT || ident) return -1;
+  if (d == 3) return (EM_X2_3D && outer == OUTER_BALL && nh_mode == 0) ? 3 : -1;
   if (outer == OUTER_BALL && nh_mode <= 1) return nh_mode;
   if (outer == OUTER_BOX && nh_mode == 0) return 2;
   return -1;
@@ -347,17 +379,17 @@ bool f32x2_available(int d, int outer, int nh_mode, int chain, bool ident) {
   return x2_family(d, outer, nh_mode, chain, ident) >= 0;
 }
 
-cudaError_t f32x2_blocks_per_sm(int outer, int nh_mode, int bink, int* nb) {
-  F32Kernel k = pick_f32x2(outer == OUTER_BOX ? 2 : nh_mode, bink, 0);
+cudaError_t f32x2_blocks_per_sm(int d, int outer, int nh_mode, int bink, int* nb) {
+  F32Kernel k = pick_f32x2(d == 3 ? 3 : (outer == OUTER_BOX ? 2 : nh_mode), bink, 0);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * f32::kWarps, 0);
 }
 
-cudaError_t launch_f32x2(const F32Params& P, int outer, int nh_mode, int bink, int grid,
+cudaError_t launch_f32x2(const F32Params& P, int d, int outer, int nh_mode, int bink, int grid,
                          int block, cudaStream_t s) {
   if (block != 32 * f32::kWarps) return cudaErrorInvalidConfiguration;
   const int sched = P.w.smem_stats;
-  F32Kernel k = pick_f32x2(outer == OUTER_BOX ? 2 : nh_mode, bink, sched);
+  F32Kernel k = pick_f32x2(d == 3 ? 3 : (outer == OUTER_BOX ? 2 : nh_mode), bink, sched);
   if (!k) return cudaErrorInvalidValue;
   size_t smem = 0;
   if (sched == 1) smem = (size_t)f32::kWarps * 3 * P.w.n_poles * 8;

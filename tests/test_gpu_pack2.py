@@ -74,11 +74,11 @@ def test_default_kernel_follows_job_size(B):
         assert plan.last_walks_per_lane() == 1
         plan.run(cfg.seed, 40_000)
         assert plan.last_walks_per_lane() == 2
-    cfg4 = configs.get(4).subset(8)
-    with B.Plan(B.pack_geometry(cfg4.dom), cfg4.kt.k_sqrt, cfg4.poles, cfg4.eps, 10**6,
-                B.pack_side(cfg4.fam0, 3, cfg4.eps), B.pack_side(cfg4.fam1, 3, cfg4.eps),
+    cfg5 = configs.get(5).subset(8)
+    with B.Plan(B.pack_geometry(cfg5.dom), cfg5.kt.k_sqrt, cfg5.poles, cfg5.eps, 10**6,
+                B.pack_side(cfg5.fam0, 3, cfg5.eps), B.pack_side(cfg5.fam1, 3, cfg5.eps),
                 precision="fp32") as plan:
-        assert plan.walks_per_lane() == 1  # no packed kernel for the 3D chains
+        assert plan.walks_per_lane() == 1  # no packed kernel for the L-box's table-driven chain
 
 
 @pytest.mark.parametrize("n_poles,n_rep", [(256, 100_000), (256, 3_000), (5, 77)])
@@ -91,6 +91,21 @@ def test_packed_equals_one_walk_per_lane_cfg2(B, n_poles, n_rep):
     with p2, p1:
         assert p2.walks_per_lane() == 2 and p1.walks_per_lane() == 1
         r2, r1 = p2.run(cfg.seed, n_rep), p1.run(cfg.seed, n_rep)
+    assert np.array_equal(r2.counts.sum(1), np.full(cfg.n_poles, n_rep))
+    _same(r2, r1)
+
+
+@pytest.mark.parametrize("n_poles,n_rep", [(1024, 5_000), (32, 100_000), (3, 33)])
+def test_packed_equals_one_walk_per_lane_cfg4(B, n_poles, n_rep):
+    """The 3D ball on rolling balls (roll3_core), candidate-grid binner."""
+    from paper_2409_03686_b200 import configs
+
+    cfg = configs.get(4).subset(n_poles)
+    p2, p1 = _plans(B, cfg)
+    with p2, p1:
+        assert p2.walks_per_lane() == 2 and p1.walks_per_lane() == 1
+        r2, r1 = p2.run(cfg.seed, n_rep), p1.run(cfg.seed, n_rep)
+        assert p2.last_walks_per_lane() == 2 and p1.last_walks_per_lane() == 1
     assert np.array_equal(r2.counts.sum(1), np.full(cfg.n_poles, n_rep))
     _same(r2, r1)
 
