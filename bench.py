@@ -54,9 +54,9 @@ F_STEP = {
     (2, "woe"): (15, 2), (2, "max"): (14, 2),    # max: sheared box axes
     (2, "tangent"): (37, 3),                     # tangent balls in the whitened parallelogram
     (3, "woe"): (19, 4), (3, "max"): (29, 6),    # concentric hole: shared |v|^2, |Av|^2, one rcp
-    (3, "tangent"): (49.9, 6.2),                 # one rolling / hole-tangent disk, else centred (difference form)
+    (3, "tangent"): (49.1, 6.2),                 # one rolling / hole-tangent disk, else centred (difference form)
     (4, "woe"): (22, 4), (4, "max"): (31, 6),    # balls: frame rotated onto K's eigenbasis
-    (4, "tangent"): (79.3, 8.25),                # rolling balls, else the centred ball
+    (4, "tangent"): (76.3, 8.0),                 # rolling balls, else the centred ball (difference form)
     (5, "woe"): (36, 4), (5, "max"): (41, 4),    # max: sheared box axes, world-unit notch
     (5, "tangent"): (87, 5),                     # tangent balls in 3D, notch planes as faces
 }
