@@ -190,6 +190,7 @@ struct F32Params {
   float gk[3];      // g * keep (rounded down): face gain with the relative margin folded in
   float m2;         // sigma_min(A)^2 (hole bound)
   float eps;
+  float eps2;  // eps^2 (the L-box notch stop test compares squared distances)
   float stop_scale, stop_bias;   // FFMA.SAT stop test: sat(e * scale + bias) = [e > eps]
   float oR2, s2_scale, s2_bias;  // ball: R^2 and sat(-|x|^2 s + b) = [|x|^2 < (R - eps)^2]
   float h2_scale, h2_bias;       // concentric hole: sat(|x|^2 s + b) = [|x|^2 > (rho + eps)^2]

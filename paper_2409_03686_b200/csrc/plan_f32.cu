@@ -294,6 +294,7 @@ struct F32Build {
     const double lam = sym_min_eig(g->ksqrt, d);
     P.m2 = (float)(std::max(0.0, lam) * std::max(0.0, lam) * (1.0 - 1e-4));
     P.eps = (float)eps;
+    P.eps2 = (float)((double)P.eps * (double)P.eps);
     {
       // scale = 2^k with ulp(eps_f) * 2^k >= 1: every representable e > eps
       // then gives (e - eps) * scale >= 1 (bias = -eps * scale is exact)

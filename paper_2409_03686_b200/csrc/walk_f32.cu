@@ -262,61 +262,66 @@ __global__ void __launch_bounds__(256, EM_MINB_K(D, OUTER, CHAIN)) walk_f32_kern
       // running product is needed: a stopped lane does not move, so every
       // later step of the batch recomputes the same e <= eps (and idle lanes
       // are parked outside the domain, e < 0).
-      float wm = 0.0f, sf = 0.0f;
+      if (TANG || ROLL) {
+        // tangent / rolling chains: the stop tests are compares (the same
+        // thresholds the FFMA.SAT masks encode), steps count with predicated
+        // integer adds -- as in the packed kernel (walk_f32x2.cu)
+        bool go = false;
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if (TANG || ROLL) {
+        for (int k = 0; k < K; ++k) {
           float nx[3];
-          if (ROLL && D == 3) wm = roll_step3(P, x, wv[k], P.one_bits, nx);
-          else if (ROLL) wm = roll_step2<NH>(P, x, wv[k], P.one_bits, nx);
-          else if (D == 2) wm = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
-          else wm = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
-          const bool go = wm != 0.0f;
+          if (ROLL && D == 3) go = roll3_go(P, x, wv[k], P.one_bits, nx);
+          else if (ROLL) go = roll2_go<NH>(P, x, wv[k], P.one_bits, nx);
+          else if (D == 2) go = tang2_go(P, x, wv[k], P.one_bits, nx);
+          else go = tang3_go<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
 #pragma unroll
           for (int l = 0; l < D; ++l) x[l] = go ? nx[l] : x[l];
-        } else {
+          steps += go;
+        }
+        walking = go;
+        if (EM_POST_STOP) {
+          // the stop test of the point the last move landed on (the next
+          // batch's first test, evaluated now): a walk that reached the shell
+          // on a batch's last step retires at this service pass instead of
+          // idling through one more batch (cfg2-cfg5 +9-12%).  Only the
+          // predicate of the step functions is live here (the rest is dead
+          // code); a lane left without work is parked far outside (service).
+          float nx[3];
+          bool g2;
+          if (ROLL && D == 3) g2 = roll3_go(P, x, 0u, P.one_bits, nx);
+          else if (ROLL) g2 = roll2_go<NH>(P, x, 0u, P.one_bits, nx);
+          else if (D == 2) g2 = tang2_go(P, x, 0u, P.one_bits, nx);
+          else g2 = tang3_go<OUTER>(P, ttab, x, 0u, P.one_bits, nx);
+          walking &= g2;
+        }
+      } else {
+        float wm = 0.0f, sf = 0.0f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
           float t, r;
           dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
           wm = t;  // already the saturated 0/1 mask
           step<D, OUTER, IDENT, SHEAR>(P, x, r * wm, D == 3 ? z_of<D>(wv, k, P.one_bits) : 0.0f,
                                        angle_bits<D>(wv, k, P.one_bits));
+          sf += wm;
         }
-        sf += wm;
-      }
-      walking = wm != 0.0f;
-      steps += (int)sf;
-      if (EM_POST_STOP) {
-        // the stop test of the point the last move landed on (the next
-        // batch's first test, evaluated now): a walk that reached the shell
-        // on a batch's last step retires at this service pass instead of
-        // idling through one more batch (cfg2-cfg5 +9-12%).  Only the stop
-        // mask of the step functions is live here (the rest is dead code).
-        // Same criterion, same moves and draws; the two evaluations of the
-        // test may round apart on a point at the shell's edge (separately
-        // scheduled FMA chains), so such a walk can end one step earlier --
-        // and a lane left without work is parked far outside (service).
-        float t2;
-        if (TANG || ROLL) {
-          float nx[3];
-          if (ROLL && D == 3) t2 = roll_step3(P, x, 0u, P.one_bits, nx);
-          else if (ROLL) t2 = roll_step2<NH>(P, x, 0u, P.one_bits, nx);
-          else if (D == 2) t2 = tangent_step(P, x, 0u, P.one_bits, nx[0], nx[1]);
-          else t2 = tangent_step3<OUTER>(P, ttab, x, 0u, P.one_bits, nx);
-        } else {
-          float r2;
+        walking = wm != 0.0f;
+        steps += (int)sf;
+        if (EM_POST_STOP) {
+          float t2, r2;
           dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t2, r2);
+          walking &= t2 != 0.0f;
         }
-        walking &= t2 != 0.0f;
       }
     } else {
       int failed = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        float t, r, nx[3] = {0.0f, 0.0f, 0.0f};
-        if (ROLL && D == 3) t = roll_step3(P, x, wv[k], P.one_bits, nx);
-        else if (ROLL) t = roll_step2<NH>(P, x, wv[k], P.one_bits, nx);
-        else if (TANG && D == 2) t = tangent_step(P, x, wv[k], P.one_bits, nx[0], nx[1]);
-        else if (TANG) t = tangent_step3<OUTER>(P, ttab, x, wv[k], P.one_bits, nx);
+        float t = 0.0f, r, nx[3] = {0.0f, 0.0f, 0.0f};
+        if (ROLL && D == 3) t = roll3_go(P, x, wv[k], P.one_bits, nx) ? 1.0f : 0.0f;
+        else if (ROLL) t = roll2_go<NH>(P, x, wv[k], P.one_bits, nx) ? 1.0f : 0.0f;
+        else if (TANG && D == 2) t = tang2_go(P, x, wv[k], P.one_bits, nx) ? 1.0f : 0.0f;
+        else if (TANG) t = tang3_go<OUTER>(P, ttab, x, wv[k], P.one_bits, nx) ? 1.0f : 0.0f;
         else dist<D, OUTER, NH, CHAIN, IDENT>(P, x, t, r);
         const int stop = walking & (t <= 0.0f);
         const int over = walking & (stop ^ 1) & (steps >= P.max_steps);

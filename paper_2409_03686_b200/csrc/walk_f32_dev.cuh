@@ -729,12 +729,15 @@ __device__ __forceinline__ float tangent_step(const F32Params& P, const float* x
 // sqrt(dep (2 rho - dep)) along a uniform azimuth.  V and the azimuth take
 // 16 bits each of one 32-bit word: 2^32 cells of equal harmonic measure
 // (the midpoint rule of the 3D directions).
+// Returns the walking predicate of x (the stop tests as compares: every face
+// margin positive, and for the L-box the squared Euclidean distance to the
+// notch prism above eps^2 -- no root).
 template <int OUTER>
-__device__ __forceinline__ float tangent_step3(const F32Params& P, const float* tab, const float* x,
-                                               unsigned word, unsigned one_bits, float* nx) {
+__device__ __forceinline__ bool tang3_go(const F32Params& P, const float* tab, const float* x,
+                                         unsigned word, unsigned one_bits, float* nx) {
   const float a0 = fabsf(x[0]), a1 = fabsf(x[1]), a2 = fabsf(x[2]);
   const float m0 = P.tbt[0] - a0, m1 = P.tbt[1] - a1, m2 = P.tbt[2] - a2;
-  float wm = __saturatef(fminf(fminf(P.tsb[0] - a0, P.tsb[1] - a1), P.tsb[2] - a2) * P.ss_scale);
+  bool go = (a0 < P.tsb[0]) & (a1 < P.tsb[1]) & (a2 < P.tsb[2]);
   // nearest face as a running argmin carrying the face's coordinate and the
   // offset of its constant row (selects only, no index arithmetic)
   float m = m0, xi = x[0];
@@ -757,8 +760,7 @@ __device__ __forceinline__ float tangent_step3(const F32Params& P, const float* 
     // Euclidean distance to the notch prism (world units) for the stop test
     const float qx = fmaf(-P.ax[0], x[0], P.notch[0]), qy = fmaf(-P.ax[1], x[1], P.notch[1]);
     const float ex = fmaxf(qx, 0.0f), ey = fmaxf(qy, 0.0f);
-    const float en = fsqrt(fmaf(ex, ex, ey * ey));
-    wm = fminf(wm, __saturatef(fmaf(en, P.stop_scale, P.stop_bias)));
+    go &= fmaf(ex, ex, ey * ey) > P.eps2;
     const float d0 = P.tn[0] - x[0], d1 = P.tn[1] - x[1];
     const float dn = fmaxf(d0, d1);
     notch = dn < m;
@@ -796,7 +798,14 @@ __device__ __forceinline__ float tangent_step3(const F32Params& P, const float* 
   const float tc = tr * cs, ts = tr * sn;
 #pragma unroll
   for (int l = 0; l < 3; ++l) nx[l] = sg * fmaf(ts, P2[l], fmaf(tc, P1[l], fmaf(-dep, C[l], F[l])));
-  return wm;
+  return go;
+}
+
+// the same step with the walking mask as a 0/1 float (em_debug_step)
+template <int OUTER>
+__device__ __forceinline__ float tangent_step3(const F32Params& P, const float* tab, const float* x,
+                                               unsigned word, unsigned one_bits, float* nx) {
+  return tang3_go<OUTER>(P, tab, x, word, one_bits, nx) ? 1.0f : 0.0f;
 }
 
 // 3D ball on the tangent chain: walk on ROLLING balls.  In whitened
@@ -1272,6 +1281,33 @@ __device__ __forceinline__ float roll_step3(const F32Params& P, const float* x, 
   float s2;
   roll3_core<float, unsigned>(P, x[0], x[1], x[2], word, one_bits, s2, nx[0], nx[1], nx[2]);
   return __saturatef(fmaf(s2, -P.s2_scale, P.s2_bias));
+}
+
+// ---- walking predicates of the tangent / rolling chains (one-walk kernel) ----
+// The stop tests as compares on the same thresholds the FFMA.SAT masks encode
+// (s2_lo < |x|^2 < s2_hi; |xt_i| < tsb_i), as in the packed kernel.
+template <int NH>
+__device__ __forceinline__ bool roll2_go(const F32Params& P, const float* x, unsigned word,
+                                         unsigned one_bits, float* nx) {
+#if EM_ROLL2_GENERIC
+  float s2;
+  roll2_core<NH, float, unsigned>(P, x[0], x[1], word, one_bits, s2, nx[0], nx[1]);
+  return NH == 1 ? (s2 < P.s2_hi) & (s2 > P.s2_lo) : s2 < P.s2_hi;
+#else
+  return roll_step2_legacy<NH>(P, x, word, one_bits, nx) != 0.0f;
+#endif
+}
+__device__ __forceinline__ bool roll3_go(const F32Params& P, const float* x, unsigned word,
+                                         unsigned one_bits, float* nx) {
+  float s2;
+  roll3_core<float, unsigned>(P, x[0], x[1], x[2], word, one_bits, s2, nx[0], nx[1], nx[2]);
+  return s2 < P.s2_hi;
+}
+__device__ __forceinline__ bool tang2_go(const F32Params& P, const float* x, unsigned word,
+                                         unsigned one_bits, float* nx) {
+  float a0, a1;
+  tang2_core<float, unsigned>(P, x[0], x[1], word, one_bits, a0, a1, nx[0], nx[1]);
+  return (a0 < P.tsb[0]) & (a1 < P.tsb[1]);
 }
 
 template <int D, int OUTER, int NH, int CHAIN, bool IDENT>
