@@ -1,3 +1,8 @@
+// roll2_core<1, float> against roll2_core<1, float2> on 2.1e6 random pairs of annulus points:
+// bit-identical (0 mismatches) once no add takes a bare product (see walk_f32_dev.cuh).
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a --extended-lambda -std=c++17 \
+//     -I paper_2409_03686_b200/csrc -I include -fmad=true -prec-sqrt=false -prec-div=false \
+//     -DEM_TANG_K=4 -DEM_ROLL2_ONE=1 -DEM_ROLL2_DYN=0 -o variants/core_eq tools/diag/core_eq.cu
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>

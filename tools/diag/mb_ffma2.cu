@@ -1,3 +1,5 @@
+// FFMA2 vs FFMA throughput, alone and with ALU-pipe work (B200):
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o variants/mb tools/diag/mb_ffma2.cu && gpurun -- ./variants/mb
 #include <cstdio>
 #include <cuda_runtime.h>
 // issue-rate microbenchmarks: FFMA vs FFMA2, alone and mixed with ALU-pipe work

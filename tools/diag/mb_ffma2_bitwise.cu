@@ -1,3 +1,6 @@
+// __ffma2_rn / __fmul2_rn / __fadd2_rn against the scalar _rn operations on 8.4e6 random
+// pairs (any bit pattern, denormals, values near 1): 0 mismatches on the B200.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a --extended-lambda -o variants/eq tools/diag/mb_ffma2_bitwise.cu
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
