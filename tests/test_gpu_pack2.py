@@ -218,3 +218,75 @@ def test_packed_disc_without_hole_equals_one_walk_per_lane(B):
     assert out[0][1] == 2 and out[1][1] == 1
     assert np.array_equal(out[0][0].counts.sum(1), np.full(48, 50_000))
     _same(out[0][0], out[1][0])
+
+
+def _strong_anisotropy_case(name):
+    """Rolling-chain geometries with strongly anisotropic K (the difference-form
+    centred radius with 1 / m2 up to 5 and |A| up to 5.5, rolling radii far
+    below the hole-tangent one, eigenvalues below 1)."""
+    from paper_2409_03686_b200.conductivity import make_tensor
+    from paper_2409_03686_b200.geometry import (Ball, Domain, circle_points, fibonacci_sphere,
+                                                generic_points)
+
+    if name == "annulus30":
+        c, s = np.cos(0.4), np.sin(0.4)
+        rot = np.array([[c, -s], [s, c]])
+        dom = Domain(2, Ball(np.zeros(2), 1.0), (Ball(np.zeros(2), 0.4),), frozenset({0}))
+        kt = make_tensor(rot @ np.diag([1.0, 30.0]) @ rot.T)
+        f0 = circle_points(np.zeros(2), 1.0, 96, component=0)
+        f1 = circle_points(np.zeros(2), 0.4, 48, component=1)
+        poles = np.array([[0.7, 0.1], [-0.2, 0.55], [0.05, -0.9], [-0.45, -0.1]])
+        return dom, kt, f0, f1, poles
+    if name == "disc_small_eig":
+        dom = Domain(2, Ball(np.array([0.3, -0.2]), 0.8), (), frozenset())
+        kt = make_tensor(np.array([[0.2, 0.0], [0.0, 6.0]]))
+        f1 = circle_points(np.array([0.3, -0.2]), 0.8, 64, component=0, phase=0.5)
+        poles = np.array([[0.3, -0.2], [0.8, 0.1], [0.2, 0.45]])
+        return dom, kt, None, f1, poles
+    dom = Domain(3, Ball(np.zeros(3), 1.0), (), frozenset())
+    kt = make_tensor(np.diag([0.3, 1.0, 9.0]))
+    f1 = generic_points(fibonacci_sphere(120, 1.0), component=0)
+    poles = np.array([[0.0, 0.0, 0.0], [0.6, -0.3, 0.2], [-0.1, 0.2, -0.85]])
+    return dom, kt, None, f1, poles
+
+
+@pytest.mark.parametrize("name", ["annulus30", "disc_small_eig", "ball9"])
+def test_packed_rolling_chains_strong_anisotropy_vs_oracle(B, oracle, name):
+    """The packed kernel on strongly anisotropic rolling-chain geometries:
+    equal to the one-walk kernel bit for bit, and statistically equal to the
+    oracle's FP64 reference chain (entry-wise exact binomial tests at
+    family-wise level 1e-4, row chi^2 homogeneity)."""
+    from helpers import P_Z4, exact_two_sample_p, exceed_quantile, row_chi2_pvalues
+    from paper_2409_03686_b200 import _native
+
+    dom, kt, f0, f1, poles = _strong_anisotropy_case(name)
+    d = poles.shape[1]
+    eps = 1e-5
+    geom = B.pack_geometry(dom)
+    s0, s1 = B.pack_side(f0, d, eps), B.pack_side(f1, d, eps)
+    n_gpu, n_ref = 400_000, 20_000
+    res = []
+    for fl in (_native.EM_FLAG_TWO_WALKS_PER_LANE, _native.EM_FLAG_ONE_WALK_PER_LANE):
+        with B.Plan(geom, kt.k_sqrt, poles, eps, 10**6, s0, s1, precision="fp32", flags=fl) as plan:
+            assert plan.chain == "tangent"
+            res.append((plan.run(77, n_gpu), plan.last_walks_per_lane()))
+    assert res[0][1] == 2 and res[1][1] == 1
+    _same(res[0][0], res[1][0])
+    r = res[0][0]
+    assert np.array_equal(r.counts.sum(1), np.full(len(poles), n_gpu))
+
+    def generic(sd):  # brute-force Voronoi blocks: the oracle's exact binning
+        return (sd.anchors, np.array([[0, 0, sd.size]]), np.zeros((1, 4)))
+
+    raw0, raw1, *_ = oracle.run_accumulate_packed(geom.gi, geom.gf, geom.comp_side, kt.k_sqrt, poles,
+                                                  5, eps, 10**6, n_ref, generic(s0), generic(s1))
+    ref = np.concatenate([raw0, raw1], axis=1)
+    p = exact_two_sample_p(r.counts, n_gpu, ref, n_ref)
+    m = p.size
+    worst = np.unravel_index(p.argmin(), p.shape)
+    assert p.min() >= 1e-4 / m, (p.min(), worst, r.counts[worst], ref[worst])
+    assert int((p < P_Z4).sum()) <= exceed_quantile(m, q=0.99999)
+    rows = row_chi2_pvalues(r.counts, n_gpu, ref, n_ref)
+    assert rows.min() > 1e-5 / len(rows), rows.min()
+    # the tangent chain engaged: far fewer steps than the reference chain's
+    assert r.steps_sum.sum() / (len(poles) * n_gpu) < 14
